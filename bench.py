@@ -1,0 +1,298 @@
+"""Benchmark of the hot path: BASELINE.json configs[1] (c1) -- one batched
+preconditioner apply A^{-1} on 5 independent 1023 x 1023 fp64 Dirichlet
+rectangles (DST-I -> Thomas -> DST-I), kappa = 0, RHS uniform[-1,1] from
+default_rng(0).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+One JSON line on rank 0.  `value` = grid points solved per second over all
+ranks (weak scaling: every rank solves its own batch of 5; no data-path
+collective), inputs resident in HBM, 8 rotating buffer sets (670 MB > the
+126 MB L2) so every step reads and writes HBM.  `e2e` = the same solve through
+the public C-ABI entry point with pinned host buffers: H2D of the RHS and D2H
+of the solution inside the timed region.  `roofline` uses the 32 B/point
+algorithmic traffic of a separable transform solve.
+`--impl reference` times the CPU restatement of the reference solver
+(oracle/, numpy pocketfft + Thomas loops, one thread per subdomain like the
+reference's thread pool) on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_SIDE, COUNT, KAPPA = 1023, 5, 0.0
+POINTS = COUNT * N_SIDE * N_SIDE
+B_ALG = 32.0                      # algorithmic bytes per grid point per apply
+METRIC = "grid points solved/sec (fp64, 1e-10 res); precond-apply HBM GB/s vs peak"
+WORKLOAD = "c1: batched precond apply, 5 x 1023^2 fp64 Dirichlet, kappa=0, DST-I->Thomas->DST-I"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_rhs():
+    rng = np.random.default_rng(0)
+    return [rng.uniform(-1.0, 1.0, N_SIDE * N_SIDE) for _ in range(COUNT)]
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference(steps: int, warmup: int, sample_subdomains: int = COUNT, max_seconds: float = 20.0):
+    """Reference CPU solver (oracle restatement) on this host: each step solves
+    `sample_subdomains` 1023^2 rectangles, one thread per subdomain like the
+    reference's ThreadPoolExecutor (ddm.py:204-207).  Returns (pts/s, cores, sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from concurrent.futures import ThreadPoolExecutor
+
+    import fftddm_oracle as O
+    from paper_2509_23180_b200 import configs
+
+    subs = configs.batch_rects(N_SIDE, sample_subdomains, KAPPA)
+    f = make_rhs()[:sample_subdomains]
+    plans = [O.plan(s) for s in subs]
+    cores = min(sample_subdomains, len(os.sched_getaffinity(0)))
+    pool = ThreadPoolExecutor(max_workers=cores)
+    run = lambda: list(pool.map(lambda a: O.solve(*a), zip(plans, f)))  # noqa: E731
+    for _ in range(warmup):
+        run()
+    times = []
+    t_start = time.perf_counter()
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > max_seconds:
+            break
+    pool.shutdown()
+    per = statistics.median(times)
+    pts = sample_subdomains * N_SIDE * N_SIDE
+    return pts / per, cores, (f"{len(times)} timed steps x {sample_subdomains} x 1023^2 solves "
+                              f"(median step {per:.3f} s), {cores} threads")
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    value, cores, sample = cpu_reference(args.steps, min(args.warmup, 1))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "grid_points/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": POINTS / value * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform[-1,1], seed 0)",
+            "config": {"workload": WORKLOAD, "points_per_step": POINTS},
+            "cpu_baseline": {"value": value, "unit": "grid_points/s", "cores": cores,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "grid_points/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_23180_b200 import _native, configs, rectsolver
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    subs = configs.batch_rects(N_SIDE, COUNT, KAPPA)
+    plans = [rectsolver.plan_rect(s) for s in subs]
+    rhs = make_rhs()
+    SETS = 8
+    fin = [[torch.as_tensor(r, device=dev) for r in rhs] for _ in range(SETS)]
+    out = [[torch.empty_like(x) for x in s] for s in fin]
+    hp = _native.ptr_array([p.handle.ptr for p in plans])
+    fps = [_native.ptr_array([_native.dptr(x) for x in s]) for s in fin]
+    ops = [_native.ptr_array([_native.dptr(x) for x in s]) for s in out]
+    lib = _native.lib()
+    stream = torch.cuda.current_stream()
+    sp = _native.P(stream.cuda_stream)
+
+    def apply(i):
+        st = lib.fd_rect_solve_batched(COUNT, hp, fps[i % SETS], ops[i % SETS], sp)
+        if st:
+            _native.check(st)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(max(args.warmup, 3)):
+        apply(i)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for i in range(args.steps):
+            apply(i)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = POINTS * world / (ms * 1e-3)
+
+    # correctness spot check of the timed buffers against the plan's residual
+    chk = rectsolver.apply_rect_operator(subs[0], out[(args.steps - 1) % SETS][0])
+    resid = float(torch.linalg.norm(chk - fin[0][0]) / torch.linalg.norm(fin[0][0]))
+
+    # end to end through the C ABI: pinned host RHS -> device -> solve -> host
+    hin = [torch.from_numpy(r).pin_memory() for r in rhs]
+    hout = [torch.empty(r.shape, dtype=torch.float64).pin_memory() for r in rhs]
+    din, dout = fin[0], out[0]
+
+    def e2e_step():
+        for h, d in zip(hin, din):
+            d.copy_(h, non_blocking=True)
+        apply(0)
+        for h, d in zip(hout, dout):
+            h.copy_(d, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_steps = max(3, min(args.steps, 20))
+    e0.record(stream)
+    for _ in range(e_steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e_ms = e0.elapsed_time(e1) / e_steps
+    if world > 1:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e_value = POINTS * world / (e_ms * 1e-3)
+    io_bytes = sum(r.nbytes for r in rhs)
+
+    peak, peak_kind = peaks()
+    achieved = B_ALG * POINTS / (ms * 1e-3) / 1e9
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            v, cores, sample = cpu_reference(steps=8, warmup=1, max_seconds=15.0)
+            cpu = {"value": v, "unit": "grid_points/s", "cores": cores, "kind": "port",
+                   "sample": sample}
+        line = {"metric": METRIC, "value": value, "unit": "grid_points/s", "n_gpus": world,
+                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (uniform[-1,1], seed 0; BASELINE config 1)",
+                "config": {"workload": WORKLOAD, "points_per_step": POINTS,
+                           "batch": COUNT, "n": N_SIDE, "kappa": KAPPA,
+                           "l2_policy": f"{SETS} rotating buffer sets = "
+                                        f"{SETS * 2 * io_bytes / 1e6:.0f} MB > 126 MB L2",
+                           "parallelism": f"replicas x{world} (independent batches, no collective)"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None,
+                             "peak_kind": peak_kind,
+                             "algorithmic_bytes_per_point": B_ALG,
+                             "kernel": "fused precond apply (pass1 + carry + pass2)"},
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": "grid_points/s",
+                        "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
+                        "ms_per_step": e_ms},
+                "gpu_launches": 3 * args.steps,
+                "clocks": clk.summary(),
+                "check": {"rel_residual_Ap_minus_f": resid}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_gpu(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/*
+ * fftddm_b200.h -- C ABI of the B200-native hot path of the FFT-preconditioned
+ * Schur/GMRES solver (arXiv 2509.23180, reference package `fftddm`).
+ *
+ * Plain C types only: sizes are ints, fields are fp64 DEVICE pointers in the
+ * x-line-major layout of the reference (node (i,j) at (i-1)*n + (j-1),
+ * fftddm/geometry.py:3-8,142-148), streams are `cudaStream_t` passed as void*.
+ * Every entry point returns an FD_* status; on failure fd_last_error() holds a
+ * thread-local message.  The Python shim (paper_2509_23180_b200/_native.py)
+ * maps the codes onto the reference's exception classes
+ * (fftddm/errors.py:1-24).
+ *
+ * Ownership: the caller owns every field buffer it passes; the library owns the
+ * opaque handles (plans, Schur operators, GMRES workspace incl. the Krylov
+ * basis) from *_create to *_destroy.  No hidden host<->device copies happen in
+ * the solve/apply calls.  One handle is used by one stream at a time.
+ */
+#ifndef FFTDDM_B200_H
+#define FFTDDM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* status codes ------------------------------------------------------------- */
+#define FD_OK 0
+#define FD_ERR_VALIDATION 1     /* ValidationError / ValueError (shape, ids)   */
+#define FD_ERR_SINGULAR 2       /* SingularOperatorError (rectsolver.py:156-163) */
+#define FD_ERR_NOT_CONVERGED 3  /* ConvergenceError (krylov.py:156-165)         */
+#define FD_ERR_CUDA 4           /* CUDA runtime failure                        */
+#define FD_ERR_UNSUPPORTED 5    /* outside the GPU path's scope (NN/PP axes)   */
+
+typedef struct fd_plan_s *fd_plan;
+typedef struct fd_schur_s *fd_schur;
+
+/* GMRES report; replaces krylov.SolveReport (krylov.py:52-58). */
+typedef struct {
+    int converged;
+    int iterations;
+    int restarts;          /* restart cycles run                               */
+    int hist_len;          /* entries written to the caller's history buffer   */
+    double wall_time;      /* seconds, host clock around the device loop       */
+    double true_residual;  /* ||rhs - op(x)||, or the solve_coupled residual   */
+} fd_report;
+
+const char *fd_last_error(void);
+int fd_version(void);
+
+/* --- rectangle plan: replaces rectsolver.plan_rect (rectsolver.py:94-180) ---
+ * DD transform along y (the contiguous axis), per-end diagonal modifiers on
+ * the sweep axis (end_modifier west/east, geometry.py:118-128).  Builds the
+ * eigenvalues (transforms.py:26-31), the per-mode LU of the sweep system with
+ * the reference's recurrence (rectsolver.py:62-77) and the block-carry tables
+ * of the two-pass Thomas solve.  FD_ERR_SINGULAR on a zero pivot. */
+int fd_plan_create(fd_plan *out, int m, int n, double dx, double dy, double kappa,
+                   double mod_west, double mod_east, int device);
+int fd_plan_destroy(fd_plan plan);
+/* rows per carry block, explicit factor rows, transform kind (0 dense, 1 fft) */
+int fd_plan_info(fd_plan plan, int *block_rows, long long *explicit_rows, int *transform);
+
+/* Host-only restatement of the factor tables for testing without a GPU:
+ * writes the full (m, n) beta and lower arrays rebuilt from the compressed
+ * per-mode tables the device uses. */
+int fd_factor_tables_host(int m, int n, double dx, double dy, double kappa,
+                          double mod_west, double mod_east, double *beta, double *lower);
+
+/* --- rectangle solve: replaces rectsolver.solve_rect (rectsolver.py:183-213)
+ * out = A^{-1} f.  f and out may alias.  Batched form solves `count`
+ * independent rectangles in one pipeline (DST-I -> Thomas -> DST-I). */
+int fd_rect_solve(fd_plan plan, const double *f, double *out, void *stream);
+int fd_rect_solve_batched(int count, const fd_plan *plans, const double *const *f,
+                          double *const *out, void *stream);
+
+/* --- transforms.apply_Q / apply_Qt for the DD pair (transforms.py:106-136):
+ * out[r, :] = sqrt(2/(n+1)) DST-I(in[r, :]), rows x n, may alias. */
+int fd_dst_rows(int rows, int n, const double *in, double *out, int device, void *stream);
+
+/* --- rectsolver.apply_rect_operator (rectsolver.py:264-289), non-periodic:
+ * out = 5-point stencil of v on an m x n grid, delta = 1/h^2, end modifiers
+ * mod_* on the four boundary-adjacent lines (geometry.py:118-128). */
+int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa,
+                     double mod_west, double mod_east, double mod_south, double mod_north,
+                     const double *v, double *out, void *stream);
+
+/* --- ddm.build_schur_operator (ddm.py:182-201).  For neighbour i:
+ * to_center maps its line into the centre  (R_ci, ddm.py:85),
+ * from_center maps the centre line into it (R_ic, ddm.py:86).
+ * Index arrays are HOST int64 of length line_len[i]; they are copied. */
+int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south,
+                    double center_mod_north, int n_nb, const fd_plan *nb,
+                    const int *line_len,
+                    const int64_t *const *to_c_from, const int64_t *const *to_c_to,
+                    const double *to_c_coupling,
+                    const int64_t *const *from_c_from, const int64_t *const *from_c_to,
+                    const double *from_c_coupling);
+int fd_schur_destroy(fd_schur op);
+/* SchurOperator.schur / center_solve / preconditioned / unpreconditioned
+ * (ddm.py:112-136); p, out are centre-sized device vectors, may not alias. */
+int fd_schur_apply(fd_schur op, const double *p, double *out, void *stream);
+int fd_center_solve(fd_schur op, const double *r, double *out, void *stream);
+int fd_precond_apply(fd_schur op, const double *p, double *out, void *stream);
+int fd_unprecond_apply(fd_schur op, const double *p, double *out, void *stream);
+
+/* --- krylov.gmres(op.preconditioned, rhs) (krylov.py:61-165), x0 = 0 when
+ * x_is_zero, else x holds x0.  history (host, capacity hist_cap) receives
+ * |g_{k+1}|/||r0|| per step with the reference's final overwrite.
+ * FD_ERR_NOT_CONVERGED leaves the last iterate in x and fills *rep. */
+int fd_gmres_precond(fd_schur op, const double *rhs, double *x, int x_is_zero,
+                     int m, double tol, int max_restarts, double *history,
+                     int hist_cap, fd_report *rep, void *stream);
+
+/* --- ddm.ddm_solve for a star composite (ddm.py:210-270 with
+ * krylov.solve_coupled's fft branch, krylov.py:168-195): f_center/f_nb are
+ * device right-hand sides, p_center/p_nb receive the solution. */
+int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
+                 double *p_center, double *const *p_nb, int m, double tol,
+                 int max_restarts, double *history, int hist_cap, fd_report *rep,
+                 void *stream);
+
+/* --- Arnoldi building blocks (krylov.py:105-111,141) for GMRES driven by a
+ * caller-supplied operator.  V is a device array of >= k+2 rows of length N
+ * (row stride N).  fd_arnoldi_step: MGS of w against V[0..k], writes
+ * h[0..k+1] (host) and *w_norm (||w|| before orthogonalisation) and leaves the
+ * orthogonalised w in place (not normalised). */
+int fd_arnoldi_step(int N, int k, const double *V, double *w, double *h,
+                    double *w_norm, void *stream);
+/* x += V[0..k-1]^T y  (y host, length k) */
+int fd_basis_update(int N, int k, const double *V, const double *y, double *x, void *stream);
+/* out = a * x (+ b * y if y) ; y may be NULL */
+int fd_axpby(int N, double a, const double *x, double b, const double *y, double *out,
+             void *stream);
+/* host result: ||x||_2 with the library's deterministic reduction order */
+int fd_norm(int N, const double *x, double *result, void *stream);
+int fd_dot(int N, const double *x, const double *y, double *result, void *stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFTDDM_B200_H */

@@ -1,0 +1,612 @@
+// Host orchestration + C ABI: Schur operator (ddm.py:94-136), restarted GMRES
+// with device-resident Krylov basis (krylov.py:61-165), Algorithm 1
+// (ddm.py:210-270).  Scalars of the Hessenberg/Givens recurrences live on the
+// host in fp64 with -ffp-contract=off, so the least-squares arithmetic rounds
+// like the reference's numpy scalars; every vector-sized operation runs in a
+// kernel on the caller's stream.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <chrono>
+#include <map>
+#include <mutex>
+#include <sstream>
+
+#include "fd_internal.h"
+
+namespace fd {
+
+Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
+                  int device);
+void plan_destroy(Plan *p);
+void factor_tables_host(int m, int n, double dx, double dy, double kappa, double mod_w,
+                        double mod_e, double *beta, double *lower);
+
+static thread_local std::string g_last_error;
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+// ---------------------------------------------------------------------------
+// per-device scratch for reductions (used by the generic Arnoldi entry points)
+struct Scratch {
+    RedWork red;
+    double *dval;      // device scalars
+    double *hval;      // pinned host mirror
+    int cap;
+};
+static Scratch make_scratch(int cap) {
+    Scratch s{};
+    FD_CUDA(cudaMalloc(&s.red.partials, sizeof(double) * kRedBlocks));
+    FD_CUDA(cudaMalloc(&s.red.counter, sizeof(unsigned int)));
+    FD_CUDA(cudaMemset(s.red.counter, 0, sizeof(unsigned int)));
+    FD_CUDA(cudaMalloc(&s.dval, sizeof(double) * cap));
+    FD_CUDA(cudaMallocHost(&s.hval, sizeof(double) * cap));
+    s.cap = cap;
+    return s;
+}
+static void free_scratch(Scratch &s) {
+    cudaFree(s.red.partials);
+    cudaFree(s.red.counter);
+    cudaFree(s.dval);
+    cudaFreeHost(s.hval);
+}
+static std::mutex g_scr_mu;
+static std::map<int, Scratch> g_scratch;
+static Scratch &device_scratch() {
+    int dev = 0;
+    FD_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(g_scr_mu);
+    auto it = g_scratch.find(dev);
+    if (it == g_scratch.end()) it = g_scratch.emplace(dev, make_scratch(1024)).first;
+    return it->second;
+}
+
+// ---------------------------------------------------------------------------
+// Arnoldi step (krylov.py:105-111): w_norm = ||w||; MGS against V[0..k];
+// h[0..k] projections, h[k+1] = ||w|| after.  h, w_norm are host outputs.
+static void arnoldi_step(long long N, int k, const double *V, double *w, double *h, double *w_norm,
+                         Scratch &sc, cudaStream_t s) {
+    if (k + 3 > sc.cap) FD_FAIL(FD_ERR_VALIDATION, "arnoldi: restart length too large");
+    double *d = sc.dval;   // d[0] = ||w||^2, d[1..k+1] = h_0..h_k, d[k+2] = ||w_orth||^2
+    launch_dot(N, w, w, d, sc.red, s);
+    for (int i = 0; i <= k; ++i)
+        launch_mgs(N, w, i ? V + (long long)(i - 1) * N : nullptr, i ? d + i : nullptr,
+                   V + (long long)i * N, d + 1 + i, sc.red, s);
+    launch_mgs(N, w, V + (long long)k * N, d + 1 + k, nullptr, d + k + 2, sc.red, s);
+    FD_CUDA(cudaMemcpyAsync(sc.hval, d, sizeof(double) * (k + 3), cudaMemcpyDeviceToHost, s));
+    FD_CUDA(cudaStreamSynchronize(s));
+    *w_norm = sqrt(sc.hval[0]);
+    for (int i = 0; i <= k; ++i) h[i] = sc.hval[1 + i];
+    h[k + 1] = sqrt(sc.hval[k + 2]);
+}
+
+static double norm2(long long N, const double *x, Scratch &sc, cudaStream_t s) {
+    launch_dot(N, x, x, sc.dval, sc.red, s);
+    FD_CUDA(cudaMemcpyAsync(sc.hval, sc.dval, sizeof(double), cudaMemcpyDeviceToHost, s));
+    FD_CUDA(cudaStreamSynchronize(s));
+    return sqrt(sc.hval[0]);
+}
+
+// ---------------------------------------------------------------------------
+// Schur operator
+struct Coupling {
+    int len;
+    int64_t *from, *to;   // device
+    double c;
+};
+
+}  // namespace fd
+
+struct fd_plan_s {
+    fd::Plan *p;
+};
+
+struct fd_schur_s {
+    int device;
+    fd::Plan *center;
+    double mod_s, mod_n;
+    std::vector<fd::Plan *> nb;
+    std::vector<fd::Coupling> to_c, from_c;   // R_ci, R_ic per neighbour
+    std::vector<double *> nbf;                // neighbour work fields
+    double *tmp = nullptr, *tmp2 = nullptr;   // centre-sized work vectors
+    // GMRES workspace
+    double *V = nullptr;
+    int vcap = 0;
+    double *w = nullptr, *r = nullptr, *ydev = nullptr;
+    fd::Scratch sc{};
+    std::vector<void *> allocs;
+};
+
+namespace fd {
+
+static void *dalloc(fd_schur_s *op, size_t bytes) {
+    void *d = nullptr;
+    FD_CUDA(cudaMalloc(&d, bytes));
+    op->allocs.push_back(d);
+    return d;
+}
+
+static void solve_batch(const std::vector<SolveJob> &jobs, cudaStream_t s) {
+    // group by transform length (one pipeline launch per length)
+    std::map<int, std::vector<SolveJob>> groups;
+    for (const auto &j : jobs) groups[j.p.n].push_back(j);
+    for (auto &g : groups) launch_solve(g.second, s);
+}
+
+static SolveJob job_of(const Plan *p, const double *in, double *out) {
+    SolveJob j{};
+    j.p = p->dev;
+    j.in = in;
+    j.out = out;
+    j.alpha = 1.0;
+    j.beta = 0.0;
+    j.other = nullptr;
+    return j;
+}
+
+// out = sum_i R_ci A_i^{-1} R_ic p   (ddm.py:108-123)
+static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
+    const size_t nnb = op->nb.size();
+    std::vector<SolveJob> jobs;
+    for (size_t i = 0; i < nnb; ++i) {
+        const Plan *q = op->nb[i];
+        FD_CUDA(cudaMemsetAsync(op->nbf[i], 0, sizeof(double) * q->m * q->n, s));
+        const Coupling &c = op->from_c[i];
+        launch_scatter(c.len, c.from, c.to, c.c, p, op->nbf[i], 0, s);
+        jobs.push_back(job_of(q, op->nbf[i], op->nbf[i]));
+    }
+    solve_batch(jobs, s);
+    const Plan *cp = op->center;
+    FD_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * cp->m * cp->n, s));
+    for (size_t i = 0; i < nnb; ++i) {
+        const Coupling &c = op->to_c[i];
+        launch_scatter(c.len, c.from, c.to, c.c, op->nbf[i], out, 1, s);
+    }
+}
+
+// out = alpha * A_c^{-1} r + beta * other
+static void center_solve(fd_schur_s *op, const double *r, double *out, double alpha, double beta,
+                         const double *other, cudaStream_t s) {
+    SolveJob j = job_of(op->center, r, out);
+    j.alpha = alpha;
+    j.beta = beta;
+    j.other = other;
+    solve_batch({j}, s);
+}
+
+// (I - A_c^{-1} S) p   (ddm.py:133-136); out must not alias p
+static void precond_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
+    schur_apply(op, p, op->tmp, s);
+    center_solve(op, op->tmp, out, -1.0, 1.0, p, s);
+}
+
+// (A_c - S) p   (ddm.py:128-131)
+static void unprecond_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
+    launch_stencil(*op->center, op->mod_s, op->mod_n, p, op->tmp2, s);
+    schur_apply(op, p, out, s);
+    const long long N = (long long)op->center->m * op->center->n;
+    launch_axpby(N, 1.0, op->tmp2, -1.0, out, out, s);
+}
+
+static void ensure_basis(fd_schur_s *op, int m) {
+    if (op->vcap >= m + 1) return;
+    if (op->V) cudaFree(op->V);
+    const long long N = (long long)op->center->m * op->center->n;
+    FD_CUDA(cudaMalloc(&op->V, sizeof(double) * N * (m + 1)));
+    op->vcap = m + 1;
+    if (op->sc.cap < m + 8) {
+        if (op->sc.cap) free_scratch(op->sc);
+        op->sc = make_scratch(std::max(m + 8, 64));
+    }
+}
+
+// Restarted GMRES on op.preconditioned (krylov.py:61-165).  x holds x0 (or is
+// zeroed when x_is_zero).  Returns FD_OK or FD_ERR_NOT_CONVERGED.
+static int gmres_precond(fd_schur_s *op, const double *rhs, double *x, int x_is_zero, int mcfg,
+                         double tol, int max_restarts, std::vector<double> &hist, fd_report *rep,
+                         cudaStream_t s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    const long long N = (long long)op->center->m * op->center->n;
+    const int m = (int)std::min<long long>(mcfg, N);
+    ensure_basis(op, m);
+    Scratch &sc = op->sc;
+    double *r = op->r, *w = op->w;
+    if (x_is_zero) {
+        FD_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * N, s));
+        FD_CUDA(cudaMemcpyAsync(r, rhs, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    } else {
+        precond_apply(op, x, w, s);
+        launch_axpby(N, 1.0, rhs, -1.0, w, r, s);
+    }
+    const double r0 = norm2(N, r, sc, s);
+    hist.clear();
+    memset(rep, 0, sizeof(*rep));
+    if (r0 == 0.0) {
+        hist.push_back(0.0);
+        rep->converged = 1;
+        rep->wall_time = elapsed();
+        return FD_OK;
+    }
+    hist.push_back(1.0);
+    int total = 0, cycles = 0;
+    std::vector<double> H((m + 1) * (size_t)m), g(m + 1), cs(m), sn(m), hcol(m + 2), y(m);
+    auto Hat = [&](int i, int k) -> double & { return H[(size_t)i * m + k]; };
+    for (int cyc = 0; cyc < max_restarts; ++cyc) {
+        const double beta = norm2(N, r, sc, s);
+        if (beta / r0 <= tol) break;
+        ++cycles;
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        std::fill(cs.begin(), cs.end(), 0.0);
+        std::fill(sn.begin(), sn.end(), 0.0);
+        sc.hval[0] = beta;
+        FD_CUDA(cudaMemcpyAsync(sc.dval, sc.hval, sizeof(double), cudaMemcpyHostToDevice, s));
+        launch_scale(N, r, sc.dval, op->V, s);   // V[0] = r / beta
+        g[0] = beta;
+        int k_used = 0;
+        bool breakdown = false;
+        for (int k = 0; k < m; ++k) {
+            precond_apply(op, op->V + (long long)k * N, w, s);
+            double w_norm = 0.0;
+            arnoldi_step(N, k, op->V, w, hcol.data(), &w_norm, sc, s);
+            for (int i = 0; i <= k; ++i) Hat(i, k) = hcol[i];
+            const double h_next = hcol[k + 1];
+            Hat(k + 1, k) = h_next;
+            for (int i = 0; i < k; ++i) {   // krylov.py:114-117
+                const double t = cs[i] * Hat(i, k) + sn[i] * Hat(i + 1, k);
+                Hat(i + 1, k) = -sn[i] * Hat(i, k) + cs[i] * Hat(i + 1, k);
+                Hat(i, k) = t;
+            }
+            const double rho = hypot(Hat(k, k), Hat(k + 1, k));   // krylov.py:118-124
+            cs[k] = rho != 0.0 ? Hat(k, k) / rho : 1.0;
+            sn[k] = rho != 0.0 ? Hat(k + 1, k) / rho : 0.0;
+            Hat(k, k) = rho;
+            Hat(k + 1, k) = 0.0;
+            g[k + 1] = -sn[k] * g[k];
+            g[k] = cs[k] * g[k];
+            ++total;
+            k_used = k + 1;
+            hist.push_back(fabs(g[k + 1]) / r0);
+            if (h_next <= 1e-14 * w_norm || h_next == 0.0) {   // krylov.py:130-132
+                breakdown = true;
+                break;
+            }
+            sc.hval[0] = h_next;
+            FD_CUDA(cudaMemcpyAsync(sc.dval, sc.hval, sizeof(double), cudaMemcpyHostToDevice, s));
+            launch_scale(N, w, sc.dval, op->V + (long long)(k + 1) * N, s);
+            if (hist.back() <= tol) break;
+        }
+        for (int i = k_used - 1; i >= 0; --i) {   // krylov.py:138-140
+            double acc = 0.0;
+            for (int j = i + 1; j < k_used; ++j) acc += Hat(i, j) * y[j];
+            y[i] = (g[i] - acc) / Hat(i, i);
+        }
+        FD_CUDA(cudaMemcpyAsync(op->ydev, y.data(), sizeof(double) * k_used, cudaMemcpyHostToDevice, s));
+        launch_basis_update(N, k_used, op->V, op->ydev, x, s);   // krylov.py:141
+        precond_apply(op, x, w, s);
+        launch_axpby(N, 1.0, rhs, -1.0, w, r, s);                // krylov.py:143
+        const double rn = norm2(N, r, sc, s);
+        const double rel = rn / r0;
+        if (rel <= tol || (breakdown && hist.back() <= tol)) {
+            hist.back() = rel;
+            rep->converged = 1;
+            rep->iterations = total;
+            rep->restarts = cycles;
+            rep->true_residual = rn;
+            rep->wall_time = elapsed();
+            return FD_OK;
+        }
+        if (breakdown) break;
+    }
+    precond_apply(op, x, w, s);
+    launch_axpby(N, 1.0, rhs, -1.0, w, r, s);
+    rep->converged = 0;
+    rep->iterations = total;
+    rep->restarts = cycles;
+    rep->true_residual = norm2(N, r, sc, s);
+    rep->wall_time = elapsed();
+    return FD_ERR_NOT_CONVERGED;
+}
+
+static void copy_hist(const std::vector<double> &h, double *out, int cap, fd_report *rep) {
+    const int n = (int)std::min<size_t>(h.size(), cap > 0 ? (size_t)cap : 0);
+    if (out && n > 0) memcpy(out, h.data(), sizeof(double) * n);
+    rep->hist_len = (int)h.size();
+}
+
+}  // namespace fd
+
+// ===========================================================================
+// C ABI
+using namespace fd;
+
+#define FD_API_BEGIN try {
+#define FD_API_END                                        \
+    }                                                     \
+    catch (const fd::Error &e) {                          \
+        fd::set_error(e.msg);                             \
+        return e.code;                                    \
+    }                                                     \
+    catch (const std::exception &e) {                     \
+        fd::set_error(std::string("internal: ") + e.what()); \
+        return FD_ERR_CUDA;                               \
+    }                                                     \
+    return FD_OK;
+
+static cudaStream_t S(void *s) { return (cudaStream_t)s; }
+
+extern "C" {
+
+const char *fd_last_error(void) { return g_last_error.c_str(); }
+int fd_version(void) { return 100; }
+
+int fd_plan_create(fd_plan *out, int m, int n, double dx, double dy, double kappa, double mod_west,
+                   double mod_east, int device) {
+    FD_API_BEGIN
+    if (!out) FD_FAIL(FD_ERR_VALIDATION, "null output handle");
+    *out = nullptr;
+    Plan *p = plan_create(m, n, dx, dy, kappa, mod_west, mod_east, device);
+    *out = new fd_plan_s{p};
+    FD_API_END
+}
+
+int fd_plan_destroy(fd_plan plan) {
+    FD_API_BEGIN
+    if (plan) {
+        plan_destroy(plan->p);
+        delete plan;
+    }
+    FD_API_END
+}
+
+int fd_plan_info(fd_plan plan, int *block_rows, long long *explicit_rows, int *transform) {
+    FD_API_BEGIN
+    if (!plan) FD_FAIL(FD_ERR_VALIDATION, "null plan");
+    if (block_rows) *block_rows = plan->p->dev.R;
+    if (explicit_rows) *explicit_rows = plan->p->explicit_rows;
+    if (transform) *transform = plan->p->transform;
+    FD_API_END
+}
+
+int fd_factor_tables_host(int m, int n, double dx, double dy, double kappa, double mod_west,
+                          double mod_east, double *beta, double *lower) {
+    FD_API_BEGIN
+    factor_tables_host(m, n, dx, dy, kappa, mod_west, mod_east, beta, lower);
+    FD_API_END
+}
+
+int fd_rect_solve(fd_plan plan, const double *f, double *out, void *stream) {
+    FD_API_BEGIN
+    if (!plan || !f || !out) FD_FAIL(FD_ERR_VALIDATION, "null argument");
+    solve_batch({job_of(plan->p, f, out)}, S(stream));
+    FD_API_END
+}
+
+int fd_rect_solve_batched(int count, const fd_plan *plans, const double *const *f, double *const *out,
+                          void *stream) {
+    FD_API_BEGIN
+    std::vector<SolveJob> jobs;
+    for (int i = 0; i < count; ++i) {
+        if (!plans[i] || !f[i] || !out[i]) FD_FAIL(FD_ERR_VALIDATION, "null argument");
+        jobs.push_back(job_of(plans[i]->p, f[i], out[i]));
+    }
+    solve_batch(jobs, S(stream));
+    FD_API_END
+}
+
+int fd_dst_rows(int rows, int n, const double *in, double *out, int device, void *stream) {
+    FD_API_BEGIN
+    if (transform_kind(n) < 0) FD_FAIL(FD_ERR_UNSUPPORTED, "no GPU transform for this length");
+    FD_CUDA(cudaSetDevice(device));
+    launch_dst_rows(rows, n, in, out, twiddles_for(device, n), dense_table_for(device, n), S(stream));
+    FD_API_END
+}
+
+int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa, double mod_west,
+                     double mod_east, double mod_south, double mod_north, const double *v,
+                     double *out, void *stream) {
+    FD_API_BEGIN
+    if (m < 1 || n < 1 || !v || !out) FD_FAIL(FD_ERR_VALIDATION, "bad stencil arguments");
+    launch_stencil(m, n, delta_x, delta_y, kappa, mod_west, mod_east, mod_south, mod_north, v, out,
+                   S(stream));
+    FD_API_END
+}
+
+int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, double center_mod_north,
+                    int n_nb, const fd_plan *nb, const int *line_len,
+                    const int64_t *const *to_c_from, const int64_t *const *to_c_to,
+                    const double *to_c_coupling, const int64_t *const *from_c_from,
+                    const int64_t *const *from_c_to, const double *from_c_coupling) {
+    FD_API_BEGIN
+    if (!out || !center) FD_FAIL(FD_ERR_VALIDATION, "null argument");
+    *out = nullptr;
+    fd_schur_s *op = new fd_schur_s();
+    try {
+        op->device = center->p->device;
+        FD_CUDA(cudaSetDevice(op->device));
+        op->center = center->p;
+        op->mod_s = center_mod_south;
+        op->mod_n = center_mod_north;
+        const long long Nc = (long long)center->p->m * center->p->n;
+        for (int i = 0; i < n_nb; ++i) {
+            Plan *q = nb[i]->p;
+            op->nb.push_back(q);
+            auto up = [&](const int64_t *h, int len) {
+                int64_t *d = (int64_t *)dalloc(op, sizeof(int64_t) * std::max(len, 1));
+                FD_CUDA(cudaMemcpy(d, h, sizeof(int64_t) * len, cudaMemcpyHostToDevice));
+                return d;
+            };
+            const int len = line_len[i];
+            op->to_c.push_back(Coupling{len, up(to_c_from[i], len), up(to_c_to[i], len), to_c_coupling[i]});
+            op->from_c.push_back(
+                Coupling{len, up(from_c_from[i], len), up(from_c_to[i], len), from_c_coupling[i]});
+            op->nbf.push_back((double *)dalloc(op, sizeof(double) * q->m * q->n));
+        }
+        op->tmp = (double *)dalloc(op, sizeof(double) * Nc);
+        op->tmp2 = (double *)dalloc(op, sizeof(double) * Nc);
+        op->w = (double *)dalloc(op, sizeof(double) * Nc);
+        op->r = (double *)dalloc(op, sizeof(double) * Nc);
+        op->ydev = (double *)dalloc(op, sizeof(double) * 4096);
+        op->sc = make_scratch(128);
+    } catch (...) {
+        for (void *a : op->allocs) cudaFree(a);
+        delete op;
+        throw;
+    }
+    *out = op;
+    FD_API_END
+}
+
+int fd_schur_destroy(fd_schur op) {
+    FD_API_BEGIN
+    if (op) {
+        cudaSetDevice(op->device);
+        for (void *a : op->allocs) cudaFree(a);
+        if (op->V) cudaFree(op->V);
+        if (op->sc.cap) free_scratch(op->sc);
+        delete op;
+    }
+    FD_API_END
+}
+
+int fd_schur_apply(fd_schur op, const double *p, double *out, void *stream) {
+    FD_API_BEGIN
+    schur_apply(op, p, out, S(stream));
+    FD_API_END
+}
+
+int fd_center_solve(fd_schur op, const double *r, double *out, void *stream) {
+    FD_API_BEGIN
+    center_solve(op, r, out, 1.0, 0.0, nullptr, S(stream));
+    FD_API_END
+}
+
+int fd_precond_apply(fd_schur op, const double *p, double *out, void *stream) {
+    FD_API_BEGIN
+    precond_apply(op, p, out, S(stream));
+    FD_API_END
+}
+
+int fd_unprecond_apply(fd_schur op, const double *p, double *out, void *stream) {
+    FD_API_BEGIN
+    unprecond_apply(op, p, out, S(stream));
+    FD_API_END
+}
+
+int fd_gmres_precond(fd_schur op, const double *rhs, double *x, int x_is_zero, int m, double tol,
+                     int max_restarts, double *history, int hist_cap, fd_report *rep,
+                     void *stream) {
+    FD_API_BEGIN
+    if (!op || !rhs || !x || !rep) FD_FAIL(FD_ERR_VALIDATION, "null argument");
+    if (m < 1 || !(tol > 0) || max_restarts < 1) FD_FAIL(FD_ERR_VALIDATION, "bad GMRES config");
+    std::vector<double> hist;
+    const int st = gmres_precond(op, rhs, x, x_is_zero, m, tol, max_restarts, hist, rep, S(stream));
+    copy_hist(hist, history, hist_cap, rep);
+    if (st != FD_OK) {
+        std::ostringstream os;
+        os << "GMRES did not reach tol=" << tol << " in " << rep->iterations << " iterations";
+        FD_FAIL(st, os.str());
+    }
+    FD_API_END
+}
+
+int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb, double *p_center,
+                 double *const *p_nb, int m, double tol, int max_restarts, double *history,
+                 int hist_cap, fd_report *rep, void *stream) {
+    FD_API_BEGIN
+    if (!op || !f_center || !p_center || !rep) FD_FAIL(FD_ERR_VALIDATION, "null argument");
+    if (m < 1 || !(tol > 0) || max_restarts < 1) FD_FAIL(FD_ERR_VALIDATION, "bad GMRES config");
+    cudaStream_t s = S(stream);
+    const size_t nnb = op->nb.size();
+    const long long Nc = (long long)op->center->m * op->center->n;
+    // pre-solves q_i = A_i^{-1} f_i into the caller's output fields (ddm.py:249-250)
+    std::vector<SolveJob> jobs;
+    for (size_t i = 0; i < nnb; ++i) jobs.push_back(job_of(op->nb[i], f_nb[i], p_nb[i]));
+    solve_batch(jobs, s);
+    // f' = f_c - sum_i R_ci q_i  (ddm.py:252-254); tmp2 holds f'
+    double *fp = op->tmp2;
+    FD_CUDA(cudaMemcpyAsync(fp, f_center, sizeof(double) * Nc, cudaMemcpyDeviceToDevice, s));
+    for (size_t i = 0; i < nnb; ++i) {
+        const Coupling &c = op->to_c[i];
+        // fp[to] = fp[to] - c * q[from]
+        launch_scatter(c.len, c.from, c.to, -c.c, p_nb[i], fp, 1, s);
+    }
+    // solve_coupled fft branch: rhs = A_c^{-1} f'; GMRES on the preconditioned system
+    // (krylov.py:176-187); fp must survive, so rhs goes to a fresh buffer
+    double *rhs = nullptr;
+    FD_CUDA(cudaMallocAsync(&rhs, sizeof(double) * Nc, s));
+    center_solve(op, fp, rhs, 1.0, 0.0, nullptr, s);
+    std::vector<double> hist;
+    int st = gmres_precond(op, rhs, p_center, 1, m, tol, max_restarts, hist, rep, s);
+    copy_hist(hist, history, hist_cap, rep);
+    // true residual ||(A_c - S) x - f'|| (krylov.py:189); rhs buffer reused
+    unprecond_apply(op, p_center, rhs, s);
+    launch_axpby(Nc, 1.0, rhs, -1.0, fp, rhs, s);
+    rep->true_residual = norm2(Nc, rhs, op->sc, s);
+    FD_CUDA(cudaFreeAsync(rhs, s));
+    // back-substitution p_i = q_i - A_i^{-1} R_ic p_c (ddm.py:259-269)
+    jobs.clear();
+    for (size_t i = 0; i < nnb; ++i) {
+        const Plan *q = op->nb[i];
+        FD_CUDA(cudaMemsetAsync(op->nbf[i], 0, sizeof(double) * q->m * q->n, s));
+        const Coupling &c = op->from_c[i];
+        launch_scatter(c.len, c.from, c.to, c.c, p_center, op->nbf[i], 0, s);
+        jobs.push_back(job_of(q, op->nbf[i], op->nbf[i]));
+    }
+    solve_batch(jobs, s);
+    for (size_t i = 0; i < nnb; ++i) {
+        const Plan *q = op->nb[i];
+        launch_axpby((long long)q->m * q->n, 1.0, p_nb[i], -1.0, op->nbf[i], p_nb[i], s);
+    }
+    if (st != FD_OK) {
+        std::ostringstream os;
+        os << "GMRES did not reach tol=" << tol << " in " << rep->iterations << " iterations";
+        FD_FAIL(st, os.str());
+    }
+    FD_API_END
+}
+
+int fd_arnoldi_step(int N, int k, const double *V, double *w, double *h, double *w_norm,
+                    void *stream) {
+    FD_API_BEGIN
+    arnoldi_step(N, k, V, w, h, w_norm, device_scratch(), S(stream));
+    FD_API_END
+}
+
+int fd_basis_update(int N, int k, const double *V, const double *y, double *x, void *stream) {
+    FD_API_BEGIN
+    Scratch &sc = device_scratch();
+    if (k > sc.cap) FD_FAIL(FD_ERR_VALIDATION, "basis update: k too large");
+    memcpy(sc.hval, y, sizeof(double) * k);
+    FD_CUDA(cudaMemcpyAsync(sc.dval, sc.hval, sizeof(double) * k, cudaMemcpyHostToDevice, S(stream)));
+    launch_basis_update(N, k, V, sc.dval, x, S(stream));
+    FD_CUDA(cudaStreamSynchronize(S(stream)));
+    FD_API_END
+}
+
+int fd_axpby(int N, double a, const double *x, double b, const double *y, double *out, void *stream) {
+    FD_API_BEGIN
+    launch_axpby(N, a, x, b, y, out, S(stream));
+    FD_API_END
+}
+
+int fd_norm(int N, const double *x, double *result, void *stream) {
+    FD_API_BEGIN
+    *result = norm2(N, x, device_scratch(), S(stream));
+    FD_API_END
+}
+
+int fd_dot(int N, const double *x, const double *y, double *result, void *stream) {
+    FD_API_BEGIN
+    Scratch &sc = device_scratch();
+    launch_dot(N, x, y, sc.dval, sc.red, S(stream));
+    FD_CUDA(cudaMemcpyAsync(sc.hval, sc.dval, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
+    FD_CUDA(cudaStreamSynchronize(S(stream)));
+    *result = sc.hval[0];
+    FD_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// Internal structures of libfftddm_b200 (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/fftddm_b200.h"
+
+namespace fd {
+
+// ---------------------------------------------------------------------------
+// error plumbing
+void set_error(const std::string &msg);
+struct Error {
+    int code;
+    std::string msg;
+};
+#define FD_CUDA(call)                                                              \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess)                                                     \
+            throw ::fd::Error{FD_ERR_CUDA, std::string(#call) + ": " +             \
+                                               cudaGetErrorString(e_)};           \
+    } while (0)
+#define FD_FAIL(code, msg) throw ::fd::Error{(code), (msg)}
+
+// ---------------------------------------------------------------------------
+// Device view of one rectangle plan.  Passed by value to kernels.
+//
+// Layout: field (m, n) fp64 row-major; rows = x-lines = sweep axis, columns =
+// y = DST axis.  Rows are grouped into carry blocks of R rows (the last one
+// may be short): nb = ceil(m / R).
+//
+// Factor tables (compressed, ref rectsolver.py:62-77): for mode k the rows
+// i < ex_len[k] are stored explicitly at ex_off[k] + i; rows >= ex_len[k]
+// (a multiple of R) carry the bitwise fixed point (l_inf, beta_inf).  Row m-1
+// always uses last_b (it carries the east end modifier).
+struct PlanDev {
+    int m, n, R, nb;
+    double off;          // delta_x: constant off-diagonal of the sweep system
+    double scale;        // sqrt(2/(n+1)): orthonormal DST-I factor
+    const int *ex_off;   // [n]
+    const int *ex_len;   // [n]
+    const double *ex;    // [sum ex_len][4]: l, 1/beta, beta, P(block-relative)
+    const double *cv;    // [n][4]: l_inf, 1/beta_inf, beta_inf, 1/(-l_inf)
+    const double *last;  // [n][2]: beta_{m-1}, 1/beta_{m-1}
+    const double *blk;   // [nb][3][n]: Pe, xi_s, Q per block and mode
+    double *ye;          // [nb][n] pass-1 local forward value at block end -> Y carries
+    double *fs;          // [nb][n] pass-1 local backward value at block start -> X carries
+    const double *dense; // [n][n] sin table (dense transform) or nullptr
+    const double2 *tw;   // FFT twiddles e^{-2 pi i t / L}, t < L = 2(n+1), or nullptr
+};
+
+enum Transform { kDense = 0, kFFT = 1 };
+
+struct Plan {
+    int device;
+    int m, n;
+    double dx, dy, kappa, mod_w, mod_e;
+    double delta_x, delta_y;
+    int transform;
+    long long explicit_rows;
+    PlanDev dev;
+    std::vector<void *> allocs;
+};
+
+// one job of a batched rectangle launch
+struct SolveJob {
+    PlanDev p;
+    const double *in;
+    double *out;
+    // pass-2 epilogue: out = alpha * x + beta * other  (other may be null)
+    double alpha, beta;
+    const double *other;
+};
+
+constexpr int kMaxJobs = 8;
+struct JobList {
+    int count;
+    int block_start[kMaxJobs + 1];  // prefix of CTAs per job
+    SolveJob job[kMaxJobs];
+};
+
+// kernels / launchers (solve.cu)
+int rows_per_block(int n);
+int transform_kind(int n);
+void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s);
+void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,
+                     const double *dense, cudaStream_t s);
+const double2 *twiddles_for(int device, int n);
+const double *dense_table_for(int device, int n);
+
+// vector kernels (ops.cu)
+void launch_stencil(int m, int n, double delta_x, double delta_y, double kappa, double mw,
+                    double me, double ms, double mn, const double *v, double *out, cudaStream_t s);
+inline void launch_stencil(const Plan &p, double ms, double mn, const double *v, double *out,
+                           cudaStream_t s) {
+    launch_stencil(p.m, p.n, p.delta_x, p.delta_y, p.kappa, p.mod_w, p.mod_e, ms, mn, v, out, s);
+}
+void launch_scatter(int len, const int64_t *from, const int64_t *to, double c, const double *src,
+                    double *dst, int accumulate, cudaStream_t s);
+void launch_axpby(long long N, double a, const double *x, double b, const double *y, double *out,
+                  cudaStream_t s);
+// deterministic reductions: result written to device scalar *out
+struct RedWork {
+    double *partials;   // [kRedBlocks]
+    unsigned int *counter;
+};
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+void launch_dot(long long N, const double *x, const double *y, double *out, RedWork w,
+                cudaStream_t s);
+// fused MGS step: w -= (*h_prev) * vprev (if vprev); *h_out = vi . w   (vi may be null -> ||w||^2)
+void launch_mgs(long long N, double *w, const double *vprev, const double *h_prev,
+                const double *vi, double *h_out, RedWork wk, cudaStream_t s);
+void launch_basis_update(long long N, int k, const double *V, const double *y_dev, double *x,
+                         cudaStream_t s);
+void launch_scale(long long N, const double *x, const double *s_dev, double *out, cudaStream_t s);
+
+}  // namespace fd

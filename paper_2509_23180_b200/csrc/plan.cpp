@@ -1,0 +1,347 @@
+// Plan construction (host): eigenvalues, compressed per-mode LU factors of the
+// sweep systems, block-carry tables, transform tables.  Compiled with
+// -ffp-contract=off so every recurrence rounds exactly like the reference's
+// numpy expressions.
+//
+// Reference: transforms.eigenvalues DD (transforms.py:26-31,38),
+// rectsolver._factor_tridiag (rectsolver.py:62-77), plan_rect diag/end
+// modifiers and pivot tolerance (rectsolver.py:122-135,153-163).
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <sstream>
+
+#include "fd_internal.h"
+
+namespace fd {
+
+namespace {
+
+struct ModeFactors {
+    std::vector<double> l, b;  // rows 0..len-1 explicit
+    int fix;                   // first row of the fixed point (-1 if none)
+    double l_inf, b_inf;       // converged values (valid when fix >= 0)
+    double b_last;             // beta_{m-1}
+    bool bad;
+};
+
+// eigenvalue of mode k (0-based), exactly as numpy evaluates transforms.py:29,38
+double eig_dd(int k, int n, double dt, double dor, double kappa) {
+    const double j = double(k + 1);
+    const double arg = j * M_PI / double(n + 1);
+    double lam = -2.0 * (dt + dor) + (2.0 * dt) * cos(arg);
+    return lam + kappa;
+}
+
+// Run the reference recurrence for one mode until the bitwise fixed point.
+ModeFactors factor_mode(int m, double lam, double mod_w, double mod_e, double off, double tol,
+                        int R) {
+    ModeFactors f;
+    f.bad = false;
+    f.fix = -1;
+    auto diag = [&](int i) {
+        double d = lam;
+        if (i == 0) d = d + mod_w;
+        if (i == m - 1) d = d + mod_e;
+        return d;
+    };
+    double b0 = diag(0);
+    bool bad = fabs(b0) < tol;
+    double safe = bad ? 1.0 : b0;
+    f.l.push_back(0.0);
+    f.b.push_back(b0);
+    // regular rows 1..m-2 (no end modifier): stop at the fixed point
+    int i = 1;
+    for (; i < m; ++i) {
+        const double l = off / safe;
+        double b = diag(i) - off * l;
+        bad = bad || fabs(b) < tol;
+        safe = bad ? 1.0 : b;
+        b = safe;
+        f.l.push_back(l);
+        f.b.push_back(b);
+        if (i >= 1 && i <= m - 2 && b == f.b[i - 1] && f.fix < 0) {
+            f.fix = i;
+            break;
+        }
+    }
+    f.bad = bad;
+    if (f.fix >= 0) {
+        f.l_inf = f.l[f.fix];
+        f.b_inf = f.b[f.fix];
+        // explicit region: block aligned, >= fix
+        const int len = std::min(m, ((f.fix + R - 1) / R) * R);
+        while ((int)f.l.size() < len) {
+            f.l.push_back(f.l_inf);
+            f.b.push_back(f.b_inf);
+        }
+        f.l.resize(len);
+        f.b.resize(len);
+        // last row carries the east modifier (rectsolver.py:133)
+        const double l = off / f.b_inf;
+        double b = diag(m - 1) - off * l;
+        f.bad = f.bad || fabs(b) < tol;
+        f.b_last = b;
+        if (len == m) f.b[m - 1] = b;
+    } else {
+        f.l_inf = f.l.back();
+        f.b_inf = f.b.back();
+        f.b_last = f.b[m - 1];
+    }
+    return f;
+}
+
+std::mutex g_tab_mu;
+std::map<std::pair<int, int>, void *> g_tw, g_dense;
+
+}  // namespace
+
+// block-relative products for rows [s, e] of one mode given l(i), b(i)
+template <class GetL, class GetB>
+static void block_scalars(int s, int e, int m, double off, GetL gl, GetB gb, double *Pe, double *xi,
+                          double *Q, double *Pcol /* per row P, may be null */) {
+    // P_i = prod_{t=s}^{i} (-l_t) (block 0: unused, 0); pi_i = prod_{t=s+1}^{i} (-l_t)
+    double P = (s == 0) ? 0.0 : -gl(s);
+    double pi = 1.0, xs = 0.0;
+    for (int i = s; i <= e; ++i) {
+        if (i > s) {
+            const double nl = -gl(i);
+            P = P * nl;
+            pi = pi * nl;
+        }
+        if (Pcol) Pcol[i - s] = P;
+        xs = xs + P * (pi / gb(i));
+    }
+    *Pe = P;
+    *xi = xs;
+    // Q = prod_{t=s}^{e} (-off / beta_t)
+    double q = 1.0;
+    for (int i = s; i <= e; ++i) q = q * (-off / gb(i));
+    *Q = q;
+    (void)m;
+}
+
+struct HostTables {
+    std::vector<int> off, len;
+    std::vector<double> ex;    // 4 per explicit row
+    std::vector<double> cv;    // 4 per mode
+    std::vector<double> last;  // 2 per mode
+    std::vector<double> blk;   // nb * 3 * n
+    std::vector<int> bad_modes;
+    long long explicit_rows = 0;
+};
+
+static HostTables build_tables(int m, int n, double dx, double dy, double kappa, double mod_w,
+                               double mod_e, int R) {
+    const double delta_x = 1.0 / (dx * dx), delta_y = 1.0 / (dy * dy);
+    const double off = delta_x;
+    std::vector<double> lam(n);
+    double amax = 0.0;
+    for (int k = 0; k < n; ++k) {
+        lam[k] = eig_dd(k, n, delta_y, delta_x, kappa);
+        amax = std::max(amax, fabs(lam[k]));
+    }
+    const double tol = 1e-13 * std::max(amax, off);   // rectsolver.py:135
+    const int nb = (m + R - 1) / R;
+    HostTables T;
+    T.off.resize(n);
+    T.len.resize(n);
+    T.cv.resize(4 * size_t(n));
+    T.last.resize(2 * size_t(n));
+    T.blk.assign(size_t(nb) * 3 * n, 0.0);
+    for (int k = 0; k < n; ++k) {
+        ModeFactors f = factor_mode(m, lam[k], mod_w, mod_e, off, tol, R);
+        if (f.bad) T.bad_modes.push_back(k);
+        const int len = (int)f.l.size();
+        T.off[k] = (int)(T.ex.size() / 4);
+        T.len[k] = len;
+        T.explicit_rows += len;
+        auto gl = [&](int i) { return i < len ? f.l[i] : f.l_inf; };
+        auto gb = [&](int i) { return i == m - 1 ? f.b_last : (i < len ? f.b[i] : f.b_inf); };
+        T.cv[4 * k + 0] = f.l_inf;
+        T.cv[4 * k + 1] = 1.0 / f.b_inf;
+        T.cv[4 * k + 2] = f.b_inf;
+        T.cv[4 * k + 3] = 1.0 / (-f.l_inf);
+        T.last[2 * k + 0] = f.b_last;
+        T.last[2 * k + 1] = 1.0 / f.b_last;
+        std::vector<double> Pcol(R);
+        const size_t base = T.ex.size();
+        T.ex.resize(base + 4 * size_t(len));
+        // explicit blocks
+        double conv[3];
+        bool conv_done = false;
+        for (int b = 0; b < nb; ++b) {
+            const int s = b * R, e = std::min(m, s + R) - 1;
+            double Pe, xi, Q;
+            if (s < len || e == m - 1 || !conv_done) {
+                if (s >= len && e < m - 1) {
+                    block_scalars(s, e, m, off, gl, gb, &conv[0], &conv[1], &conv[2], nullptr);
+                    conv_done = true;
+                    Pe = conv[0], xi = conv[1], Q = conv[2];
+                } else {
+                    block_scalars(s, e, m, off, gl, gb, &Pe, &xi, &Q, Pcol.data());
+                }
+            } else {
+                Pe = conv[0], xi = conv[1], Q = conv[2];
+            }
+            if (s < len) {
+                for (int i = s; i <= e && i < len; ++i) {
+                    double *r = &T.ex[base + 4 * size_t(i)];
+                    r[0] = f.l[i];
+                    r[1] = 1.0 / gb(i);
+                    r[2] = gb(i);
+                    r[3] = Pcol[i - s];
+                }
+            }
+            T.blk[(size_t(b) * 3 + 0) * n + k] = Pe;
+            T.blk[(size_t(b) * 3 + 1) * n + k] = xi;
+            T.blk[(size_t(b) * 3 + 2) * n + k] = Q;
+        }
+    }
+    return T;
+}
+
+// ---------------------------------------------------------------------------
+// transform tables, shared per (device, n)
+const double2 *twiddles_for(int device, int n) {
+    if (transform_kind(n) != kFFT) return nullptr;
+    std::lock_guard<std::mutex> g(g_tab_mu);
+    auto key = std::make_pair(device, n);
+    auto it = g_tw.find(key);
+    if (it != g_tw.end()) return (const double2 *)it->second;
+    const int L = 2 * (n + 1);
+    std::vector<double2> h(L);
+    for (int t = 0; t < L; ++t) {
+        // e^{-2 pi i t / L} with the angle reduced to the first octant in long double
+        long double a = 2.0L * 3.141592653589793238462643383279502884L * (long double)t / (long double)L;
+        h[t].x = (double)cosl(a);
+        h[t].y = (double)(-sinl(a));
+    }
+    void *d = nullptr;
+    FD_CUDA(cudaMalloc(&d, sizeof(double2) * L));
+    FD_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
+    g_tw[key] = d;
+    return (const double2 *)d;
+}
+
+const double *dense_table_for(int device, int n) {
+    if (transform_kind(n) != kDense) return nullptr;
+    std::lock_guard<std::mutex> g(g_tab_mu);
+    auto key = std::make_pair(device, n);
+    auto it = g_dense.find(key);
+    if (it != g_dense.end()) return (const double *)it->second;
+    std::vector<double> h(size_t(n) * n);
+    const long long P2 = 2LL * (n + 1);
+    for (int j = 0; j < n; ++j)
+        for (int k = 0; k < n; ++k) {
+            long long q = ((long long)(j + 1) * (k + 1)) % P2;   // sin(pi q/(n+1)), exact reduction
+            long double a = 3.141592653589793238462643383279502884L * (long double)q / (long double)(n + 1);
+            h[size_t(j) * n + k] = (double)sinl(a);
+        }
+    void *d = nullptr;
+    FD_CUDA(cudaMalloc(&d, sizeof(double) * h.size()));
+    FD_CUDA(cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    g_dense[key] = d;
+    return (const double *)d;
+}
+
+template <class T>
+static T *upload(Plan *p, const std::vector<T> &h) {
+    void *d = nullptr;
+    size_t bytes = std::max<size_t>(sizeof(T), sizeof(T) * h.size());
+    FD_CUDA(cudaMalloc(&d, bytes));
+    p->allocs.push_back(d);
+    if (!h.empty()) FD_CUDA(cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    return (T *)d;
+}
+
+Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
+                  int device) {
+    if (m < 1 || n < 1) FD_FAIL(FD_ERR_VALIDATION, "plan: empty grid");
+    if (!(dx > 0) || !(dy > 0)) FD_FAIL(FD_ERR_VALIDATION, "plan: nonpositive spacing");
+    const int tk = transform_kind(n);
+    if (tk < 0) {
+        std::ostringstream os;
+        os << "plan: no GPU transform for n = " << n
+           << " (supported: n+1 a power of two in [256, 4096], or n <= 1024)";
+        FD_FAIL(FD_ERR_UNSUPPORTED, os.str());
+    }
+    const int R = rows_per_block(n);
+    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R);
+    if (!T.bad_modes.empty()) {
+        std::ostringstream os;
+        os << "operator singular in spectral modes (";
+        for (size_t i = 0; i < T.bad_modes.size() && i < 16; ++i) os << (i ? ", " : "") << T.bad_modes[i];
+        os << ")";
+        FD_FAIL(FD_ERR_SINGULAR, os.str());
+    }
+    FD_CUDA(cudaSetDevice(device));
+    Plan *p = new Plan();
+    try {
+        p->device = device;
+        p->m = m;
+        p->n = n;
+        p->dx = dx;
+        p->dy = dy;
+        p->kappa = kappa;
+        p->mod_w = mod_w;
+        p->mod_e = mod_e;
+        p->delta_x = 1.0 / (dx * dx);
+        p->delta_y = 1.0 / (dy * dy);
+        p->transform = tk;
+        p->explicit_rows = T.explicit_rows;
+        PlanDev &d = p->dev;
+        d.m = m;
+        d.n = n;
+        d.R = R;
+        d.nb = (m + R - 1) / R;
+        d.off = p->delta_x;
+        d.scale = sqrt(2.0 / (n + 1));
+        d.ex_off = upload(p, T.off);
+        d.ex_len = upload(p, T.len);
+        d.ex = upload(p, T.ex);
+        d.cv = upload(p, T.cv);
+        d.last = upload(p, T.last);
+        d.blk = upload(p, T.blk);
+        std::vector<double> zeros(size_t(d.nb) * n, 0.0);
+        d.ye = upload(p, zeros);
+        d.fs = upload(p, zeros);
+        d.tw = twiddles_for(device, n);
+        d.dense = dense_table_for(device, n);
+    } catch (...) {
+        for (void *a : p->allocs) cudaFree(a);
+        delete p;
+        throw;
+    }
+    return p;
+}
+
+void plan_destroy(Plan *p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    for (void *a : p->allocs) cudaFree(a);
+    delete p;
+}
+
+void factor_tables_host(int m, int n, double dx, double dy, double kappa, double mod_w,
+                        double mod_e, double *beta, double *lower) {
+    if (m < 1 || n < 1) FD_FAIL(FD_ERR_VALIDATION, "factor: empty grid");
+    const int R = (transform_kind(n) >= 0) ? rows_per_block(n) : 16;
+    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R);
+    for (int k = 0; k < n; ++k) {
+        for (int i = 0; i < m; ++i) {
+            const bool ex = i < T.len[k];
+            const double *r = &T.ex[4 * size_t(T.off[k] + (ex ? i : 0))];
+            double l = ex ? r[0] : T.cv[4 * k + 0];
+            double b = (i == m - 1) ? T.last[2 * k] : (ex ? r[2] : T.cv[4 * k + 2]);
+            beta[size_t(i) * n + k] = b;
+            lower[size_t(i) * n + k] = l;
+        }
+    }
+    if (!T.bad_modes.empty()) FD_FAIL(FD_ERR_SINGULAR, "operator singular");
+}
+
+}  // namespace fd

@@ -1,0 +1,180 @@
+"""Generate the parity fixtures in tests/golden/ by running the REAL reference.
+
+Run in the build container only (needs /root/reference):
+
+    python tests/golden/make_golden.py small c0 c1        # seconds
+    python tests/golden/make_golden.py c2 c3              # minutes (c3 ~15 min, 16 GB)
+
+The reference package is imported from /root/reference/pkg/src; its inputs
+come from paper_2509_23180_b200.configs driven with the *reference's*
+geometry API (api=fftddm), so the GPU tests rebuild bit-identical inputs from
+the same recipe.  Large fields are stored as norms plus values at fixed
+sampled indices; c0 and the small cases are stored in full.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+from types import SimpleNamespace
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import fftddm                                          # noqa: E402  (the reference)
+from fftddm import ddm, geometry, krylov, rectsolver, transforms  # noqa: E402
+from paper_2509_23180_b200 import configs              # noqa: E402
+
+API = SimpleNamespace(RectSubdomain=geometry.RectSubdomain, BoundaryKind=geometry.BoundaryKind,
+                      CompositeDomain=geometry.CompositeDomain,
+                      make_interface=geometry.make_interface, validate=geometry.validate,
+                      lift_dirichlet=rectsolver.lift_dirichlet)
+B = geometry.BoundaryKind
+SAMPLES = 4096
+
+
+def sample_idx(size, sid):
+    rng = np.random.default_rng(1000 + sid)
+    k = min(SAMPLES, size)
+    return np.sort(rng.choice(size, k, replace=False))
+
+
+def rect(m, n, dx, dy, kappa, bc, half=()):
+    kinds = {"D": B.DIRICHLET, "N": B.NEUMANN, "I": B.INTERFACE}
+    edge_bc = {e: kinds[c] for e, c in zip(("west", "east", "south", "north"), bc)}
+    return geometry.RectSubdomain(id=0, origin=(0.0, 0.0), m=m, n=n, dx=dx, dy=dy,
+                                  edge_bc=edge_bc, kappa=kappa,
+                                  half_cell_dirichlet=frozenset(half))
+
+
+# (m, n, dx, dy, kappa, bc WESN, half-cell edges) -- all DD along y
+RECT_CASES = [
+    (1, 1, 1.0, 1.0, 0.0, "DDDD", ()),
+    (3, 3, 1.0, 1.0, 0.0, "DDDD", ()),
+    (5, 4, 0.5, 0.25, -1.5, "DDDD", ()),
+    (8, 7, 1.0 / 8, 1.0 / 8, 0.0, "DDDD", ()),
+    (16, 15, 1.0 / 16, 1.0 / 16, -10.0, "DDDD", ()),
+    (33, 31, 1.0 / 31, 1.0 / 31, 0.0, "DDDD", ()),
+    (64, 63, 1.0 / 64, 1.0 / 64, 3.0, "DDDD", ()),
+    (20, 127, 0.01, 0.02, -100.0, "DDDD", ()),
+    (141, 141, 1.0 / 141, 1.0 / 141, 0.0, "DDDD", ()),
+    (12, 9, 1.0, 1.0, 0.0, "DDDD", ("west",)),
+    (12, 9, 1.0, 1.0, 0.0, "DDDD", ("west", "east")),
+    (10, 15, 0.1, 0.1, -2.0, "NNDD", ()),
+    (9, 31, 1.0, 0.5, 0.0, "IDDD", ("east",)),
+    (257, 255, 1.0 / 255, 1.0 / 255, 0.0, "DDDD", ()),
+    (40, 1023, 1.0 / 1023, 1.0 / 1023, -10.0, "DDDD", ()),
+]
+
+
+def make_small():
+    out = {}
+    rng = np.random.default_rng(7)
+    # DST-I / apply_Q on row batches (transforms.py:106-113)
+    for n in (1, 2, 3, 4, 7, 8, 15, 31, 63, 64, 127, 141, 255, 511, 1023, 2047, 4095):
+        x = rng.standard_normal((3, n))
+        pl = transforms.make_plan("DD", n, 1.0, 1.0)
+        out[f"dst_in_{n}"] = x
+        out[f"dst_out_{n}"] = transforms.apply_Q(pl, x)
+        out[f"eig_{n}"] = transforms.eigenvalues("DD", n, 2.5, 0.75, kappa=-0.5)
+    # rectangle plans and solves (rectsolver.py:94-213,264-289)
+    for c, (m, n, dx, dy, kappa, bc, half) in enumerate(RECT_CASES):
+        sub = rect(m, n, dx, dy, kappa, bc, half)
+        pl = rectsolver.plan_rect(sub)
+        f = rng.uniform(-1, 1, m * n)
+        out[f"rect_f_{c}"] = f
+        out[f"rect_p_{c}"] = rectsolver.solve_rect(pl, f).values
+        if m * n <= 5000:
+            out[f"rect_beta_{c}"] = pl.beta
+            out[f"rect_lower_{c}"] = pl.lower
+        out[f"rect_Av_{c}"] = rectsolver.apply_rect_operator(sub, f)
+    # BASELINE-geometry crosses at reduced N: Schur applies + full solves
+    for N in (4, 8, 15, 31):
+        for kappa in (0.0, -100.0):
+            tag = f"{N}_{int(-kappa)}"
+            comp = configs.cross_composite(N, kappa=kappa, api=API)
+            op = ddm.build_schur_operator(comp, threads=1)
+            p = rng.standard_normal(op.size)
+            out[f"x_p_{tag}"] = p
+            out[f"x_schur_{tag}"] = op.schur(p)
+            out[f"x_pre_{tag}"] = op.preconditioned(p)
+            out[f"x_unpre_{tag}"] = op.unpreconditioned(p)
+            f, exact = configs.manufactured_rhs(comp, "sin_exp", api=API)
+            fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+            for sid, fld in fields.items():
+                out[f"x_sol_{tag}_{sid}"] = fld.values
+            out[f"x_iters_{tag}"] = np.array(rep.iterations)
+            out[f"x_hist_{tag}"] = rep.residual_history
+            out[f"x_true_{tag}"] = np.array(rep.true_residual)
+    # GMRES on a dense well-conditioned system with a small restart (krylov.py:61-165)
+    A = np.eye(40) + 0.3 * rng.standard_normal((40, 40)) / np.sqrt(40)
+    b = rng.standard_normal(40)
+    x, rep = krylov.gmres(lambda v: A @ v, b, cfg=krylov.GmresConfig(m=7, tol=1e-12))
+    out.update(gm_A=A, gm_b=b, gm_x=x, gm_iters=np.array(rep.iterations),
+               gm_hist=rep.residual_history)
+    np.savez_compressed(os.path.join(HERE, "small.npz"), **out)
+    print("small.npz", len(out), "arrays")
+
+
+def solve_cross(name, full):
+    t0 = time.perf_counter()
+    comp, f, exact, meta = configs.build_cross_case(name, api=API)
+    t_build = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+    wall = time.perf_counter() - t0
+    out = dict(iterations=np.array(rep.iterations), history=rep.residual_history,
+               true_residual=np.array(rep.true_residual), wall=np.array(wall),
+               build=np.array(t_build), threads=np.array(ddm.solver_threads()),
+               points=np.array(meta["points"]))
+    if exact is not None:
+        out["rel_l2_exact"] = np.array(configs.rel_l2(fields, exact))
+    for sid, fld in fields.items():
+        v = fld.values
+        out[f"norm_{sid}"] = np.array(np.linalg.norm(v))
+        out[f"sum_{sid}"] = np.array(v.sum())
+        idx = sample_idx(v.size, sid)
+        out[f"idx_{sid}"] = idx
+        out[f"val_{sid}"] = v[idx]
+        if full:
+            out[f"sol_{sid}"] = v
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, "iters", rep.iterations, "wall", round(wall, 2), "s",
+          "rel_l2", out.get("rel_l2_exact"))
+
+
+def make_c1():
+    out = {}
+    for kappa in (0.0, -10.0):
+        subs = configs.batch_rects(1023, 5, kappa, api=API)
+        rng = np.random.default_rng(0)
+        f = [rng.uniform(-1, 1, s.size) for s in subs]
+        plans = [rectsolver.plan_rect(s) for s in subs]
+        t0 = time.perf_counter()
+        ps = [rectsolver.solve_rect(pl, fi).values for pl, fi in zip(plans, f)]
+        out[f"wall_{int(-kappa)}"] = np.array(time.perf_counter() - t0)
+        for sid, v in enumerate(ps):
+            idx = sample_idx(v.size, sid)
+            out[f"idx_{int(-kappa)}_{sid}"] = idx
+            out[f"val_{int(-kappa)}_{sid}"] = v[idx]
+            out[f"norm_{int(-kappa)}_{sid}"] = np.array(np.linalg.norm(v))
+            out[f"sum_{int(-kappa)}_{sid}"] = np.array(v.sum())
+            out[f"row0_{int(-kappa)}_{sid}"] = v[:1023]
+            out[f"rowlast_{int(-kappa)}_{sid}"] = v[-1023:]
+    np.savez_compressed(os.path.join(HERE, "c1.npz"), **out)
+    print("c1.npz written")
+
+
+if __name__ == "__main__":
+    for what in sys.argv[1:] or ["small", "c0", "c1"]:
+        if what == "small":
+            make_small()
+        elif what == "c1":
+            make_c1()
+        else:
+            solve_cross(what, full=(what == "c0"))

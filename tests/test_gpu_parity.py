@@ -1,0 +1,219 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden fixtures and the CPU oracle.  Tolerances (fp64):
+  transforms / single solves: 1e-12 relative L2 (rounding-different DST)
+  Schur operator applies:      1e-11 relative L2
+  full solves:                 1e-10 relative L2 and identical iteration counts
+"""
+import numpy as np
+import pytest
+
+import fftddm_oracle as O
+from conftest import load_golden, rel
+from paper_2509_23180_b200 import configs
+from rects import RECT_CASES, make
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2509_23180_b200 import ddm, krylov, rectsolver, transforms  # noqa: E402
+from paper_2509_23180_b200.errors import ConvergenceError  # noqa: E402
+
+
+def dev(x):
+    return torch.as_tensor(np.asarray(x, dtype=float), device="cuda")
+
+
+class TestTransforms:
+    @pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 8, 15, 31, 63, 64, 127, 141, 255, 511, 1023,
+                                   2047, 4095])
+    def test_apply_q_golden(self, golden_small, n):
+        pl = transforms.make_plan("DD", n, 1.0, 1.0)
+        out = transforms.apply_Q(pl, golden_small[f"dst_in_{n}"])
+        assert rel(out, golden_small[f"dst_out_{n}"]) < 1e-13
+
+    def test_known_answer(self):
+        pl = transforms.make_plan("DD", 3, 1.0, 1.0)
+        np.testing.assert_allclose(transforms.apply_Q(pl, np.array([1.0, 0.0, 0.0])),
+                                   [0.5, 1 / np.sqrt(2), 0.5], atol=1e-14)
+
+    @pytest.mark.parametrize("n", [255, 1023, 2047, 4095])
+    def test_involution_many_rows(self, n, rng):
+        pl = transforms.make_plan("DD", n, 1.0, 1.0)
+        x = dev(rng.standard_normal((37, n)))
+        y = transforms.apply_Q(pl, transforms.apply_Q(pl, x))
+        assert rel(y.cpu().numpy(), x.cpu().numpy()) < 1e-14
+
+    def test_against_oracle_torch_in_torch_out(self, rng):
+        x = rng.standard_normal((9, 1023))
+        pl = transforms.make_plan("DD", 1023, 1.0, 1.0)
+        out = transforms.apply_Q(pl, dev(x))
+        assert out.is_cuda
+        assert rel(out.cpu().numpy(), O.apply_q_dd(x)) < 1e-14
+
+
+class TestRectSolve:
+    @pytest.mark.parametrize("c", range(len(RECT_CASES)))
+    def test_golden(self, golden_small, c):
+        sub = make(RECT_CASES[c])
+        pl = rectsolver.plan_rect(sub)
+        p = rectsolver.solve_rect(pl, golden_small[f"rect_f_{c}"])
+        assert rel(p.values, golden_small[f"rect_p_{c}"]) < 1e-12
+        Av = rectsolver.apply_rect_operator(sub, golden_small[f"rect_f_{c}"])
+        np.testing.assert_array_equal(Av, golden_small[f"rect_Av_{c}"])
+
+    @pytest.mark.parametrize("m,n,kappa,half", [(1023, 1023, 0.0, ()), (1023, 1023, -10.0, ()),
+                                                (100, 2047, -3.0, ("west",)),
+                                                (300, 4095, 0.0, ("east",)), (517, 255, 7.0, ()),
+                                                (2, 1023, 0.0, ()), (1, 255, 0.0, ()),
+                                                (77, 141, 0.0, ("west", "east"))])
+    def test_against_oracle(self, m, n, kappa, half, rng):
+        sub = make((m, n, 1.0 / n, 1.0 / n, kappa, "DDDD", half))
+        f = rng.uniform(-1, 1, m * n)
+        p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f)
+        assert rel(p.values, O.solve(O.plan(sub), f)) < 1e-12
+
+    def test_c1_golden(self):
+        g = load_golden("c1")
+        for kappa in (0.0, -10.0):
+            k = int(-kappa)
+            subs = configs.batch_rects(1023, 5, kappa)
+            r = np.random.default_rng(0)
+            f = [r.uniform(-1, 1, s.size) for s in subs]
+            plans = [rectsolver.plan_rect(s) for s in subs]
+            outs = rectsolver.solve_rect_batched(plans, f)
+            for sid, o in enumerate(outs):
+                v = o.cpu().numpy()
+                assert rel(v[g[f"idx_{k}_{sid}"]], g[f"val_{k}_{sid}"]) < 1e-12
+                assert np.linalg.norm(v) == pytest.approx(float(g[f"norm_{k}_{sid}"]), rel=1e-12)
+                assert rel(v[:1023], g[f"row0_{k}_{sid}"]) < 1e-12
+                assert rel(v[-1023:], g[f"rowlast_{k}_{sid}"]) < 1e-12
+
+    @pytest.mark.parametrize("n", [1023, 2047, 4095])
+    def test_full_size_residual_and_linearity(self, n, rng):
+        """Size-independent properties at BASELINE sizes: A p = f to rounding
+        (5-point stencil on the GPU), and A^{-1}(a f + b g) = a p + b q."""
+        sub = make((n, n, 1.0 / n, 1.0 / n, -10.0, "DDDD", ()))
+        pl = rectsolver.plan_rect(sub)
+        f = dev(rng.uniform(-1, 1, sub.size))
+        g = dev(rng.uniform(-1, 1, sub.size))
+        p = rectsolver.solve_rect(pl, f).values
+        q = rectsolver.solve_rect(pl, g).values
+        Ap = rectsolver.apply_rect_operator(sub, p)
+        assert (torch.linalg.norm(Ap - f) / torch.linalg.norm(f)).item() < 1e-10
+        pq = rectsolver.solve_rect(pl, 2.0 * f - 0.5 * g).values
+        assert (torch.linalg.norm(pq - (2.0 * p - 0.5 * q)) / torch.linalg.norm(pq)).item() < 1e-13
+
+    def test_in_place_and_aliasing(self, rng):
+        sub = make((300, 1023, 1.0 / 1023, 1.0 / 1023, 0.0, "DDDD", ()))
+        pl = rectsolver.plan_rect(sub)
+        f = dev(rng.uniform(-1, 1, sub.size))
+        ref = rectsolver.solve_rect(pl, f).values.clone()
+        from paper_2509_23180_b200 import _native
+        _native.call("fd_rect_solve", pl.handle.ptr, _native.dptr(f), _native.dptr(f),
+                     _native.stream_ptr())
+        assert torch.equal(f, ref)
+
+
+class TestSchur:
+    @pytest.mark.parametrize("N", [4, 8, 15, 31])
+    @pytest.mark.parametrize("kappa", [0.0, -100.0])
+    def test_golden(self, golden_small, N, kappa):
+        tag = f"{N}_{int(-kappa)}"
+        comp = configs.cross_composite(N, kappa=kappa)
+        op = ddm.build_schur_operator(comp)
+        p = golden_small[f"x_p_{tag}"]
+        assert rel(op.schur(p), golden_small[f"x_schur_{tag}"]) < 1e-11
+        assert rel(op.preconditioned(p), golden_small[f"x_pre_{tag}"]) < 1e-11
+        assert rel(op.unpreconditioned(p), golden_small[f"x_unpre_{tag}"]) < 1e-11
+
+    def test_against_oracle_1023(self, rng):
+        comp = configs.cross_composite(1023, kappa=-100.0)
+        op = ddm.build_schur_operator(comp)
+        oo = O.Schur(comp)
+        p = rng.standard_normal(op.size)
+        assert rel(op.preconditioned(p), oo.preconditioned(p)) < 1e-11
+
+
+class TestDdmSolve:
+    @pytest.mark.parametrize("N", [4, 8, 15, 31])
+    @pytest.mark.parametrize("kappa", [0.0, -100.0])
+    def test_golden_small(self, golden_small, N, kappa):
+        tag = f"{N}_{int(-kappa)}"
+        comp = configs.cross_composite(N, kappa=kappa)
+        f, _ = configs.manufactured_rhs(comp, "sin_exp")
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+        assert rep.iterations == int(golden_small[f"x_iters_{tag}"])
+        for sid in range(5):
+            assert rel(fields[sid].values, golden_small[f"x_sol_{tag}_{sid}"]) < 1e-10
+
+    def test_c0(self):
+        g = load_golden("c0")
+        comp, f, exact, _ = configs.build_cross_case("c0")
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+        assert rep.converged
+        assert rep.iterations == int(g["iterations"]) == 38
+        num = sum(float(np.sum((fields[s].values - g[f"sol_{s}"]) ** 2)) for s in range(5))
+        den = sum(float(np.sum(g[f"sol_{s}"] ** 2)) for s in range(5))
+        assert np.sqrt(num / den) < 1e-10
+        assert configs.rel_l2(fields, exact) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-6)
+        np.testing.assert_allclose(rep.residual_history[:-1], g["history"][:-1], rtol=1e-6)
+
+    def test_second_order(self):
+        errs = []
+        for N in (71, 141, 283):
+            comp, f, exact, _ = configs.build_cross_case("c0", N=N)
+            fields, _ = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+            errs.append(configs.rel_l2(fields, exact))
+        orders = [np.log(errs[i] / errs[i + 1]) / np.log(2) for i in range(2)]
+        assert all(1.9 < o < 2.1 for o in orders), orders
+
+    def test_device_inputs_stay_on_device(self):
+        comp, f, _, _ = configs.build_cross_case("c0", N=15)
+        fd = {k: dev(v) for k, v in f.items()}
+        fields, rep = ddm.ddm_solve(comp, fd, krylov.GmresConfig(m=50, tol=1e-10))
+        assert all(fields[k].values.is_cuda for k in fields)
+
+    def test_not_converged_raises_with_report(self):
+        comp, f, _, _ = configs.build_cross_case("c0", N=31)
+        with pytest.raises(ConvergenceError) as ei:
+            ddm.ddm_solve(comp, f, krylov.GmresConfig(m=3, tol=1e-14, max_restarts=2))
+        assert ei.value.report is not None and not ei.value.report.converged
+        assert ei.value.report.iterations == 6
+
+    @pytest.mark.slow
+    def test_c2_golden(self):
+        g = load_golden("c2")
+        comp, f, exact, _ = configs.build_cross_case("c2")
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        for sid in range(5):
+            v = fields[sid].values
+            assert rel(v[g[f"idx_{sid}"]], g[f"val_{sid}"]) < 1e-10
+            assert np.linalg.norm(v) == pytest.approx(float(g[f"norm_{sid}"]), rel=1e-10)
+        assert configs.rel_l2(fields, exact) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-4)
+
+
+class TestGenericGmres:
+    def test_dense_golden(self, golden_small):
+        A, b = golden_small["gm_A"], golden_small["gm_b"]
+        x, rep = krylov.gmres(lambda v: A @ v, b, cfg=krylov.GmresConfig(m=7, tol=1e-12))
+        assert rep.iterations == int(golden_small["gm_iters"])
+        assert rel(x, golden_small["gm_x"]) < 1e-12
+
+    def test_identity_one_iteration(self, rng):
+        b = rng.standard_normal(50)
+        x, rep = krylov.gmres(lambda v: v, b, cfg=krylov.GmresConfig(m=10))
+        assert rep.iterations == 1
+        np.testing.assert_allclose(x, b, rtol=1e-14)
+
+    def test_native_vs_generic_same_iterations(self):
+        comp, f, _, _ = configs.build_cross_case("c0", N=31)
+        op = ddm.build_schur_operator(comp)
+        rhs = op.center_solve(f[0])
+        cfg = krylov.GmresConfig(m=50, tol=1e-10)
+        x1, r1 = krylov.gmres(op.preconditioned, rhs, cfg=cfg)
+        x2, r2 = krylov.gmres(lambda v: op.preconditioned(v), rhs, cfg=cfg)
+        assert r1.iterations == r2.iterations
+        assert rel(x1, x2) < 1e-13

@@ -1,0 +1,94 @@
+"""Pin the CPU oracle (oracle/fftddm_oracle.py) to fixtures written by the real
+reference (tests/golden/make_golden.py) and to the reference's own
+known-answer tests.  CPU only."""
+import numpy as np
+import pytest
+
+import fftddm_oracle as O
+from conftest import load_golden, rel
+from paper_2509_23180_b200 import configs
+from rects import RECT_CASES, make
+
+
+class TestKnownAnswers:
+    def test_eigenvalues_dd(self):
+        # test_transforms.py:20-27
+        np.testing.assert_allclose(O.eigenvalues_dd(1, 1.0, 1.0), [-4.0], atol=1e-15)
+        np.testing.assert_allclose(sorted(O.eigenvalues_dd(3, 1.0, 1.0)),
+                                   sorted([-4 + np.sqrt(2), -4.0, -4 - np.sqrt(2)]))
+
+    def test_apply_q_first_basis_vector(self):
+        # test_transforms.py:64-68
+        np.testing.assert_allclose(O.apply_q_dd(np.array([1.0, 0.0, 0.0])),
+                                   [0.5, 1 / np.sqrt(2), 0.5], atol=1e-14)
+
+    def test_thomas_example(self):
+        # test_rectsolver.py:31-34: tridiag(1, -2, 1) x = e1
+        beta, lower, bad = O.factor_tridiag(np.full((3, 1), -2.0), 1.0, 1e-13)
+        x = O.tridiag_solve(beta, lower, 1.0, np.array([[1.0], [0.0], [0.0]]))
+        np.testing.assert_allclose(x[:, 0], [-0.75, -0.5, -0.25])
+        assert not bad.any()
+
+    def test_one_by_one(self):
+        # test_rectsolver.py:70-73: 1x1 DD with unit spacing -> -1/4
+        sub = make((1, 1, 1.0, 1.0, 0.0, "DDDD", ()))
+        assert O.solve(O.plan(sub), np.array([1.0]))[0] == pytest.approx(-0.25)
+
+    def test_q_orthonormal(self):
+        Q = O.apply_q_dd(np.eye(17))
+        np.testing.assert_allclose(Q @ Q, np.eye(17), atol=1e-14)
+
+
+class TestAgainstReferenceFixtures:
+    @pytest.mark.parametrize("n", [1, 2, 3, 4, 7, 8, 15, 31, 63, 64, 127, 141, 255, 511, 1023,
+                                   2047, 4095])
+    def test_dst(self, golden_small, n):
+        out = O.apply_q_dd(golden_small[f"dst_in_{n}"])
+        assert rel(out, golden_small[f"dst_out_{n}"]) < 1e-15
+        lam = O.eigenvalues_dd(n, 2.5, 0.75, kappa=-0.5)
+        np.testing.assert_array_equal(lam, golden_small[f"eig_{n}"])
+
+    @pytest.mark.parametrize("c", range(len(RECT_CASES)))
+    def test_rect(self, golden_small, c):
+        sub = make(RECT_CASES[c])
+        pl = O.plan(sub)
+        if f"rect_beta_{c}" in golden_small:
+            np.testing.assert_array_equal(pl.beta, golden_small[f"rect_beta_{c}"])
+            np.testing.assert_array_equal(pl.lower, golden_small[f"rect_lower_{c}"])
+        p = O.solve(pl, golden_small[f"rect_f_{c}"])
+        np.testing.assert_array_equal(p, golden_small[f"rect_p_{c}"])
+        np.testing.assert_array_equal(O.apply_operator(sub, golden_small[f"rect_f_{c}"]),
+                                      golden_small[f"rect_Av_{c}"])
+
+    @pytest.mark.parametrize("N", [4, 8, 15, 31])
+    @pytest.mark.parametrize("kappa", [0.0, -100.0])
+    def test_cross(self, golden_small, N, kappa):
+        tag = f"{N}_{int(-kappa)}"
+        comp = configs.cross_composite(N, kappa=kappa)
+        op = O.Schur(comp)
+        p = golden_small[f"x_p_{tag}"]
+        np.testing.assert_array_equal(op.schur(p), golden_small[f"x_schur_{tag}"])
+        np.testing.assert_array_equal(op.preconditioned(p), golden_small[f"x_pre_{tag}"])
+        np.testing.assert_array_equal(op.unpreconditioned(p), golden_small[f"x_unpre_{tag}"])
+        f, _ = configs.manufactured_rhs(comp, "sin_exp")
+        fields, rep = O.ddm_solve(comp, f, m=50, tol=1e-10)
+        assert rep.iterations == int(golden_small[f"x_iters_{tag}"])
+        np.testing.assert_allclose(rep.residual_history, golden_small[f"x_hist_{tag}"],
+                                   rtol=1e-9, atol=0)
+        for sid in range(5):
+            assert rel(fields[sid], golden_small[f"x_sol_{tag}_{sid}"]) < 1e-14
+
+    def test_gmres_dense(self, golden_small):
+        A, b = golden_small["gm_A"], golden_small["gm_b"]
+        x, rep = O.gmres(lambda v: A @ v, b, m=7, tol=1e-12)
+        assert rep.iterations == int(golden_small["gm_iters"])
+        assert rel(x, golden_small["gm_x"]) < 1e-13
+
+    def test_c0_full(self):
+        g = load_golden("c0")
+        comp, f, exact, meta = configs.build_cross_case("c0")
+        fields, rep = O.ddm_solve(comp, f, m=50, tol=1e-10)
+        assert rep.iterations == int(g["iterations"]) == 38
+        for sid in range(5):
+            assert rel(fields[sid], g[f"sol_{sid}"]) < 1e-13
+        assert configs.rel_l2(fields, exact) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-9)
