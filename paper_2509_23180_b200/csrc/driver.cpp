@@ -141,6 +141,7 @@ static SolveJob job_of(const Plan *p, const double *in, double *out) {
     j.alpha = 1.0;
     j.beta = 0.0;
     j.other = nullptr;
+    j.ws = const_cast<Workspace *>(&p->ws);
     return j;
 }
 

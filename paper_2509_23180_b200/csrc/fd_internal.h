@@ -41,12 +41,16 @@ struct Error {
 struct PlanDev {
     int m, n, R, nb;
     double off;          // delta_x: constant off-diagonal of the sweep system
+    double mod_w, mod_e; // sweep-axis end modifiers on rows 0 and m-1
     double scale;        // sqrt(2/(n+1)): orthonormal DST-I factor
     const int *ex_off;   // [n]
     const int *ex_len;   // [n]
     const double *ex;    // [sum ex_len][4]: l, 1/beta, beta, P(block-relative)
     const double *cv;    // [n][4]: l_inf, 1/beta_inf, beta_inf, 1/(-l_inf)
     const double *last;  // [n][2]: beta_{m-1}, 1/beta_{m-1}
+    const double *mode;  // [n][8]: l_inf, 1/b_inf, b_inf, 1/(-l_inf), b_last, lambda, ex_off, ex_len (int64 bits)
+    int ecap;            // rows [0, ecap) of every mode also stored row-major (coalesced):
+    const double *dl, *dib, *db;   // [ecap][n] lower, 1/beta, beta
     const double *blk;   // [nb][3][n]: Pe, xi_s, Q per block and mode
     double *ye;          // [nb][n] pass-1 local forward value at block end -> Y carries
     double *fs;          // [nb][n] pass-1 local backward value at block start -> X carries
@@ -55,6 +59,26 @@ struct PlanDev {
 };
 
 enum Transform { kDense = 0, kFFT = 1 };
+
+// grow-only device scratch (block carries of the persistent solve)
+struct Workspace {
+    double *ptr = nullptr;
+    size_t cap = 0;
+    double *get(size_t count) {
+        if (count > cap) {
+            if (ptr) cudaFree(ptr);
+            ptr = nullptr;
+            cap = 0;
+            if (cudaMalloc(&ptr, count * sizeof(double)) != cudaSuccess)
+                throw Error{FD_ERR_CUDA, "workspace allocation failed"};
+            cap = count;
+        }
+        return ptr;
+    }
+    ~Workspace() {
+        if (ptr) cudaFree(ptr);
+    }
+};
 
 struct Plan {
     int device;
@@ -65,6 +89,7 @@ struct Plan {
     long long explicit_rows;
     PlanDev dev;
     std::vector<void *> allocs;
+    Workspace ws;
 };
 
 // one job of a batched rectangle launch
@@ -75,6 +100,7 @@ struct SolveJob {
     // pass-2 epilogue: out = alpha * x + beta * other  (other may be null)
     double alpha, beta;
     const double *other;
+    Workspace *ws;   // host-side: scratch owner for the batch (unused on device)
 };
 
 constexpr int kMaxJobs = 8;
@@ -88,6 +114,7 @@ struct JobList {
 int rows_per_block(int n);
 int transform_kind(int n);
 void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s);
+bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,
                      const double *dense, cudaStream_t s);
 const double2 *twiddles_for(int device, int n);

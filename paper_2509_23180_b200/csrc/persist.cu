@@ -1,0 +1,762 @@
+// Persistent fused rectangle solve for the FFT transform lengths (n + 1 = 2^p).
+//
+// One cooperative launch per batched solve, one CTA set resident on every SM:
+//   phase 1  rows of all jobs (rectangles) are split evenly over the CTAs; each
+//            CTA streams its row groups global -> shared with TMA bulk copies
+//            (cp.async.bulk + mbarrier; the next group is in flight while the
+//            current one is transformed), DST-I's them (radix-16 Stockham FFT
+//            of packed row pairs) and runs the local forward elimination of its
+//            block; yhat goes to the output buffer, the block scalars
+//            (yhat_e, F_s, P_e, xi_s, Q) to the carry workspace.
+//   grid sync
+//   phase 2  carries: per (rectangle, 32 modes) one warp runs the block
+//            recurrences Y_b = yhat_e + P_e Y_{b-1},
+//            X_b = F_s + Y_{b-1} xi_s + Q X_{b+1} (L2-resident data).
+//   grid sync
+//   phase 3  per CTA, groups descending: TMA-streamed yhat rows, carry fix-up
+//            y_i = yhat_i + P_i Y_{b-1}, the reference back-substitution
+//            x_i = (y_i - delta x_{i+1}) / beta_i (rectsolver.py:88-90) with
+//            x_{e+1} = X_{b+1}, inverse DST-I, epilogue out = alpha x + beta o.
+// Between the phases yhat (8 B/pt) normally stays in the 126 MB L2 for the
+// BASELINE config-1 batch; the algorithmic traffic is 32 B/pt either way.
+#include <cooperative_groups.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <set>
+
+#include "dst_device.cuh"
+#include "fd_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace fd {
+
+struct PJob {
+    PlanDev p;
+    const double *in;
+    double *out;
+    double alpha, beta;
+    const double *other;
+    long long row0;   // first global row of the job
+    int c_first;      // first virtual range touching the job
+    int nblk;         // carry blocks of the job
+    int blk_base;     // global index of its first block
+};
+
+constexpr int kMaxPJobs = 8;
+constexpr int kMaxSegs = 48;
+constexpr int kMaxRowsPerBlock = 256;   // keeps block products P_e far from underflow
+constexpr int kCarryVals = 7;           // yhat_e, F_s, P_e, xi_s, Q, Y, X
+
+struct PList {
+    int count;
+    int V;               // virtual row ranges (carry blocks)
+    long long total_rows;
+    double *carry;       // [total_blocks][kCarryVals][n]
+    int n;
+    unsigned long long *tstamp;   // optional [gridDim][8] phase timestamps (FD_PHASE_TIMING)
+    double *bsave;       // [gridDim][bstride][n] beta checkpoints (phase 1 -> phase 3)
+    int bstride;
+    PJob job[kMaxPJobs];
+};
+
+struct Seg {
+    int job, s, e, blk, ngroups, item0;
+};
+
+// --- TMA bulk copy + mbarrier helpers --------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Issue the copy of rows [g0, g0+rows) of an (m, n) array into `stg`; the data
+// lands at stg + off where off = (address mod 16) / 8.  The bulk copy is
+// widened to 16-byte boundaries; only the last group of an array, whose end may
+// be the end of the allocation, leaves an 8-byte tail that thread 0 fetches
+// into a register (returned) and stores once the copy has landed.
+struct Tail {
+    double v;
+    int idx;   // -1: none
+};
+__device__ __forceinline__ Tail issue_rows(double *stg, const double *base, int g0, int rows, int n,
+                                           int m, uint64_t *bar) {
+    const uintptr_t start = reinterpret_cast<uintptr_t>(base + size_t(g0) * n);
+    const uintptr_t end = start + uintptr_t(rows) * n * sizeof(double);
+    const uintptr_t a = start & ~uintptr_t(15);
+    const bool last = (g0 + rows >= m);
+    const uintptr_t e = last ? (end & ~uintptr_t(15)) : ((end + 15) & ~uintptr_t(15));
+    const uint32_t bytes = uint32_t(e - a);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, bytes);
+    tma_load_1d(stg, reinterpret_cast<const void *>(a), bytes, bar);
+    Tail t{0.0, -1};
+    if (end != e) {
+        t.v = __ldcg(reinterpret_cast<const double *>(e));
+        t.idx = int((e - a) / 8);
+    }
+    return t;
+}
+// true when the group's copy leaves a tail (identical on every thread)
+__device__ __forceinline__ bool has_tail(const double *base, int g0, int rows, int n, int m) {
+    const uintptr_t end = reinterpret_cast<uintptr_t>(base + size_t(g0 + rows) * n);
+    return (g0 + rows >= m) && (end & 15);
+}
+
+__device__ __forceinline__ int stg_off(const double *base, int g0, int n) {
+    return int((reinterpret_cast<uintptr_t>(base + size_t(g0) * n) & 15) >> 3);
+}
+
+// Per-mode record (PlanDev::mode, 64 B): l_inf, 1/beta_inf, beta_inf,
+// 1/(-l_inf), beta_{m-1}, lambda_k, explicit offset, explicit length.
+struct ModeRec {
+    double l_inf, ib_inf, b_inf, inv_nl, b_last, lam;
+    int off, len;
+    __device__ void load(const PlanDev &p, int k) {
+        const double2 *r = reinterpret_cast<const double2 *>(p.mode) + 4 * k;
+        const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3);
+        l_inf = a.x;
+        ib_inf = a.y;
+        b_inf = b.x;
+        inv_nl = b.y;
+        b_last = c.x;
+        lam = c.y;
+        off = int(__double_as_longlong(d.x));
+        len = int(__double_as_longlong(d.y));
+    }
+};
+
+// beta_i of mode k from the plan's tables (used once per segment start)
+__device__ __forceinline__ double beta_at(const PlanDev &p, const ModeRec &c, int k, int i) {
+    if (i == p.m - 1) return c.b_last;
+    if (i < p.ecap) return __ldg(p.db + size_t(i) * p.n + k);
+    if (i < c.len) return __ldg(p.ex + 4 * (size_t(c.off) + i) + 2);
+    return c.b_inf;
+}
+
+// Diagonal of row i: lambda (+ west modifier on row 0) (+ east on row m-1),
+// summed in the reference's order (rectsolver.py:125,132-133).
+__device__ __forceinline__ double diag_at(const PlanDev &p, double lam, int i) {
+    double d = lam;
+    if (i == 0) d = __dadd_rn(d, p.mod_w);
+    if (i == p.m - 1) d = __dadd_rn(d, p.mod_e);
+    return d;
+}
+
+constexpr int kPersistThreads = 512;   // one CTA per SM, 128 registers per thread
+
+template <int LG>
+struct PCfg {
+    using F = FftDst<LG, kPersistThreads>;
+    static constexpr int NT = F::NT, G = F::G;
+    static constexpr int MPT = (F::N - 1 + NT - 1) / NT;
+    static constexpr size_t XBUF = F::SMEM;
+    static constexpr size_t STG = (size_t(G) * (F::N - 1) + 4) * sizeof(double);
+    static constexpr size_t TWS = (16 + 256 + 256 + 16) * sizeof(double2);
+    static constexpr size_t SMEM = XBUF + STG + TWS;
+};
+
+template <int LG>
+__global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_constant__ PList pl) {
+    using F = typename PCfg<LG>::F;
+    using FL = Fft2<LG, kPersistThreads>;
+    using C = PCfg<LG>;
+    constexpr int NT = C::NT, G = C::G, MPT = C::MPT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double2 *xbuf = reinterpret_cast<double2 *>(smem_raw);
+    double *rowbuf = reinterpret_cast<double *>(smem_raw);            // aliases xbuf
+    double *stg = reinterpret_cast<double *>(smem_raw + C::XBUF);
+    double2 *tw16 = reinterpret_cast<double2 *>(smem_raw + C::XBUF + C::STG);
+    double2 *tw256 = tw16 + 16, *twla = tw256 + 256, *twlb = twla + 256;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ Seg segs[kMaxSegs];
+    __shared__ int nseg_s, nitems_s;
+
+    const int tid = threadIdx.x;
+    const int n = pl.n;
+    const int pr = tid / F::T, t = tid % F::T;
+    cg::grid_group grid = cg::this_grid();
+    auto stamp = [&](int slot) {
+        if (pl.tstamp && tid == 0) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+            pl.tstamp[blockIdx.x * 8 + slot] = g;
+        }
+    };
+    stamp(0);
+
+    if (tid == 0) {
+        int ns = 0, items = 0;
+        for (int v = blockIdx.x; v < pl.V; v += gridDim.x) {
+            const long long lo = pl.total_rows * v / pl.V, hi = pl.total_rows * (v + 1) / pl.V;
+            for (int j = 0; j < pl.count; ++j) {
+                const long long r0 = pl.job[j].row0, r1 = r0 + pl.job[j].p.m;
+                if (r0 < hi && r1 > lo && ns < kMaxSegs) {
+                    Seg sg;
+                    sg.job = j;
+                    sg.s = int(max(lo, r0) - r0);
+                    sg.e = int(min(hi, r1) - r0) - 1;
+                    sg.blk = pl.job[j].blk_base + (v - pl.job[j].c_first);
+                    sg.ngroups = (sg.e - sg.s + G) / G;
+                    sg.item0 = items;
+                    items += sg.ngroups;
+                    segs[ns++] = sg;
+                }
+            }
+        }
+        nseg_s = ns;
+        nitems_s = items;
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    {   // twiddle base tables from the exact L-point table (all jobs share n)
+        constexpr int L = F::L, NBL = L / F::RL;
+        const double2 *tw = pl.job[0].p.tw;
+        for (int q = tid; q < 16; q += NT) tw16[q] = __ldg(tw + q * (L / 256));
+        if constexpr (L >= 4096)
+            for (int q = tid; q < 256; q += NT) tw256[q] = __ldg(tw + q * (L / 4096));
+        for (int q = tid; q < 256; q += NT) twla[q] = __ldg(tw + q * (NBL <= 256 ? 1 : 16));
+        for (int q = tid; q < 16; q += NT) twlb[q] = __ldg(tw + q);
+    }
+    __syncthreads();
+    const TwPow tws{tw16, tw256, twla, twlb};
+    const int nseg = nseg_s, nitems = nitems_s;
+    uint32_t parity = 0;
+    // per-CTA beta checkpoints: slot it (phase-1 item) = beta at the item's last
+    // row; slot bstride-1-si = beta_{s-1} of segment si
+    double *bsave = pl.bsave + size_t(blockIdx.x) * pl.bstride * n;
+
+    auto item_of = [&](int it, int &si, int &g0, int &rows, bool desc) {
+        si = 0;
+        while (si + 1 < nseg && it >= segs[si + 1].item0) ++si;
+        const Seg &sg = segs[si];
+        const int gi = it - sg.item0;
+        const int gg = desc ? (sg.ngroups - 1 - gi) : gi;
+        g0 = sg.s + gg * G;
+        rows = min(G, sg.e - g0 + 1);
+    };
+
+    // ===================== phase 1: DST + local forward elimination ===================
+    {
+        // per mode: yhat, pi (running product), F_s, sum pi^2/beta, beta of the
+        // previous row, -l_s (P_i = -l_s pi_i)
+        double ys[MPT], pis[MPT], fss[MPT], s2s[MPT], bps[MPT], ccs[MPT];
+        Tail tail{0.0, -1};
+        if (tid == 0 && nitems > 0) {
+            int si, g0, rows;
+            item_of(0, si, g0, rows, false);
+            const PJob &J = pl.job[segs[si].job];
+            tail = issue_rows(stg, J.in, g0, rows, n, J.p.m, &bar);
+        }
+#pragma unroll 1
+        for (int it = 0; it < nitems; ++it) {
+            int si, g0, rows;
+            item_of(it, si, g0, rows, false);
+            const Seg sg = segs[si];
+            const PJob &J = pl.job[sg.job];
+            const PlanDev &p = J.p;
+            const double off = p.off;
+            mbar_wait(&bar, parity);
+            parity ^= 1u;
+            if (has_tail(J.in, g0, rows, n, p.m)) {
+                if (tid == 0) stg[tail.idx] = tail.v;
+                __syncthreads();
+            }
+            const int so = stg_off(J.in, g0, n);
+            {
+                const int ra = 2 * pr, rb = 2 * pr + 1;
+                double2 *buf = xbuf + pr * F::PADL;
+                double2 v[16];
+                FL::load(v, ra < rows ? stg + so + ra * n : nullptr, rb < rows ? stg + so + rb * n : nullptr, t);
+                __syncthreads();   // staging consumed
+                if (tid == 0 && it + 1 < nitems) {
+                    int si2, g2, rows2;
+                    item_of(it + 1, si2, g2, rows2, false);
+                    const PJob &J2 = pl.job[segs[si2].job];
+                    tail = issue_rows(stg, J2.in, g2, rows2, n, J2.p.m, &bar);
+                }
+                FL::store(buf, v, t);
+                FL::template mids<F::NMID, 16>(buf, tws, t);
+                double *oa = rowbuf + ra * n, *ob = rowbuf + rb * n;
+                const bool va = ra < rows, vb = rb < rows;
+                FL::last(buf, tws, t, p.scale, [&](int k, double a, double b) {
+                    if (va) oa[k] = a;
+                    if (vb) ob[k] = b;
+                });
+                __syncthreads();
+            }
+            const bool first = (g0 == sg.s), last = (g0 + rows - 1 == sg.e);
+#pragma unroll
+            for (int u = 0; u < MPT; ++u) {
+                const int k = tid + u * NT;
+                if (k >= n) continue;
+                ModeRec c;
+                c.load(p, k);
+                double y = ys[u], w = pis[u], f = fss[u], s2 = s2s[u], bp = bps[u];
+                if (first) {
+                    bp = g0 > 0 ? beta_at(p, c, k, g0 - 1) : 0.0;
+                    __stcg(bsave + size_t(pl.bstride - 1 - si) * n + k, bp);
+                }
+#pragma unroll
+                for (int rr = 0; rr < G; ++rr) {
+                    if (rr >= rows) break;
+                    const int i = g0 + rr;
+                    const double r = rowbuf[rr * n + k];
+                    double l, ib;
+                    if (i < c.len) {
+                        // transient row: the reference factorisation, recomputed
+                        // bitwise (rectsolver.py:72-73), no table traffic
+                        const double d = diag_at(p, c.lam, i);
+                        double b;
+                        if (i == 0) {
+                            l = 0.0;
+                            b = d;
+                        } else {
+                            l = __ddiv_rn(off, bp);
+                            b = __dsub_rn(d, __dmul_rn(off, l));
+                        }
+                        ib = 1.0 / b;
+                        bp = b;
+                    } else {
+                        l = c.l_inf;
+                        ib = (i == p.m - 1) ? 1.0 / c.b_last : c.ib_inf;
+                    }
+                    if (first && rr == 0) {
+                        y = r;
+                        w = 1.0;
+                        f = 0.0;
+                        s2 = 0.0;
+                        ccs[u] = (i == 0) ? 0.0 : -l;   // P_i = -l_s pi_i
+                    } else {
+                        y = __dsub_rn(r, __dmul_rn(l, y));   // rectsolver.py:86
+                        w = -l * w;
+                    }
+                    const double W = w * ib;
+                    f = fma(y, W, f);
+                    s2 = fma(w, W, s2);
+                    J.out[size_t(i) * n + k] = y;
+                }
+                const int ie = g0 + rows - 1;
+                const double bend = ie < c.len ? bp : (ie == p.m - 1 ? c.b_last : c.b_inf);
+                __stcg(bsave + size_t(it) * n + k, bend);
+                ys[u] = y;
+                pis[u] = w;
+                fss[u] = f;
+                s2s[u] = s2;
+                bps[u] = bp;
+                if (last) {
+                    double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
+                    const int e = sg.e;
+                    const double cc = ccs[u];
+                    // Q = pi_e * (-l_{e+1}),  l_{e+1} = delta / beta_e
+                    const double lnext = (e + 1 < c.len) ? __ddiv_rn(off, bend) : c.l_inf;
+                    const double Q = (e < p.m - 1) ? w * (-lnext) : 0.0;
+                    __stcg(cb + 0 * n, y);
+                    __stcg(cb + 1 * n, f);
+                    __stcg(cb + 2 * n, cc * w);
+                    __stcg(cb + 3 * n, cc * s2);
+                    __stcg(cb + 4 * n, Q);
+                }
+            }
+            __syncthreads();   // rowbuf consumed before the next group's FFT
+        }
+    }
+    stamp(1);
+    grid.sync();
+    stamp(2);
+
+    // ===================== phase 2: block carries =====================================
+    // One CTA per (job, 32 modes): stage the block scalars of all blocks through
+    // shared memory with every thread issuing loads, then warp 0 (lane = mode)
+    // runs the two short recurrences out of shared memory.
+    {
+        constexpr int CHB = 64;                       // blocks per staged chunk
+        double *sv = reinterpret_cast<double *>(smem_raw);   // [CHB][4][32]
+        const int chunks = (n + 31) / 32;
+        const size_t bs = size_t(kCarryVals) * n;
+        for (int item = blockIdx.x; item < pl.count * chunks; item += gridDim.x) {
+            const PJob &J = pl.job[item / chunks];
+            const int k0 = (item % chunks) * 32;
+            const double *cb = pl.carry + size_t(J.blk_base) * bs + k0;
+            double *cw = pl.carry + size_t(J.blk_base) * bs + k0;
+            const int nb = J.nblk, lane = tid & 31;
+            const bool lane_ok = (tid < 32) && (k0 + lane < n);
+            double prev = 0.0;
+            for (int c0 = 0; c0 < nb; c0 += CHB) {
+                const int cn = min(CHB, nb - c0);
+                for (int idx = tid; idx < cn * 64; idx += NT) {
+                    const int b = idx >> 6, v = (idx >> 5) & 1, kk = idx & 31;
+                    sv[(b * 4 + v) * 32 + kk] =
+                        (k0 + kk < n) ? __ldcg(cb + (c0 + b) * bs + (v ? 2 : 0) * n + kk) : 0.0;
+                }
+                __syncthreads();
+                if (lane_ok) {
+#pragma unroll 4
+                    for (int b = 0; b < cn; ++b) {
+                        const double ye = sv[(b * 4 + 0) * 32 + lane], pe = sv[(b * 4 + 1) * 32 + lane];
+                        const double y = (c0 + b == 0) ? ye : fma(pe, prev, ye);
+                        __stcg(cw + (c0 + b) * bs + 5 * n + lane, y);
+                        prev = y;
+                    }
+                }
+                __syncthreads();
+            }
+            __threadfence_block();
+            double next = 0.0;
+            for (int c1 = nb; c1 > 0; c1 -= CHB) {
+                const int c0 = max(0, c1 - CHB), cn = c1 - c0;
+                for (int idx = tid; idx < cn * 128; idx += NT) {
+                    const int b = idx >> 7, v = (idx >> 5) & 3, kk = idx & 31;
+                    const int blk = c0 + b;
+                    double val = 0.0;
+                    if (k0 + kk < n) {
+                        if (v == 0) val = __ldcg(cb + blk * bs + 1 * n + kk);
+                        else if (v == 1) val = __ldcg(cb + blk * bs + 3 * n + kk);
+                        else if (v == 2) val = __ldcg(cb + blk * bs + 4 * n + kk);
+                        else val = blk > 0 ? __ldcg(cb + (blk - 1) * bs + 5 * n + kk) : 0.0;
+                    }
+                    sv[(b * 4 + v) * 32 + kk] = val;
+                }
+                __syncthreads();
+                if (lane_ok) {
+#pragma unroll 4
+                    for (int b = cn - 1; b >= 0; --b) {
+                        const int blk = c0 + b;
+                        double x = sv[(b * 4 + 0) * 32 + lane];
+                        if (blk > 0) x = fma(sv[(b * 4 + 3) * 32 + lane], sv[(b * 4 + 1) * 32 + lane], x);
+                        if (blk < nb - 1) x = fma(sv[(b * 4 + 2) * 32 + lane], next, x);
+                        __stcg(cw + blk * bs + 6 * n + lane, x);
+                        next = x;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    stamp(3);
+    grid.sync();
+    stamp(4);
+
+    // ===================== phase 3: back-substitution + inverse DST ===================
+    {
+        double xs[MPT], yins[MPT], pcs[MPT], bnx[MPT];
+        Tail tail{0.0, -1};
+        auto beta_before = [&](int it3, int k) {   // beta_{g0-1} of phase-3 item it3 (from bsave)
+            int si, g0, rows;
+            item_of(it3, si, g0, rows, true);
+            const int gg = (g0 - segs[si].s) / G;
+            return gg > 0 ? __ldcg(bsave + size_t(segs[si].item0 + gg - 1) * n + k)
+                          : __ldcg(bsave + size_t(pl.bstride - 1 - si) * n + k);
+        };
+        if (tid == 0 && nitems > 0) {
+            int si, g0, rows;
+            item_of(0, si, g0, rows, true);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const PJob &J = pl.job[segs[si].job];
+            tail = issue_rows(stg, J.out, g0, rows, n, J.p.m, &bar);
+        }
+        if (nitems > 0) {
+#pragma unroll
+            for (int u = 0; u < MPT; ++u) {
+                const int k = tid + u * NT;
+                bnx[u] = (k < n) ? beta_before(0, k) : 0.0;
+            }
+        }
+#pragma unroll 1
+        for (int it = 0; it < nitems; ++it) {
+            int si, g0, rows;
+            item_of(it, si, g0, rows, true);
+            const Seg sg = segs[si];
+            const PJob &J = pl.job[sg.job];
+            const PlanDev &p = J.p;
+            const double off = p.off;
+            const bool top = (g0 + rows - 1 == sg.e);
+            const bool has_in = sg.blk > J.blk_base;                 // block does not start at row 0
+            const bool has_next = sg.blk < J.blk_base + J.nblk - 1;  // a block below carries X
+            mbar_wait(&bar, parity);
+            parity ^= 1u;
+            if (has_tail(J.out, g0, rows, n, p.m)) {
+                if (tid == 0) stg[tail.idx] = tail.v;
+                __syncthreads();
+            }
+            const int so = stg_off(J.out, g0, n);
+#pragma unroll
+            for (int u = 0; u < MPT; ++u) {
+                const int k = tid + u * NT;
+                if (k >= n) continue;
+                ModeRec c;
+                c.load(p, k);
+                if (top) {
+                    const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
+                    const size_t bs = size_t(kCarryVals) * n;
+                    xs[u] = has_next ? __ldcg(cb + bs + 6 * n) : 0.0;
+                    yins[u] = has_in ? __ldcg(cb - bs + 5 * n) : 0.0;
+                    pcs[u] = __ldcg(cb + 2 * n);
+                }
+                const double bstart = bnx[u];
+                if (it + 1 < nitems) bnx[u] = beta_before(it + 1, k);   // prefetch
+                double x = xs[u], Pc = pcs[u];
+                const double yin = yins[u];
+                if (g0 < c.len) {
+                    // transient rows: rebuild beta forward into rowbuf (bitwise the
+                    // reference factors), then sweep back over them
+                    double bp = bstart;
+#pragma unroll
+                    for (int rr = 0; rr < G; ++rr) {
+                        if (rr >= rows) break;
+                        const int i = g0 + rr;
+                        double b;
+                        if (i < c.len) {
+                            const double d = diag_at(p, c.lam, i);
+                            b = (i == 0) ? d : __dsub_rn(d, __dmul_rn(off, __ddiv_rn(off, bp)));
+                        } else {
+                            b = (i == p.m - 1) ? c.b_last : c.b_inf;
+                        }
+                        rowbuf[rr * n + k] = b;
+                        bp = b;
+                    }
+#pragma unroll
+                    for (int rr = G - 1; rr >= 0; --rr) {
+                        if (rr >= rows) continue;
+                        const double b = rowbuf[rr * n + k];
+                        double y = stg[so + rr * n + k];
+                        if (has_in) {
+                            y = fma(Pc, yin, y);
+                            // P_{i-1} = P_i / (-l_i) = -P_i beta_{i-1} / delta
+                            const double bm1 = rr > 0 ? rowbuf[(rr - 1) * n + k] : bstart;
+                            Pc = -Pc * bm1 / off;
+                        }
+                        x = __ddiv_rn(__dsub_rn(y, __dmul_rn(off, x)), b);   // rectsolver.py:90
+                        rowbuf[rr * n + k] = x;
+                    }
+                } else {
+#pragma unroll
+                    for (int rr = G - 1; rr >= 0; --rr) {
+                        if (rr >= rows) continue;
+                        const int i = g0 + rr;
+                        double y = stg[so + rr * n + k];
+                        if (has_in) {
+                            y = fma(Pc, yin, y);
+                            Pc *= c.inv_nl;
+                        }
+                        const double b = (i == p.m - 1) ? c.b_last : c.b_inf;
+                        x = __ddiv_rn(__dsub_rn(y, __dmul_rn(off, x)), b);   // rectsolver.py:90
+                        rowbuf[rr * n + k] = x;
+                    }
+                }
+                xs[u] = x;
+                pcs[u] = Pc;
+            }
+            __syncthreads();   // staging consumed, rowbuf complete
+            if (tid == 0 && it + 1 < nitems) {
+                int si2, g2, rows2;
+                item_of(it + 1, si2, g2, rows2, true);
+                const PJob &J2 = pl.job[segs[si2].job];
+                tail = issue_rows(stg, J2.out, g2, rows2, n, J2.p.m, &bar);
+            }
+            {
+                const int ra = 2 * pr, rb = 2 * pr + 1;
+                double2 *buf = xbuf + pr * F::PADL;
+                FL::first(buf, ra < rows ? rowbuf + ra * n : nullptr, rb < rows ? rowbuf + rb * n : nullptr, t);
+                FL::template mids<F::NMID, 16>(buf, tws, t);
+                const bool va = ra < rows, vb = rb < rows;
+                double *oa = J.out + size_t(g0 + ra) * n, *ob = J.out + size_t(g0 + rb) * n;
+                if (J.other) {
+                    const double *qa = J.other + size_t(g0 + ra) * n, *qb = J.other + size_t(g0 + rb) * n;
+                    const double al = J.alpha, be = J.beta;
+                    FL::last(buf, tws, t, p.scale, [&](int k, double a, double b) {
+                        if (va) oa[k] = fma(be, __ldg(qa + k), al * a);
+                        if (vb) ob[k] = fma(be, __ldg(qb + k), al * b);
+                    });
+                } else if (J.alpha == 1.0) {
+                    FL::last(buf, tws, t, p.scale, [&](int k, double a, double b) {
+                        if (va) oa[k] = a;
+                        if (vb) ob[k] = b;
+                    });
+                } else {
+                    const double al = J.alpha;
+                    FL::last(buf, tws, t, p.scale, [&](int k, double a, double b) {
+                        if (va) oa[k] = al * a;
+                        if (vb) ob[k] = al * b;
+                    });
+                }
+                __syncthreads();
+            }
+        }
+    }
+    stamp(5);
+}
+
+// ---------------------------------------------------------------------------
+// host launcher
+struct PersistInfo {
+    int grid = 0;
+};
+
+template <int LG>
+static int persist_grid(int device) {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) return it->second;
+    using C = PCfg<LG>;
+    FD_CUDA(cudaFuncSetAttribute((const void *)persist_kernel<LG>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    int per_sm = 0, sms = 0;
+    FD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist_kernel<LG>, C::NT, C::SMEM));
+    FD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (per_sm < 1) FD_FAIL(FD_ERR_CUDA, "persistent solve kernel cannot be resident");
+    cache[device] = per_sm * sms;
+    return per_sm * sms;
+}
+
+template <int LG>
+static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
+    using C = PCfg<LG>;
+    int device = 0;
+    FD_CUDA(cudaGetDevice(&device));
+    const int grid = persist_grid<LG>(device);
+    for (size_t j0 = 0; j0 < jobs.size(); j0 += kMaxPJobs) {
+        PList pl{};
+        pl.count = (int)std::min<size_t>(kMaxPJobs, jobs.size() - j0);
+        pl.n = jobs[j0].p.n;
+        long long total = 0;
+        for (int j = 0; j < pl.count; ++j) total += jobs[j0 + j].p.m;
+        pl.total_rows = total;
+        long long V = std::max<long long>(grid, (total + kMaxRowsPerBlock - 1) / kMaxRowsPerBlock);
+        V = std::min<long long>(V, total);
+        pl.V = (int)V;
+        auto lo = [&](long long v) { return total * v / V; };
+        auto range_of = [&](long long r) {   // largest v with lo(v) <= r
+            long long v = r * V / total;
+            while (v + 1 < V && lo(v + 1) <= r) ++v;
+            while (v > 0 && lo(v) > r) --v;
+            return v;
+        };
+        long long row0 = 0;
+        int blocks = 0;
+        for (int j = 0; j < pl.count; ++j) {
+            const SolveJob &sj = jobs[j0 + j];
+            PJob &pj = pl.job[j];
+            pj.p = sj.p;
+            pj.in = sj.in;
+            pj.out = sj.out;
+            pj.alpha = sj.alpha;
+            pj.beta = sj.beta;
+            pj.other = sj.other;
+            pj.row0 = row0;
+            const long long cf = range_of(row0), cl = range_of(row0 + sj.p.m - 1);
+            pj.c_first = (int)cf;
+            pj.nblk = (int)(cl - cf + 1);
+            pj.blk_base = blocks;
+            blocks += pj.nblk;
+            row0 += sj.p.m;
+        }
+        // items and segments per CTA (mirrors the kernel's enumeration)
+        int bstride = 1;
+        for (int c = 0; c < grid; ++c) {
+            int items = 0, segs_c = 0;
+            for (long long v = c; v < V; v += grid) {
+                const long long lo_v = lo(v), hi_v = lo(v + 1);
+                long long r0 = 0;
+                for (int j = 0; j < pl.count; ++j) {
+                    const long long r1 = r0 + jobs[j0 + j].p.m;
+                    if (r0 < hi_v && r1 > lo_v) {
+                        const long long len = std::min(hi_v, r1) - std::max(lo_v, r0);
+                        items += int((len + C::G - 1) / C::G);
+                        ++segs_c;
+                    }
+                    r0 = r1;
+                }
+            }
+            bstride = std::max(bstride, items + segs_c);
+        }
+        const size_t carry_sz = size_t(blocks) * kCarryVals * pl.n;
+        double *wsp = ws.get(carry_sz + size_t(grid) * bstride * pl.n);
+        pl.carry = wsp;
+        pl.bsave = wsp + carry_sz;
+        pl.bstride = bstride;
+        static const bool timing = getenv("FD_PHASE_TIMING") != nullptr;
+        unsigned long long *ts = nullptr;
+        if (timing) FD_CUDA(cudaMallocAsync(&ts, sizeof(unsigned long long) * 8 * grid, s));
+        pl.tstamp = ts;
+
+        void *args[] = {(void *)&pl};
+        FD_CUDA(cudaLaunchCooperativeKernel((const void *)persist_kernel<LG>, dim3(grid), dim3(C::NT), args,
+                                            C::SMEM, s));
+        if (timing) {
+            std::vector<unsigned long long> h(8 * grid);
+            FD_CUDA(cudaMemcpyAsync(h.data(), ts, h.size() * 8, cudaMemcpyDeviceToHost, s));
+            FD_CUDA(cudaStreamSynchronize(s));
+            FD_CUDA(cudaFreeAsync(ts, s));
+            unsigned long long t0 = ~0ull;
+            for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[8 * c]);
+            double mx[6] = {0}, mn[6] = {1e30, 1e30, 1e30, 1e30, 1e30, 1e30};
+            for (int c = 0; c < grid; ++c)
+                for (int k = 0; k < 6; ++k) {
+                    double v = (h[8 * c + k] - t0) * 1e-3;
+                    mx[k] = std::max(mx[k], v);
+                    mn[k] = std::min(mn[k], v);
+                }
+            if (getenv("FD_PHASE_TIMING_CTA")) {
+                std::vector<std::pair<double, int>> d1;
+                for (int c = 0; c < grid; ++c) d1.push_back({(h[8 * c + 1] - h[8 * c]) * 1e-3, c});
+                std::sort(d1.begin(), d1.end());
+                for (size_t q = 0; q < d1.size(); q += std::max<size_t>(1, d1.size() / 24)) {
+                    const int c = d1[q].second;
+                    fprintf(stderr, "  cta %3d rows [%lld,%lld) p1 %.1f us p3 %.1f us\n", c, total * c / V,
+                            total * (c + 1) / V, d1[q].first, (h[8 * c + 5] - h[8 * c + 4]) * 1e-3);
+                }
+            }
+            fprintf(stderr, "[fd phase us] start %.1f-%.1f p1end %.1f-%.1f sync1 %.1f-%.1f p2end %.1f-%.1f sync2 %.1f-%.1f end %.1f-%.1f (grid %d, V %d, rows %lld)\n",
+                    mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[3], mx[3], mn[4], mx[4], mn[5], mx[5], grid, pl.V, total);
+        }
+    }
+}
+
+bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
+    const int n = jobs[0].p.n;
+    int lg = 0;
+    while ((1 << lg) < 2 * (n + 1)) ++lg;
+    switch (lg) {
+        case 9: run_persist<9>(jobs, s, ws); return true;
+        case 10: run_persist<10>(jobs, s, ws); return true;
+        case 11: run_persist<11>(jobs, s, ws); return true;
+        case 12: run_persist<12>(jobs, s, ws); return true;
+        case 13: run_persist<13>(jobs, s, ws); return true;
+        default: return false;
+    }
+}
+
+}  // namespace fd

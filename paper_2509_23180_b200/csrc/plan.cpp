@@ -131,6 +131,7 @@ struct HostTables {
     std::vector<double> last;  // 2 per mode
     std::vector<double> blk;   // nb * 3 * n
     std::vector<int> bad_modes;
+    std::vector<double> lam;   // eigenvalues lambda_k (+ kappa)
     long long explicit_rows = 0;
 };
 
@@ -147,6 +148,7 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
     const double tol = 1e-13 * std::max(amax, off);   // rectsolver.py:135
     const int nb = (m + R - 1) / R;
     HostTables T;
+    T.lam = lam;
     T.off.resize(n);
     T.len.resize(n);
     T.cv.resize(4 * size_t(n));
@@ -299,12 +301,40 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
         d.R = R;
         d.nb = (m + R - 1) / R;
         d.off = p->delta_x;
+        d.mod_w = mod_w;
+        d.mod_e = mod_e;
         d.scale = sqrt(2.0 / (n + 1));
         d.ex_off = upload(p, T.off);
         d.ex_len = upload(p, T.len);
         d.ex = upload(p, T.ex);
         d.cv = upload(p, T.cv);
         d.last = upload(p, T.last);
+        std::vector<double> rec(8 * size_t(n));
+        for (int k = 0; k < n; ++k) {
+            double *r = &rec[8 * size_t(k)];
+            for (int c = 0; c < 4; ++c) r[c] = T.cv[4 * k + c];
+            r[4] = T.last[2 * k];
+            r[5] = T.lam[k];
+            long long o = T.off[k], l = T.len[k];
+            memcpy(&r[6], &o, 8);
+            memcpy(&r[7], &l, 8);
+        }
+        d.mode = upload(p, rec);
+        // row-major copies of the first ecap rows (the transient region of most modes)
+        d.ecap = std::min(m, 128);
+        std::vector<double> dl(size_t(d.ecap) * n), dib(size_t(d.ecap) * n), db(size_t(d.ecap) * n);
+        for (int k = 0; k < n; ++k)
+            for (int i = 0; i < d.ecap; ++i) {
+                const bool ex = i < T.len[k];
+                const double *r = &T.ex[4 * size_t(T.off[k] + (ex ? i : 0))];
+                const double b = (i == m - 1) ? T.last[2 * k] : (ex ? r[2] : T.cv[4 * k + 2]);
+                dl[size_t(i) * n + k] = ex ? r[0] : T.cv[4 * k + 0];
+                db[size_t(i) * n + k] = b;
+                dib[size_t(i) * n + k] = (i == m - 1) ? T.last[2 * k + 1] : (ex ? r[1] : T.cv[4 * k + 1]);
+            }
+        d.dl = upload(p, dl);
+        d.dib = upload(p, dib);
+        d.db = upload(p, db);
         d.blk = upload(p, T.blk);
         std::vector<double> zeros(size_t(d.nb) * n, 0.0);
         d.ye = upload(p, zeros);

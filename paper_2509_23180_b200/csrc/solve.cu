@@ -32,280 +32,9 @@
 #include <set>
 
 #include "fd_internal.h"
+#include "dst_device.cuh"
 
 namespace fd {
-
-// ---------------------------------------------------------------------------
-// complex helpers
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 w) {
-    return make_double2(fma(a.x, w.x, -a.y * w.y), fma(a.x, w.y, a.y * w.x));
-}
-// multiply by -i
-__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }
-
-#define C16_1 0.92387953251128675613  // cos(pi/8)
-#define S16_1 0.38268343236508977173  // sin(pi/8)
-#define R2 0.70710678118654752440
-
-// a * e^{-2 pi i p / 16}, p known at compile time
-template <int P>
-__device__ __forceinline__ double2 tw16(double2 a) {
-    constexpr int p = P & 15;
-    if constexpr (p == 0) return a;
-    else if constexpr (p == 4) return mul_mi(a);
-    else if constexpr (p == 8) return make_double2(-a.x, -a.y);
-    else if constexpr (p == 12) return make_double2(-a.y, a.x);
-    else if constexpr (p == 2) return make_double2(R2 * (a.x + a.y), R2 * (a.y - a.x));
-    else if constexpr (p == 6) return make_double2(R2 * (a.y - a.x), -R2 * (a.x + a.y));
-    else {
-        constexpr double c[16] = {1, C16_1, R2, S16_1, 0, -S16_1, -R2, -C16_1,
-                                  -1, -C16_1, -R2, -S16_1, 0, S16_1, R2, C16_1};
-        constexpr double s[16] = {0, S16_1, R2, C16_1, 1, C16_1, R2, S16_1,
-                                  0, -S16_1, -R2, -C16_1, -1, -C16_1, -R2, -S16_1};
-        return cmul(a, make_double2(c[p], -s[p]));
-    }
-}
-
-__device__ __forceinline__ void dft2(double2 &a, double2 &b) {
-    double2 t = a;
-    a = cadd(t, b);
-    b = csub(t, b);
-}
-// forward 4-point DFT in place, natural order
-__device__ __forceinline__ void dft4(double2 &a0, double2 &a1, double2 &a2, double2 &a3) {
-    double2 s02 = cadd(a0, a2), d02 = csub(a0, a2), s13 = cadd(a1, a3), d13 = csub(a1, a3);
-    a0 = cadd(s02, s13);
-    a2 = csub(s02, s13);
-    a1 = make_double2(d02.x + d13.y, d02.y - d13.x);
-    a3 = make_double2(d02.x - d13.y, d02.y + d13.x);
-}
-
-template <int R>
-__device__ __forceinline__ void dft(double2 (&v)[R]);
-
-template <>
-__device__ __forceinline__ void dft<2>(double2 (&v)[2]) { dft2(v[0], v[1]); }
-template <>
-__device__ __forceinline__ void dft<4>(double2 (&v)[4]) { dft4(v[0], v[1], v[2], v[3]); }
-template <>
-__device__ __forceinline__ void dft<8>(double2 (&v)[8]) {
-    // n = 2 n1 + n2, k = k1 + 4 k2
-    dft4(v[0], v[2], v[4], v[6]);
-    dft4(v[1], v[3], v[5], v[7]);
-    v[3] = tw16<2>(v[3]);
-    v[5] = tw16<4>(v[5]);
-    v[7] = tw16<6>(v[7]);
-    dft2(v[0], v[1]);
-    dft2(v[2], v[3]);
-    dft2(v[4], v[5]);
-    dft2(v[6], v[7]);
-    // X[k1 + 4 k2] sits at v[2 k1 + k2]
-    double2 t[8];
-#pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1)
-#pragma unroll
-        for (int k2 = 0; k2 < 2; ++k2) t[k1 + 4 * k2] = v[2 * k1 + k2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = t[i];
-}
-template <>
-__device__ __forceinline__ void dft<16>(double2 (&v)[16]) {
-    // n = 4 n1 + n2, k = k1 + 4 k2
-    dft4(v[0], v[4], v[8], v[12]);
-    dft4(v[1], v[5], v[9], v[13]);
-    dft4(v[2], v[6], v[10], v[14]);
-    dft4(v[3], v[7], v[11], v[15]);
-    // v[4 k1 + n2] *= W16^{n2 k1}
-    v[5] = tw16<1>(v[5]);
-    v[6] = tw16<2>(v[6]);
-    v[7] = tw16<3>(v[7]);
-    v[9] = tw16<2>(v[9]);
-    v[10] = tw16<4>(v[10]);
-    v[11] = tw16<6>(v[11]);
-    v[13] = tw16<3>(v[13]);
-    v[14] = tw16<6>(v[14]);
-    v[15] = tw16<9>(v[15]);
-    dft4(v[0], v[1], v[2], v[3]);
-    dft4(v[4], v[5], v[6], v[7]);
-    dft4(v[8], v[9], v[10], v[11]);
-    dft4(v[12], v[13], v[14], v[15]);
-    double2 t[16];
-#pragma unroll
-    for (int k1 = 0; k1 < 4; ++k1)
-#pragma unroll
-        for (int k2 = 0; k2 < 4; ++k2) t[k1 + 4 * k2] = v[4 * k1 + k2];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = t[i];
-}
-
-__device__ __forceinline__ int pad16(int q) { return q + (q >> 4); }
-
-// ---------------------------------------------------------------------------
-// Row sources / sinks.  A "row" is n contiguous doubles.
-struct GRow {   // global memory
-    const double *p;
-    __device__ double get(int j) const { return p ? __ldg(p + j) : 0.0; }
-};
-struct SRow {   // shared memory
-    const double *p;
-    __device__ double get(int j) const { return p ? p[j] : 0.0; }
-};
-
-// Sink for the transform output k in [0, n): out[k] = alpha*val + beta*other[k]
-struct OutRow {
-    double *p;
-    const double *other;
-    double alpha, beta;
-    __device__ void put(int k, double v) const {
-        if (!p) return;
-        double r = alpha * v;
-        if (other) r = fma(beta, __ldg(other + k), r);
-        p[k] = r;
-    }
-};
-struct SmemRow {
-    double *p;
-    __device__ void put(int k, double v) const {
-        if (p) p[k] = v;
-    }
-};
-
-// ---------------------------------------------------------------------------
-// DST-I of row pairs via one complex FFT of length L = 2N (N = n + 1 = 2^(LG-1)):
-// c = a + i b odd-extended, C = FFT(c) = 2 DST(b) - 2i DST(a).
-template <int LG>
-struct FftDst {
-    static constexpr int L = 1 << LG;
-    static constexpr int N = L / 2;
-    static constexpr int T = L / 16;                       // threads per pair
-    static constexpr int PAIRS = (T >= 256) ? 1 : 256 / T;
-    static constexpr int NT = PAIRS * T;
-    static constexpr int G = 2 * PAIRS;                    // rows per group
-    static constexpr int MINB = NT <= 256 ? 2 : 1;         // CTAs per SM (register cap)
-    static constexpr int PADL = L + L / 16;
-    static constexpr int NMID = (LG - 1) / 4 - 1;
-    static constexpr int RL = 1 << (LG - 4 * ((LG - 1) / 4));
-    static constexpr int NS_LAST = L / RL;
-    static constexpr size_t SMEM = size_t(PAIRS) * PADL * sizeof(double2);
-
-    template <class Src>
-    __device__ static void first_pass(double2 *buf, const Src &A, const Src &B, int t) {
-        double2 v[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            int q = t + r * (L / 16);
-            double2 c;
-            if (r < 8) {
-                c = (q == 0) ? make_double2(0.0, 0.0) : make_double2(A.get(q - 1), B.get(q - 1));
-            } else {
-                int qq = 2 * N - q;
-                c = (qq == N) ? make_double2(0.0, 0.0) : make_double2(-A.get(qq - 1), -B.get(qq - 1));
-            }
-            v[r] = c;
-        }
-        __syncthreads();   // the source rows may alias the exchange buffer
-        dft<16>(v);
-#pragma unroll
-        for (int r = 0; r < 16; ++r) buf[pad16(16 * t + r)] = v[r];
-        __syncthreads();
-    }
-
-    template <int NS>
-    __device__ static void mid_pass(double2 *buf, const double2 *__restrict__ tw, int t) {
-        constexpr int NB = L / 16;
-        double2 v[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) v[r] = buf[pad16(t + r * NB)];
-        __syncthreads();
-        const int jm = t % NS;
-        constexpr int TS = L / (NS * 16);
-#pragma unroll
-        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], __ldg(tw + jm * TS * r));
-        dft<16>(v);
-        const int idx = (t / NS) * NS * 16 + jm;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) buf[pad16(idx + r * NS)] = v[r];
-        __syncthreads();
-    }
-
-    template <int K, int NS>
-    __device__ static void mids(double2 *buf, const double2 *tw, int t) {
-        if constexpr (K > 0) {
-            mid_pass<NS>(buf, tw, t);
-            mids<K - 1, NS * 16>(buf, tw, t);
-        }
-    }
-
-    template <class Sink>
-    __device__ static void last_pass(double2 *buf, const double2 *__restrict__ tw, int t,
-                                     const Sink &outA, const Sink &outB, double scale) {
-        constexpr int NB = L / RL;
-        constexpr int PER = NB / T;
-        double2 v[PER][RL];
-#pragma unroll
-        for (int u = 0; u < PER; ++u)
-#pragma unroll
-            for (int r = 0; r < RL; ++r) v[u][r] = buf[pad16(t + u * T + r * NB)];
-        __syncthreads();   // the sink may alias the exchange buffer
-        const double sa = -0.5 * scale, sb = 0.5 * scale;
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int j = t + u * T;
-#pragma unroll
-            for (int r = 1; r < RL; ++r) v[u][r] = cmul(v[u][r], __ldg(tw + j * r));
-            dft<RL>(v[u]);
-#pragma unroll
-            for (int r = 0; r < RL; ++r) {
-                int o = j + r * NB;
-                if (o >= 1 && o < N) {
-                    outA.put(o - 1, sa * v[u][r].y);
-                    outB.put(o - 1, sb * v[u][r].x);
-                }
-            }
-        }
-    }
-
-};
-
-// ---------------------------------------------------------------------------
-// Dense DST-I (any n <= kDenseMax): out_k = scale * sum_j S[j][k] in_j,
-// S[j][k] = sin(pi (j+1)(k+1)/(n+1)) from a host-built table.
-constexpr int kDenseMax = 1024;
-struct DenseDst {
-    static constexpr int NT = 128;
-    static constexpr int G = 4;
-    static constexpr int MINB = 2;
-    static constexpr int MPT = kDenseMax / NT;
-    static constexpr size_t SMEM = size_t(G) * kDenseMax * sizeof(double);
-};
-
-// ---------------------------------------------------------------------------
-// per-mode table access (see PlanDev)
-struct ModeView {
-    int off, len;
-    double l_inf, ib_inf, b_inf, inv_nl;
-    double b_last, ib_last;
-    __device__ void load(const PlanDev &p, int k) {
-        off = __ldg(p.ex_off + k);
-        len = __ldg(p.ex_len + k);
-        const double4 c = *reinterpret_cast<const double4 *>(p.cv + 4 * k);
-        l_inf = c.x;
-        ib_inf = c.y;
-        b_inf = c.z;
-        inv_nl = c.w;
-        b_last = __ldg(p.last + 2 * k);
-        ib_last = __ldg(p.last + 2 * k + 1);
-    }
-};
-
-__device__ __forceinline__ int find_job(const JobList &jl, int bid) {
-    int j = 0;
-#pragma unroll 1
-    while (j + 1 < jl.count && bid >= jl.block_start[j + 1]) ++j;
-    return j;
-}
 
 // Forward-transform `rows` rows starting at `in` (global) into rowbuf (shared).
 template <class P>
@@ -324,10 +53,10 @@ struct FwdT<FftDst<LG>> {
         GRow B{rb < rows ? in + size_t(rb) * n : nullptr};
         double2 *buf = smem + pr * F::PADL;
         F::first_pass(buf, A, B, t);
-        F::template mids<F::NMID, 16>(buf, p.tw, t);
+        F::template mids<F::NMID, 16>(buf, TwGlobal{p.tw}, t);
         SmemRow oa{ra < rows ? rowbuf + ra * n : nullptr};
         SmemRow ob{rb < rows ? rowbuf + rb * n : nullptr};
-        F::last_pass(buf, p.tw, t, oa, ob, p.scale);
+        F::last_pass(buf, TwGlobal{p.tw}, t, oa, ob, p.scale);
         __syncthreads();
     }
 };
@@ -344,12 +73,12 @@ struct InvT<FftDst<LG>> {
         SRow B{rb < rows ? rowbuf + rb * n : nullptr};
         double2 *buf = smem + pr * F::PADL;
         F::first_pass(buf, A, B, t);
-        F::template mids<F::NMID, 16>(buf, p.tw, t);
+        F::template mids<F::NMID, 16>(buf, TwGlobal{p.tw}, t);
         OutRow oa{ra < rows ? out + size_t(ra) * n : nullptr,
                   other ? other + size_t(ra) * n : nullptr, alpha, beta};
         OutRow ob{rb < rows ? out + size_t(rb) * n : nullptr,
                   other ? other + size_t(rb) * n : nullptr, alpha, beta};
-        F::last_pass(buf, p.tw, t, oa, ob, p.scale);
+        F::last_pass(buf, TwGlobal{p.tw}, t, oa, ob, p.scale);
         __syncthreads();
     }
 };
@@ -752,6 +481,7 @@ void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
         run_solve<DenseDst>(jobs, s);
         return;
     }
+    if (jobs[0].ws && launch_persist(jobs, s, *jobs[0].ws)) return;
     switch (lg_of(n)) {
         FD_FFT_DISPATCH(9, run_solve<P>(jobs, s))
         FD_FFT_DISPATCH(10, run_solve<P>(jobs, s))
