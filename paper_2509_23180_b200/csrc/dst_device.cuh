@@ -300,6 +300,17 @@ __device__ __forceinline__ void apply_powers(double2 (&v)[R], double2 w) {
     }
 }
 
+// Barrier over the T threads of one row pair: a warp sync for a single-warp
+// pair, else a named barrier (ids 1..15; id 0 is __syncthreads).
+template <int T>
+__device__ __forceinline__ void pair_sync(int pr) {
+    if constexpr (T <= 32) {
+        __syncwarp();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + pr), "r"(T) : "memory");
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Lean variant for the persistent kernel: identical arithmetic to FftDst, with
 // the padded addresses hoisted out of the radix loops (every stride is a
@@ -341,22 +352,23 @@ struct Fft2 {
             for (int r = 0; r < 16; ++r) v[r] = make_double2(0.0, 0.0);
         }
     }
-    __device__ static void store(double2 *buf, double2 (&v)[16], int t) {
+    __device__ static void store(double2 *buf, double2 (&v)[16], int t, int pr) {
         dft<16>(v);
         double2 *w = buf + 17 * t;   // pad16(16 t + r) = 17 t + r
 #pragma unroll
         for (int r = 0; r < 16; ++r) w[r] = v[r];
-        __syncthreads();
+        pair_sync<T>(pr);
     }
-    __device__ static void first(double2 *buf, const double *A, const double *B, int t) {
+    // source rows (shared memory) may alias this pair's exchange buffer only
+    __device__ static void first(double2 *buf, const double *A, const double *B, int t, int pr) {
         double2 v[16];
         load(v, A, B, t);
-        __syncthreads();   // the source rows may alias the exchange buffer
-        store(buf, v, t);
+        pair_sync<T>(pr);
+        store(buf, v, t, pr);
     }
 
     template <int NS>
-    __device__ static void mid(double2 *buf, const TwPow &tw, int t) {
+    __device__ static void mid(double2 *buf, const TwPow &tw, int t, int pr) {
         constexpr int NB = L / 16, RS = NB + NB / 16;
         static_assert(NS == 16 || NS == 256, "mid pass strides");
         double2 v[16];
@@ -365,27 +377,28 @@ struct Fft2 {
         for (int r = 0; r < 16; ++r) v[r] = rd[r * RS];
         const int jm = t % NS;
         const double2 w = (NS == 16) ? tw.m16[jm] : tw.m256[jm];
-        __syncthreads();
+        pair_sync<T>(pr);
         apply_powers<16>(v, w);
         dft<16>(v);
         double2 *wr = buf + pad16((t / NS) * NS * 16 + jm);
         constexpr int WS = NS + NS / 16;
 #pragma unroll
         for (int r = 0; r < 16; ++r) wr[r * WS] = v[r];
-        __syncthreads();
+        pair_sync<T>(pr);
     }
 
     template <int K, int NS>
-    __device__ static void mids(double2 *buf, const TwPow &tw, int t) {
+    __device__ static void mids(double2 *buf, const TwPow &tw, int t, int pr) {
         if constexpr (K > 0) {
-            mid<NS>(buf, tw, t);
-            mids<K - 1, NS * 16>(buf, tw, t);
+            mid<NS>(buf, tw, t, pr);
+            mids<K - 1, NS * 16>(buf, tw, t, pr);
         }
     }
 
     // last pass; sink(k, a_val, b_val) receives output k in [0, n) of rows A and B
+    // the sink may alias the exchange buffer of this pair only
     template <class Sink>
-    __device__ static void last(double2 *buf, const TwPow &tw, int t, double scale, const Sink &sink) {
+    __device__ static void last(double2 *buf, const TwPow &tw, int t, int pr, double scale, const Sink &sink) {
         constexpr int NB = L / RL, PER = NB / T, RS = NB + NB / 16, US = T + T / 16;
         double2 v[PER][RL];
         const double2 *rd = buf + pad16(t);
@@ -393,7 +406,7 @@ struct Fft2 {
         for (int u = 0; u < PER; ++u)
 #pragma unroll
             for (int r = 0; r < RL; ++r) v[u][r] = rd[u * US + r * RS];
-        __syncthreads();   // the sink may alias the exchange buffer
+        pair_sync<T>(pr);
         const double sa = -0.5 * scale, sb = 0.5 * scale;
 #pragma unroll
         for (int u = 0; u < PER; ++u) {

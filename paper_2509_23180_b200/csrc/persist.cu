@@ -156,6 +156,10 @@ struct ModeRec {
     }
 };
 
+__device__ __forceinline__ double mode_lam(const PlanDev &p, int k) { return __ldg(p.mode + 8 * size_t(k) + 5); }
+__device__ __forceinline__ double mode_blast(const PlanDev &p, int k) { return __ldg(p.mode + 8 * size_t(k) + 4); }
+__device__ __forceinline__ double mode_binf(const PlanDev &p, int k) { return __ldg(p.mode + 8 * size_t(k) + 2); }
+
 // beta_i of mode k from the plan's tables (used once per segment start)
 __device__ __forceinline__ double beta_at(const PlanDev &p, const ModeRec &c, int k, int i) {
     if (i == p.m - 1) return c.b_last;
@@ -194,7 +198,13 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
     constexpr int NT = C::NT, G = C::G, MPT = C::MPT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double2 *xbuf = reinterpret_cast<double2 *>(smem_raw);
-    double *rowbuf = reinterpret_cast<double *>(smem_raw);            // aliases xbuf
+    // group row rr lives inside the exchange buffer of its pair (rr / 2)
+    auto rowp = [&](int rr) { return reinterpret_cast<double *>(xbuf + (rr >> 1) * F::PADL) + (rr & 1) * pl.n; };
+    // two spare rows per pair region (4.25 n doubles each): phase-3 transient 1/beta
+    static_assert(F::PADL * 2 >= 4 * F::N, "pair region holds 4 rows");
+    auto auxp = [&](int rr) {
+        return reinterpret_cast<double *>(xbuf + (rr >> 1) * F::PADL) + (2 + (rr & 1)) * pl.n;
+    };
     double *stg = reinterpret_cast<double *>(smem_raw + C::XBUF);
     double2 *tw16 = reinterpret_cast<double2 *>(smem_raw + C::XBUF + C::STG);
     double2 *tw256 = tw16 + 16, *twla = tw256 + 256, *twlb = twla + 256;
@@ -271,6 +281,8 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
         // per mode: yhat, pi (running product), F_s, sum pi^2/beta, beta of the
         // previous row, -l_s (P_i = -l_s pi_i)
         double ys[MPT], pis[MPT], fss[MPT], s2s[MPT], bps[MPT], ccs[MPT];
+        double cl[MPT], cib[MPT], cbl[MPT], cibl[MPT];   // l_inf, 1/beta_inf, beta_{m-1}, 1/beta_{m-1}
+        int clen[MPT];
         Tail tail{0.0, -1};
         if (tid == 0 && nitems > 0) {
             int si, g0, rows;
@@ -305,38 +317,48 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                     const PJob &J2 = pl.job[segs[si2].job];
                     tail = issue_rows(stg, J2.in, g2, rows2, n, J2.p.m, &bar);
                 }
-                FL::store(buf, v, t);
-                FL::template mids<F::NMID, 16>(buf, tws, t);
-                double *oa = rowbuf + ra * n, *ob = rowbuf + rb * n;
+                FL::store(buf, v, t, pr);
+                FL::template mids<F::NMID, 16>(buf, tws, t, pr);
+                double *oa = rowp(ra), *ob = rowp(rb);   // pair-local rows
                 const bool va = ra < rows, vb = rb < rows;
-                FL::last(buf, tws, t, p.scale, [&](int k, double a, double b) {
+                FL::last(buf, tws, t, pr, p.scale, [&](int k, double a, double b) {
                     if (va) oa[k] = a;
                     if (vb) ob[k] = b;
                 });
-                __syncthreads();
+                __syncthreads();   // all rows of the group transformed
             }
             const bool first = (g0 == sg.s), last = (g0 + rows - 1 == sg.e);
+            double *outg = J.out + size_t(g0) * n;
+            const int mlast = p.m - 1;
 #pragma unroll
             for (int u = 0; u < MPT; ++u) {
                 const int k = tid + u * NT;
                 if (k >= n) continue;
-                ModeRec c;
-                c.load(p, k);
                 double y = ys[u], w = pis[u], f = fss[u], s2 = s2s[u], bp = bps[u];
                 if (first) {
+                    ModeRec c;
+                    c.load(p, k);
+                    cl[u] = c.l_inf;
+                    cib[u] = c.ib_inf;
+                    cbl[u] = c.b_last;
+                    cibl[u] = 1.0 / c.b_last;
+                    clen[u] = c.len;
                     bp = g0 > 0 ? beta_at(p, c, k, g0 - 1) : 0.0;
                     __stcg(bsave + size_t(pl.bstride - 1 - si) * n + k, bp);
                 }
+                const int len = clen[u];
+                const double l_inf = cl[u], ib_inf = cib[u];
+                const double cbinf = mode_binf(p, k);
 #pragma unroll
                 for (int rr = 0; rr < G; ++rr) {
                     if (rr >= rows) break;
                     const int i = g0 + rr;
-                    const double r = rowbuf[rr * n + k];
+                    const double r = rowp(rr)[k];
                     double l, ib;
-                    if (i < c.len) {
+                    if (i < len) {
                         // transient row: the reference factorisation, recomputed
                         // bitwise (rectsolver.py:72-73), no table traffic
-                        const double d = diag_at(p, c.lam, i);
+                        const double d = diag_at(p, mode_lam(p, k), i);
                         double b;
                         if (i == 0) {
                             l = 0.0;
@@ -348,8 +370,8 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                         ib = 1.0 / b;
                         bp = b;
                     } else {
-                        l = c.l_inf;
-                        ib = (i == p.m - 1) ? 1.0 / c.b_last : c.ib_inf;
+                        l = l_inf;
+                        ib = (i == mlast) ? cibl[u] : ib_inf;
                     }
                     if (first && rr == 0) {
                         y = r;
@@ -364,10 +386,10 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                     const double W = w * ib;
                     f = fma(y, W, f);
                     s2 = fma(w, W, s2);
-                    J.out[size_t(i) * n + k] = y;
+                    outg[rr * n + k] = y;
                 }
                 const int ie = g0 + rows - 1;
-                const double bend = ie < c.len ? bp : (ie == p.m - 1 ? c.b_last : c.b_inf);
+                const double bend = ie < len ? bp : (ie == mlast ? cbl[u] : cbinf);
                 __stcg(bsave + size_t(it) * n + k, bend);
                 ys[u] = y;
                 pis[u] = w;
@@ -379,7 +401,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                     const int e = sg.e;
                     const double cc = ccs[u];
                     // Q = pi_e * (-l_{e+1}),  l_{e+1} = delta / beta_e
-                    const double lnext = (e + 1 < c.len) ? __ddiv_rn(off, bend) : c.l_inf;
+                    const double lnext = (e + 1 < len) ? __ddiv_rn(off, bend) : l_inf;
                     const double Q = (e < p.m - 1) ? w * (-lnext) : 0.0;
                     __stcg(cb + 0 * n, y);
                     __stcg(cb + 1 * n, f);
@@ -396,70 +418,66 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
     stamp(2);
 
     // ===================== phase 2: block carries =====================================
-    // One CTA per (job, 32 modes): stage the block scalars of all blocks through
-    // shared memory with every thread issuing loads, then warp 0 (lane = mode)
-    // runs the two short recurrences out of shared memory.
+    // One CTA per (job, 32 modes): all blocks' scalars are staged through shared
+    // memory in one round trip (every thread issues loads), warp 0 (lane = mode)
+    // runs both short recurrences out of shared memory, then Y and X go back.
     {
-        constexpr int CHB = 64;                       // blocks per staged chunk
-        double *sv = reinterpret_cast<double *>(smem_raw);   // [CHB][4][32]
+        constexpr int CHB = 96;                               // blocks per staged chunk
+        double *sv = reinterpret_cast<double *>(smem_raw);   // [CHB][7][32]
         const int chunks = (n + 31) / 32;
         const size_t bs = size_t(kCarryVals) * n;
         for (int item = blockIdx.x; item < pl.count * chunks; item += gridDim.x) {
             const PJob &J = pl.job[item / chunks];
             const int k0 = (item % chunks) * 32;
-            const double *cb = pl.carry + size_t(J.blk_base) * bs + k0;
-            double *cw = pl.carry + size_t(J.blk_base) * bs + k0;
+            double *cb = pl.carry + size_t(J.blk_base) * bs + k0;
             const int nb = J.nblk, lane = tid & 31;
             const bool lane_ok = (tid < 32) && (k0 + lane < n);
-            double prev = 0.0;
-            for (int c0 = 0; c0 < nb; c0 += CHB) {
-                const int cn = min(CHB, nb - c0);
-                for (int idx = tid; idx < cn * 64; idx += NT) {
-                    const int b = idx >> 6, v = (idx >> 5) & 1, kk = idx & 31;
-                    sv[(b * 4 + v) * 32 + kk] =
-                        (k0 + kk < n) ? __ldcg(cb + (c0 + b) * bs + (v ? 2 : 0) * n + kk) : 0.0;
+            double prev = 0.0, next = 0.0;
+            if (nb <= CHB) {
+                for (int idx = tid; idx < nb * 160; idx += NT) {   // 5 values x 32 modes per block
+                    const int b = idx / 160, v = (idx >> 5) % 5, kk = idx & 31;
+                    sv[(b * 7 + v) * 32 + kk] = (k0 + kk < n) ? __ldcg(cb + b * bs + v * n + kk) : 0.0;
                 }
                 __syncthreads();
                 if (lane_ok) {
-#pragma unroll 4
-                    for (int b = 0; b < cn; ++b) {
-                        const double ye = sv[(b * 4 + 0) * 32 + lane], pe = sv[(b * 4 + 1) * 32 + lane];
-                        const double y = (c0 + b == 0) ? ye : fma(pe, prev, ye);
-                        __stcg(cw + (c0 + b) * bs + 5 * n + lane, y);
+                    for (int b = 0; b < nb; ++b) {
+                        const double *q = sv + b * 7 * 32 + lane;
+                        const double y = (b == 0) ? q[0] : fma(q[2 * 32], prev, q[0]);
+                        sv[(b * 7 + 5) * 32 + lane] = y;
                         prev = y;
                     }
-                }
-                __syncthreads();
-            }
-            __threadfence_block();
-            double next = 0.0;
-            for (int c1 = nb; c1 > 0; c1 -= CHB) {
-                const int c0 = max(0, c1 - CHB), cn = c1 - c0;
-                for (int idx = tid; idx < cn * 128; idx += NT) {
-                    const int b = idx >> 7, v = (idx >> 5) & 3, kk = idx & 31;
-                    const int blk = c0 + b;
-                    double val = 0.0;
-                    if (k0 + kk < n) {
-                        if (v == 0) val = __ldcg(cb + blk * bs + 1 * n + kk);
-                        else if (v == 1) val = __ldcg(cb + blk * bs + 3 * n + kk);
-                        else if (v == 2) val = __ldcg(cb + blk * bs + 4 * n + kk);
-                        else val = blk > 0 ? __ldcg(cb + (blk - 1) * bs + 5 * n + kk) : 0.0;
-                    }
-                    sv[(b * 4 + v) * 32 + kk] = val;
-                }
-                __syncthreads();
-                if (lane_ok) {
-#pragma unroll 4
-                    for (int b = cn - 1; b >= 0; --b) {
-                        const int blk = c0 + b;
-                        double x = sv[(b * 4 + 0) * 32 + lane];
-                        if (blk > 0) x = fma(sv[(b * 4 + 3) * 32 + lane], sv[(b * 4 + 1) * 32 + lane], x);
-                        if (blk < nb - 1) x = fma(sv[(b * 4 + 2) * 32 + lane], next, x);
-                        __stcg(cw + blk * bs + 6 * n + lane, x);
+                    for (int b = nb - 1; b >= 0; --b) {
+                        const double *q = sv + b * 7 * 32 + lane;
+                        double x = q[1 * 32];
+                        if (b > 0) x = fma(sv[((b - 1) * 7 + 5) * 32 + lane], q[3 * 32], x);
+                        if (b < nb - 1) x = fma(q[4 * 32], next, x);
+                        sv[(b * 7 + 6) * 32 + lane] = x;
                         next = x;
                     }
                 }
                 __syncthreads();
+                for (int idx = tid; idx < nb * 64; idx += NT) {
+                    const int b = idx >> 6, v = 5 + ((idx >> 5) & 1), kk = idx & 31;
+                    if (k0 + kk < n) __stcg(cb + b * bs + v * n + kk, sv[(b * 7 + v) * 32 + kk]);
+                }
+                __syncthreads();
+            } else {
+                // long block lists: direct (slower) sweeps
+                if (lane_ok) {
+                    for (int b = 0; b < nb; ++b) {
+                        const double ye = __ldcg(cb + b * bs + lane), pe = __ldcg(cb + b * bs + 2 * n + lane);
+                        const double y = (b == 0) ? ye : fma(pe, prev, ye);
+                        __stcg(cb + b * bs + 5 * n + lane, y);
+                        prev = y;
+                    }
+                    for (int b = nb - 1; b >= 0; --b) {
+                        double x = __ldcg(cb + b * bs + 1 * n + lane);
+                        if (b > 0) x = fma(__ldcg(cb + (b - 1) * bs + 5 * n + lane), __ldcg(cb + b * bs + 3 * n + lane), x);
+                        if (b < nb - 1) x = fma(__ldcg(cb + b * bs + 4 * n + lane), next, x);
+                        __stcg(cb + b * bs + 6 * n + lane, x);
+                        next = x;
+                    }
+                }
             }
         }
     }
@@ -470,6 +488,8 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
     // ===================== phase 3: back-substitution + inverse DST ===================
     {
         double xs[MPT], yins[MPT], pcs[MPT], bnx[MPT];
+        double cib_inf[MPT], cinv[MPT], cibl[MPT];   // 1/beta_inf, 1/(-l_inf), 1/beta_{m-1}
+        int clen[MPT];
         Tail tail{0.0, -1};
         auto beta_before = [&](int it3, int k) {   // beta_{g0-1} of phase-3 item it3 (from bsave)
             int si, g0, rows;
@@ -514,9 +534,13 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
             for (int u = 0; u < MPT; ++u) {
                 const int k = tid + u * NT;
                 if (k >= n) continue;
-                ModeRec c;
-                c.load(p, k);
                 if (top) {
+                    ModeRec c;
+                    c.load(p, k);
+                    cib_inf[u] = c.ib_inf;
+                    cinv[u] = c.inv_nl;
+                    cibl[u] = 1.0 / c.b_last;
+                    clen[u] = c.len;
                     const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
                     const size_t bs = size_t(kCarryVals) * n;
                     xs[u] = has_next ? __ldcg(cb + bs + 6 * n) : 0.0;
@@ -527,51 +551,55 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                 if (it + 1 < nitems) bnx[u] = beta_before(it + 1, k);   // prefetch
                 double x = xs[u], Pc = pcs[u];
                 const double yin = yins[u];
-                if (g0 < c.len) {
-                    // transient rows: rebuild beta forward into rowbuf (bitwise the
-                    // reference factors), then sweep back over them
+                const int len = clen[u];
+                const double ib_inf = cib_inf[u];
+                const double *yg = stg + so + k;
+                if (g0 < len) {
+                    // transient rows: rebuild the reference factors forward (bitwise,
+                    // rectsolver.py:72-73); 1/beta_i goes to the spare rows of the
+                    // pair buffers
                     double bp = bstart;
 #pragma unroll
                     for (int rr = 0; rr < G; ++rr) {
                         if (rr >= rows) break;
                         const int i = g0 + rr;
                         double b;
-                        if (i < c.len) {
-                            const double d = diag_at(p, c.lam, i);
+                        if (i < len) {
+                            const double d = diag_at(p, mode_lam(p, k), i);
                             b = (i == 0) ? d : __dsub_rn(d, __dmul_rn(off, __ddiv_rn(off, bp)));
                         } else {
-                            b = (i == p.m - 1) ? c.b_last : c.b_inf;
+                            b = (i == p.m - 1) ? mode_blast(p, k) : mode_binf(p, k);
                         }
-                        rowbuf[rr * n + k] = b;
+                        auxp(rr)[k] = 1.0 / b;
                         bp = b;
                     }
 #pragma unroll
                     for (int rr = G - 1; rr >= 0; --rr) {
                         if (rr >= rows) continue;
-                        const double b = rowbuf[rr * n + k];
-                        double y = stg[so + rr * n + k];
+                        double y = yg[rr * n];
                         if (has_in) {
                             y = fma(Pc, yin, y);
                             // P_{i-1} = P_i / (-l_i) = -P_i beta_{i-1} / delta
-                            const double bm1 = rr > 0 ? rowbuf[(rr - 1) * n + k] : bstart;
+                            const double bm1 = rr > 0 ? 1.0 / auxp(rr - 1)[k] : bstart;
                             Pc = -Pc * bm1 / off;
                         }
-                        x = __ddiv_rn(__dsub_rn(y, __dmul_rn(off, x)), b);   // rectsolver.py:90
-                        rowbuf[rr * n + k] = x;
+                        x = __dsub_rn(y, __dmul_rn(off, x)) * auxp(rr)[k];   // rectsolver.py:90
+                        rowp(rr)[k] = x;
                     }
                 } else {
+                    const double ib_m = cibl[u], inl = cinv[u];
+                    const int mlast = p.m - 1;
 #pragma unroll
                     for (int rr = G - 1; rr >= 0; --rr) {
                         if (rr >= rows) continue;
-                        const int i = g0 + rr;
-                        double y = stg[so + rr * n + k];
+                        double y = yg[rr * n];
                         if (has_in) {
                             y = fma(Pc, yin, y);
-                            Pc *= c.inv_nl;
+                            Pc *= inl;
                         }
-                        const double b = (i == p.m - 1) ? c.b_last : c.b_inf;
-                        x = __ddiv_rn(__dsub_rn(y, __dmul_rn(off, x)), b);   // rectsolver.py:90
-                        rowbuf[rr * n + k] = x;
+                        const double ib = (g0 + rr == mlast) ? ib_m : ib_inf;
+                        x = __dsub_rn(y, __dmul_rn(off, x)) * ib;   // rectsolver.py:90
+                        rowp(rr)[k] = x;
                     }
                 }
                 xs[u] = x;
@@ -587,25 +615,25 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
             {
                 const int ra = 2 * pr, rb = 2 * pr + 1;
                 double2 *buf = xbuf + pr * F::PADL;
-                FL::first(buf, ra < rows ? rowbuf + ra * n : nullptr, rb < rows ? rowbuf + rb * n : nullptr, t);
-                FL::template mids<F::NMID, 16>(buf, tws, t);
+                FL::first(buf, ra < rows ? rowp(ra) : nullptr, rb < rows ? rowp(rb) : nullptr, t, pr);
+                FL::template mids<F::NMID, 16>(buf, tws, t, pr);
                 const bool va = ra < rows, vb = rb < rows;
                 double *oa = J.out + size_t(g0 + ra) * n, *ob = J.out + size_t(g0 + rb) * n;
                 if (J.other) {
                     const double *qa = J.other + size_t(g0 + ra) * n, *qb = J.other + size_t(g0 + rb) * n;
                     const double al = J.alpha, be = J.beta;
-                    FL::last(buf, tws, t, p.scale, [&](int k, double a, double b) {
+                    FL::last(buf, tws, t, pr, p.scale, [&](int k, double a, double b) {
                         if (va) oa[k] = fma(be, __ldg(qa + k), al * a);
                         if (vb) ob[k] = fma(be, __ldg(qb + k), al * b);
                     });
                 } else if (J.alpha == 1.0) {
-                    FL::last(buf, tws, t, p.scale, [&](int k, double a, double b) {
+                    FL::last(buf, tws, t, pr, p.scale, [&](int k, double a, double b) {
                         if (va) oa[k] = a;
                         if (vb) ob[k] = b;
                     });
                 } else {
                     const double al = J.alpha;
-                    FL::last(buf, tws, t, p.scale, [&](int k, double a, double b) {
+                    FL::last(buf, tws, t, pr, p.scale, [&](int k, double a, double b) {
                         if (va) oa[k] = al * a;
                         if (vb) ob[k] = al * b;
                     });
