@@ -195,6 +195,23 @@ class TestDdmSolve:
         assert configs.rel_l2(fields, exact) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-4)
 
 
+    @pytest.mark.slow
+    def test_c3_golden(self):
+        """c3: kappa = -100, random RHS, 5 x 4095^2 (84M points): iteration count
+        and sampled solution values against the reference run."""
+        g = load_golden("c3")
+        comp, f, _, _ = configs.build_cross_case("c3")
+        fd = {k: dev(v) for k, v in f.items()}
+        del f
+        fields, rep = ddm.ddm_solve(comp, fd, krylov.GmresConfig(m=50, tol=1e-10))
+        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        for sid in range(5):
+            v = fields[sid].values
+            idx = torch.as_tensor(g[f"idx_{sid}"], device="cuda")
+            assert rel(v[idx].cpu().numpy(), g[f"val_{sid}"]) < 1e-10
+            assert torch.linalg.norm(v).item() == pytest.approx(float(g[f"norm_{sid}"]), rel=1e-10)
+
+
 class TestGenericGmres:
     def test_dense_golden(self, golden_small):
         A, b = golden_small["gm_A"], golden_small["gm_b"]

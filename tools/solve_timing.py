@@ -1,0 +1,51 @@
+"""End-to-end ddm_solve timing on the BASELINE cross configs (GPU).
+
+    python tools/solve_timing.py [c0 c2 c3] [--reps R]
+
+RHS resident on the device; timed region = ddm_solve (plan build, arm
+pre-solves, GMRES to 1e-10, back-substitution), CUDA-synchronised, median of
+R repetitions after one warm-up.  Prints one JSON line per config.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2509_23180_b200 import configs, ddm, krylov  # noqa: E402
+
+
+def main():
+    names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["c0", "c2", "c3"]
+    reps = 3
+    if "--reps" in sys.argv:
+        reps = int(sys.argv[sys.argv.index("--reps") + 1])
+    for name in names:
+        comp, f, exact, meta = configs.build_cross_case(name)
+        fd = {k: torch.as_tensor(v, device="cuda") for k, v in f.items()}
+        del f
+        cfg = krylov.GmresConfig(m=50, tol=1e-10)
+        fields, rep = ddm.ddm_solve(comp, fd, cfg)   # warm-up (module load, tables)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fields, rep = ddm.ddm_solve(comp, fd, cfg)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        wall = float(np.median(times))
+        out = {"config": name, "points": meta["points"], "iterations": rep.iterations,
+               "wall_s": wall, "mpts_per_s": meta["points"] / wall / 1e6,
+               "gmres_wall_s": rep.wall_time, "us_per_iteration": rep.wall_time / max(rep.iterations, 1) * 1e6,
+               "true_residual": rep.true_residual}
+        if exact is not None:
+            out["rel_l2_exact"] = configs.rel_l2(fields, exact)
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
