@@ -280,10 +280,13 @@ def run_gpu(args, world, rank, local):
                                         f"{SETS * 2 * io_bytes / 1e6:.0f} MB > 126 MB L2",
                            "parallelism": f"replicas x{world} (independent batches, no collective)"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None,
+                             "frac": achieved / peak,
+                             # dram__bytes_read.sum + dram__bytes_write.sum per launch from
+                             # profiles/r01_persist_c1_ncu_full.json (ncu --set full, cold L2)
+                             "traffic": 63.0e6,
                              "peak_kind": peak_kind,
                              "algorithmic_bytes_per_point": B_ALG,
-                             "kernel": "fused precond apply (pass1 + carry + pass2)"},
+                             "kernel": "persist_kernel<11> (fused batched apply, 1 launch)"},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "grid_points/s",
                         "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
