@@ -212,6 +212,21 @@ class TestDdmSolve:
             assert torch.linalg.norm(v).item() == pytest.approx(float(g[f"norm_{sid}"]), rel=1e-10)
 
 
+class TestDistDriver:
+    def test_native_backend_single_rank(self, golden_small):
+        """dist_ddm_solve with the GPU backend and no process group (one rank owns
+        everything) reproduces the reference solution."""
+        from paper_2509_23180_b200 import dist as pdist
+        N, kappa = 15, -100.0
+        tag = f"{N}_{int(-kappa)}"
+        comp = configs.cross_composite(N, kappa=kappa)
+        f, _ = configs.manufactured_rhs(comp, "sin_exp")
+        fields, rep = pdist.dist_ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+        assert rep.iterations == int(golden_small[f"x_iters_{tag}"])
+        for sid in range(5):
+            assert rel(fields[sid].cpu().numpy(), golden_small[f"x_sol_{tag}_{sid}"]) < 1e-10
+
+
 class TestGenericGmres:
     def test_dense_golden(self, golden_small):
         A, b = golden_small["gm_A"], golden_small["gm_b"]
