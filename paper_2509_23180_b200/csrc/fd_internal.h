@@ -48,9 +48,11 @@ struct PlanDev {
     const double *ex;    // [sum ex_len][4]: l, 1/beta, beta, P(block-relative)
     const double *cv;    // [n][4]: l_inf, 1/beta_inf, beta_inf, 1/(-l_inf)
     const double *last;  // [n][2]: beta_{m-1}, 1/beta_{m-1}
-    const double *mode;  // [n][8]: l_inf, 1/b_inf, b_inf, 1/(-l_inf), b_last, lambda, ex_off, ex_len (int64 bits)
+    const double *mode;  // [n][8]: l_inf, 1/b_inf, b_inf, 1/(-l_inf), b_last, lambda, ex_off, fixed-point row (int64 bits)
     int ecap;            // rows [0, ecap) of every mode also stored row-major (coalesced):
     const double *dl, *dib, *db;   // [ecap][n] lower, 1/beta, beta
+    int kt, ktp;         // slowly converging modes k < kt: row-major table (ktp = kt rounded to even)
+    const double *lt;    // [m][3][ktp]: l_i, 1/beta_i, -beta_{i-1}/delta
     const double *blk;   // [nb][3][n]: Pe, xi_s, Q per block and mode
     double *ye;          // [nb][n] pass-1 local forward value at block end -> Y carries
     double *fs;          // [nb][n] pass-1 local backward value at block start -> X carries

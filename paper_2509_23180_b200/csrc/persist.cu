@@ -62,6 +62,7 @@ struct PList {
     unsigned long long *tstamp;   // optional [gridDim][8] phase timestamps (FD_PHASE_TIMING)
     double *bsave;       // [gridDim][bstride][n] beta checkpoints (phase 1 -> phase 3)
     int bstride;
+    int dbg;             // FD_DBG experiments (timing only)
     PJob job[kMaxPJobs];
 };
 
@@ -109,17 +110,30 @@ struct Tail {
     double v;
     int idx;   // -1: none
 };
+// The table slice (lt != null) is counted in the same expect_tx; with
+// defer_lt its copy is left to issue_lt(), so the slice buffer can still be
+// read by the current group (the mbarrier phase completes only when both
+// copies have landed).
+__device__ __forceinline__ void issue_lt(double *ltstg, const double *lt, int g0, int rows, int ktp,
+                                         uint64_t *bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tma_load_1d(ltstg, lt + size_t(g0) * 3 * ktp, uint32_t(rows) * 3u * uint32_t(ktp) * 8u, bar);
+}
 __device__ __forceinline__ Tail issue_rows(double *stg, const double *base, int g0, int rows, int n,
-                                           int m, uint64_t *bar) {
+                                           int m, uint64_t *bar, double *ltstg = nullptr,
+                                           const double *lt = nullptr, int ktp = 0,
+                                           bool defer_lt = false) {
     const uintptr_t start = reinterpret_cast<uintptr_t>(base + size_t(g0) * n);
     const uintptr_t end = start + uintptr_t(rows) * n * sizeof(double);
     const uintptr_t a = start & ~uintptr_t(15);
     const bool last = (g0 + rows >= m);
     const uintptr_t e = last ? (end & ~uintptr_t(15)) : ((end + 15) & ~uintptr_t(15));
     const uint32_t bytes = uint32_t(e - a);
+    const uint32_t ltbytes = lt ? uint32_t(rows) * 3u * uint32_t(ktp) * 8u : 0u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bar, bytes);
+    mbar_expect_tx(bar, bytes + ltbytes);
     tma_load_1d(stg, reinterpret_cast<const void *>(a), bytes, bar);
+    if (ltbytes && !defer_lt) tma_load_1d(ltstg, lt + size_t(g0) * 3 * ktp, ltbytes, bar);
     Tail t{0.0, -1};
     if (end != e) {
         t.v = __ldcg(reinterpret_cast<const double *>(e));
@@ -187,7 +201,8 @@ struct PCfg {
     static constexpr size_t XBUF = F::SMEM;
     static constexpr size_t STG = (size_t(G) * (F::N - 1) + 4) * sizeof(double);
     static constexpr size_t TWS = (16 + 256 + 256 + 16) * sizeof(double2);
-    static constexpr size_t SMEM = XBUF + STG + TWS;
+    static constexpr size_t LTB = 13 * 1024;   // one group's slice of the long-transient table
+    static constexpr size_t SMEM = XBUF + STG + TWS + LTB;
 };
 
 template <int LG>
@@ -208,6 +223,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
     double *stg = reinterpret_cast<double *>(smem_raw + C::XBUF);
     double2 *tw16 = reinterpret_cast<double2 *>(smem_raw + C::XBUF + C::STG);
     double2 *tw256 = tw16 + 16, *twla = tw256 + 256, *twlb = twla + 256;
+    double *lts = reinterpret_cast<double *>(smem_raw + C::XBUF + C::STG + C::TWS);   // [G][3][ktp]
     __shared__ __align__(8) uint64_t bar;
     __shared__ Seg segs[kMaxSegs];
     __shared__ int nseg_s, nitems_s;
@@ -288,7 +304,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
             int si, g0, rows;
             item_of(0, si, g0, rows, false);
             const PJob &J = pl.job[segs[si].job];
-            tail = issue_rows(stg, J.in, g0, rows, n, J.p.m, &bar);
+            tail = issue_rows(stg, J.in, g0, rows, n, J.p.m, &bar, lts, J.p.lt, J.p.ktp);
         }
 #pragma unroll 1
         for (int it = 0; it < nitems; ++it) {
@@ -315,7 +331,8 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                     int si2, g2, rows2;
                     item_of(it + 1, si2, g2, rows2, false);
                     const PJob &J2 = pl.job[segs[si2].job];
-                    tail = issue_rows(stg, J2.in, g2, rows2, n, J2.p.m, &bar);
+                    tail = issue_rows(stg, J2.in, g2, rows2, n, J2.p.m, &bar, lts, J2.p.lt, J2.p.ktp,
+                                      /*defer_lt=*/true);
                 }
                 FL::store(buf, v, t, pr);
                 FL::template mids<F::NMID, 16>(buf, tws, t, pr);
@@ -346,7 +363,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                     bp = g0 > 0 ? beta_at(p, c, k, g0 - 1) : 0.0;
                     __stcg(bsave + size_t(pl.bstride - 1 - si) * n + k, bp);
                 }
-                const int len = clen[u];
+                const int len = (pl.dbg & 32) ? 0 : clen[u];
                 const double l_inf = cl[u], ib_inf = cib[u];
                 const double cbinf = mode_binf(p, k);
 #pragma unroll
@@ -355,7 +372,11 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                     const int i = g0 + rr;
                     const double r = rowp(rr)[k];
                     double l, ib;
-                    if (i < len) {
+                    if (k < p.kt) {
+                        // slowly converging low mode: reference factors from the table
+                        l = lts[rr * 3 * p.ktp + k];
+                        ib = lts[rr * 3 * p.ktp + p.ktp + k];
+                    } else if (i < len) {
                         // transient row: the reference factorisation, recomputed
                         // bitwise (rectsolver.py:72-73), no table traffic
                         const double d = diag_at(p, mode_lam(p, k), i);
@@ -401,7 +422,8 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                     const int e = sg.e;
                     const double cc = ccs[u];
                     // Q = pi_e * (-l_{e+1}),  l_{e+1} = delta / beta_e
-                    const double lnext = (e + 1 < len) ? __ddiv_rn(off, bend) : l_inf;
+                    const double lnext = (k < p.kt) ? ((e + 1 < p.m) ? __ldg(p.lt + size_t(e + 1) * 3 * p.ktp + k) : 0.0)
+                                                    : ((e + 1 < len) ? __ddiv_rn(off, bend) : l_inf);
                     const double Q = (e < p.m - 1) ? w * (-lnext) : 0.0;
                     __stcg(cb + 0 * n, y);
                     __stcg(cb + 1 * n, f);
@@ -410,7 +432,13 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                     __stcg(cb + 4 * n, Q);
                 }
             }
-            __syncthreads();   // rowbuf consumed before the next group's FFT
+            __syncthreads();   // rowbuf and the table slice consumed
+            if (tid == 0 && it + 1 < nitems) {
+                int si2, g2, rows2;
+                item_of(it + 1, si2, g2, rows2, false);
+                const PJob &J2 = pl.job[segs[si2].job];
+                if (J2.p.lt) issue_lt(lts, J2.p.lt, g2, rows2, J2.p.ktp, &bar);
+            }
         }
     }
     stamp(1);
@@ -503,7 +531,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
             item_of(0, si, g0, rows, true);
             asm volatile("fence.proxy.async.global;" ::: "memory");
             const PJob &J = pl.job[segs[si].job];
-            tail = issue_rows(stg, J.out, g0, rows, n, J.p.m, &bar);
+            tail = issue_rows(stg, J.out, g0, rows, n, J.p.m, &bar, lts, J.p.lt, J.p.ktp);
         }
         if (nitems > 0) {
 #pragma unroll
@@ -551,10 +579,23 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                 if (it + 1 < nitems) bnx[u] = beta_before(it + 1, k);   // prefetch
                 double x = xs[u], Pc = pcs[u];
                 const double yin = yins[u];
-                const int len = clen[u];
+                const int len = (pl.dbg & 32) ? 0 : clen[u];
                 const double ib_inf = cib_inf[u];
                 const double *yg = stg + so + k;
-                if (g0 < len) {
+                if (k < p.kt) {
+                    const double *tb = lts + k;
+#pragma unroll
+                    for (int rr = G - 1; rr >= 0; --rr) {
+                        if (rr >= rows) continue;
+                        double y = yg[rr * n];
+                        if (has_in) {
+                            y = fma(Pc, yin, y);
+                            Pc *= tb[rr * 3 * p.ktp + 2 * p.ktp];   // P_{i-1} = -P_i beta_{i-1} / delta
+                        }
+                        x = __dsub_rn(y, __dmul_rn(off, x)) * tb[rr * 3 * p.ktp + p.ktp];   // rectsolver.py:90
+                        rowp(rr)[k] = x;
+                    }
+                } else if (g0 < len) {
                     // transient rows: rebuild the reference factors forward (bitwise,
                     // rectsolver.py:72-73); 1/beta_i goes to the spare rows of the
                     // pair buffers
@@ -610,7 +651,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                 int si2, g2, rows2;
                 item_of(it + 1, si2, g2, rows2, true);
                 const PJob &J2 = pl.job[segs[si2].job];
-                tail = issue_rows(stg, J2.out, g2, rows2, n, J2.p.m, &bar);
+                tail = issue_rows(stg, J2.out, g2, rows2, n, J2.p.m, &bar, lts, J2.p.lt, J2.p.ktp);
             }
             {
                 const int ra = 2 * pr, rb = 2 * pr + 1;
@@ -739,6 +780,7 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
         unsigned long long *ts = nullptr;
         if (timing) FD_CUDA(cudaMallocAsync(&ts, sizeof(unsigned long long) * 8 * grid, s));
         pl.tstamp = ts;
+        pl.dbg = getenv("FD_DBG") ? atoi(getenv("FD_DBG")) : 0;
 
         void *args[] = {(void *)&pl};
         FD_CUDA(cudaLaunchCooperativeKernel((const void *)persist_kernel<LG>, dim3(grid), dim3(C::NT), args,

@@ -132,6 +132,9 @@ struct HostTables {
     std::vector<double> blk;   // nb * 3 * n
     std::vector<int> bad_modes;
     std::vector<double> lam;   // eigenvalues lambda_k (+ kappa)
+    std::vector<int> fix;      // first row of the bitwise fixed point (m if none)
+    std::vector<double> lt;    // [m][3][ktp] l_i, 1/beta_i, -beta_{i-1}/delta for modes < kt
+    int kt = 0, ktp = 0;
     long long explicit_rows = 0;
 };
 
@@ -157,6 +160,7 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
     for (int k = 0; k < n; ++k) {
         ModeFactors f = factor_mode(m, lam[k], mod_w, mod_e, off, tol, R);
         if (f.bad) T.bad_modes.push_back(k);
+        T.fix.push_back(f.fix >= 0 ? f.fix : m);
         const int len = (int)f.l.size();
         T.off[k] = (int)(T.ex.size() / 4);
         T.len[k] = len;
@@ -204,6 +208,32 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
         }
     }
     return T;
+}
+
+// Row-major factor table of the slowly converging lowest modes (persistent
+// kernel): modes k < kt whose fixed point is >= kLongTransient rows away.
+constexpr int kLongTransient = 48;
+static void build_long_table(HostTables &T, int m, int n, double off, int kt_cap) {
+    int kt = 0;
+    for (int k = 0; k < n; ++k)
+        if (T.fix[k] >= kLongTransient) kt = k + 1;
+    kt = std::min(kt, kt_cap);
+    T.kt = kt;
+    T.ktp = (kt + 1) & ~1;
+    if (kt == 0) return;
+    T.lt.assign(size_t(m) * 3 * T.ktp, 0.0);
+    for (int k = 0; k < kt; ++k) {
+        const int len = T.len[k];
+        const double *ex = &T.ex[4 * size_t(T.off[k])];
+        auto gl = [&](int i) { return i < len ? ex[4 * i + 0] : T.cv[4 * k + 0]; };
+        auto gb = [&](int i) { return i == m - 1 ? T.last[2 * k] : (i < len ? ex[4 * i + 2] : T.cv[4 * k + 2]); };
+        for (int i = 0; i < m; ++i) {
+            double *r = &T.lt[size_t(i) * 3 * T.ktp];
+            r[k] = (i == 0) ? 0.0 : gl(i);
+            r[T.ktp + k] = 1.0 / gb(i);
+            r[2 * T.ktp + k] = (i == 0) ? 0.0 : -gb(i - 1) / off;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -315,7 +345,7 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
             for (int c = 0; c < 4; ++c) r[c] = T.cv[4 * k + c];
             r[4] = T.last[2 * k];
             r[5] = T.lam[k];
-            long long o = T.off[k], l = T.len[k];
+            long long o = T.off[k], l = T.fix[k];   // exact fixed-point row (persistent kernel)
             memcpy(&r[6], &o, 8);
             memcpy(&r[7], &l, 8);
         }
@@ -335,6 +365,16 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
         d.dl = upload(p, dl);
         d.dib = upload(p, dib);
         d.db = upload(p, db);
+        if (tk == kFFT) {
+            // smem budget of the persistent kernel for one group's slice: 13 KB
+            int lg = 0;
+            while ((1 << lg) < 2 * (n + 1)) ++lg;
+            const int G = 16384 >> lg;                     // rows per group at 512 threads
+            build_long_table(T, m, n, d.off, std::max(0, (13 * 1024 / (G * 24)) & ~1));
+        }
+        d.kt = T.kt;
+        d.ktp = T.ktp;
+        d.lt = T.kt ? upload(p, T.lt) : nullptr;
         d.blk = upload(p, T.blk);
         std::vector<double> zeros(size_t(d.nb) * n, 0.0);
         d.ye = upload(p, zeros);
