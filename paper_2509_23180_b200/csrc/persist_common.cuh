@@ -1,0 +1,330 @@
+// Shared pieces of the persistent fused-solve kernels (persist.cu,
+// persist_ws.cu): job/segment descriptors, TMA bulk-copy + mbarrier helpers,
+// per-mode factor access, and the host-side cooperative launcher.
+#pragma once
+#include <cooperative_groups.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "dst_device.cuh"
+#include "fd_internal.h"
+
+namespace fd {
+namespace cg = cooperative_groups;
+
+struct PJob {
+    PlanDev p;
+    const double *in;
+    double *out;
+    double alpha, beta;
+    const double *other;
+    long long row0;   // first global row of the job
+    int c_first;      // first virtual range touching the job
+    int nblk;         // carry blocks of the job
+    int blk_base;     // global index of its first block
+};
+
+constexpr int kMaxPJobs = 8;
+constexpr int kMaxSegs = 48;
+constexpr int kMaxRowsPerBlock = 256;   // keeps block products P_e far from underflow
+constexpr int kCarryVals = 7;           // yhat_e, F_s, P_e, xi_s, Q, Y, X
+
+struct PList {
+    int count;
+    int V;               // virtual row ranges (carry blocks)
+    long long total_rows;
+    double *carry;       // [total_blocks][kCarryVals][n]
+    int n;
+    unsigned long long *tstamp;   // optional [gridDim][8] phase timestamps (FD_PHASE_TIMING)
+    unsigned long long *trace;    // optional per-item timeline of one CTA (FD_TRACE=cta)
+    int trace_cta;
+    double *bsave;       // [gridDim][bstride][n] beta checkpoints (phase 1 -> phase 3)
+    int bstride;
+    PJob job[kMaxPJobs];
+};
+
+struct Seg {
+    int job, s, e, blk, ngroups, item0;
+};
+
+// --- TMA bulk copy + mbarrier helpers --------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Issue the copy of rows [g0, g0+rows) of an (m, n) array into `stg`; the data
+// lands at stg + off where off = (address mod 16) / 8.  The bulk copy is
+// widened to 16-byte boundaries; only the last group of an array, whose end may
+// be the end of the allocation, leaves an 8-byte tail that thread 0 fetches
+// into a register (returned) and stores once the copy has landed.
+struct Tail {
+    double v;
+    int idx;   // -1: none
+};
+// The table slice (lt != null) is counted in the same expect_tx; with
+// defer_lt its copy is left to issue_lt(), so the slice buffer can still be
+// read by the current group (the mbarrier phase completes only when both
+// copies have landed).
+__device__ __forceinline__ void issue_lt(double *ltstg, const double *lt, int g0, int rows, int ktp,
+                                         uint64_t *bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tma_load_1d(ltstg, lt + size_t(g0) * 3 * ktp, uint32_t(rows) * 3u * uint32_t(ktp) * 8u, bar);
+}
+__device__ __forceinline__ Tail issue_rows(double *stg, const double *base, int g0, int rows, int n,
+                                           int m, uint64_t *bar, double *ltstg = nullptr,
+                                           const double *lt = nullptr, int ktp = 0,
+                                           bool defer_lt = false) {
+    const uintptr_t start = reinterpret_cast<uintptr_t>(base + size_t(g0) * n);
+    const uintptr_t end = start + uintptr_t(rows) * n * sizeof(double);
+    const uintptr_t a = start & ~uintptr_t(15);
+    const bool last = (g0 + rows >= m);
+    const uintptr_t e = last ? (end & ~uintptr_t(15)) : ((end + 15) & ~uintptr_t(15));
+    const uint32_t bytes = uint32_t(e - a);
+    const uint32_t ltbytes = lt ? uint32_t(rows) * 3u * uint32_t(ktp) * 8u : 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, bytes + ltbytes);
+    tma_load_1d(stg, reinterpret_cast<const void *>(a), bytes, bar);
+    if (ltbytes && !defer_lt) tma_load_1d(ltstg, lt + size_t(g0) * 3 * ktp, ltbytes, bar);
+    Tail t{0.0, -1};
+    if (end != e) {
+        t.v = __ldcg(reinterpret_cast<const double *>(e));
+        t.idx = int((e - a) / 8);
+    }
+    return t;
+}
+// true when the group's copy leaves a tail (identical on every thread)
+__device__ __forceinline__ bool has_tail(const double *base, int g0, int rows, int n, int m) {
+    const uintptr_t end = reinterpret_cast<uintptr_t>(base + size_t(g0 + rows) * n);
+    return (g0 + rows >= m) && (end & 15);
+}
+
+__device__ __forceinline__ int stg_off(const double *base, int g0, int n) {
+    return int((reinterpret_cast<uintptr_t>(base + size_t(g0) * n) & 15) >> 3);
+}
+
+// Per-mode record (PlanDev::mode, 64 B): l_inf, 1/beta_inf, beta_inf,
+// 1/(-l_inf), beta_{m-1}, lambda_k, explicit offset, explicit length.
+struct ModeRec {
+    double l_inf, ib_inf, b_inf, inv_nl, b_last, lam;
+    int off, len;
+    __device__ void load(const PlanDev &p, int k) {
+        const double2 *r = reinterpret_cast<const double2 *>(p.mode) + 4 * k;
+        const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3);
+        l_inf = a.x;
+        ib_inf = a.y;
+        b_inf = b.x;
+        inv_nl = b.y;
+        b_last = c.x;
+        lam = c.y;
+        off = int(__double_as_longlong(d.x));
+        len = int(__double_as_longlong(d.y));
+    }
+};
+
+__device__ __forceinline__ double mode_lam(const PlanDev &p, int k) { return __ldg(p.mode + 8 * size_t(k) + 5); }
+__device__ __forceinline__ double mode_blast(const PlanDev &p, int k) { return __ldg(p.mode + 8 * size_t(k) + 4); }
+__device__ __forceinline__ double mode_binf(const PlanDev &p, int k) { return __ldg(p.mode + 8 * size_t(k) + 2); }
+
+// beta_i of mode k from the plan's tables (used once per segment start)
+__device__ __forceinline__ double beta_at(const PlanDev &p, const ModeRec &c, int k, int i) {
+    if (i == p.m - 1) return c.b_last;
+    if (i < p.ecap) return __ldg(p.db + size_t(i) * p.n + k);
+    if (i < c.len) return __ldg(p.ex + 4 * (size_t(c.off) + i) + 2);
+    return c.b_inf;
+}
+
+// Diagonal of row i: lambda (+ west modifier on row 0) (+ east on row m-1),
+// summed in the reference's order (rectsolver.py:125,132-133).
+__device__ __forceinline__ double diag_at(const PlanDev &p, double lam, int i) {
+    double d = lam;
+    if (i == 0) d = __dadd_rn(d, p.mod_w);
+    if (i == p.m - 1) d = __dadd_rn(d, p.mod_e);
+    return d;
+}
+
+// ---------------------------------------------------------------------------
+// host launcher
+// K: kernel traits with static members NT (threads), G (rows per item),
+// SMEM (dynamic shared bytes) and fn() (the __global__ entry point).
+template <class K>
+static int persist_grid(int device) {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(device);
+    if (it != cache.end()) return it->second;
+    FD_CUDA(cudaFuncSetAttribute(K::fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM));
+    int per_sm = 0, sms = 0;
+    FD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K::fn(), K::NT, K::SMEM));
+    FD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (per_sm < 1) FD_FAIL(FD_ERR_CUDA, "persistent solve kernel cannot be resident");
+    cache[device] = per_sm * sms;
+    return per_sm * sms;
+}
+
+template <class K>
+static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
+    using C = K;
+    int device = 0;
+    FD_CUDA(cudaGetDevice(&device));
+    const int grid = persist_grid<K>(device);
+    for (size_t j0 = 0; j0 < jobs.size(); j0 += kMaxPJobs) {
+        PList pl{};
+        pl.count = (int)std::min<size_t>(kMaxPJobs, jobs.size() - j0);
+        pl.n = jobs[j0].p.n;
+        long long total = 0;
+        for (int j = 0; j < pl.count; ++j) total += jobs[j0 + j].p.m;
+        pl.total_rows = total;
+        long long V = std::max<long long>(grid, (total + kMaxRowsPerBlock - 1) / kMaxRowsPerBlock);
+        V = std::min<long long>(V, total);
+        pl.V = (int)V;
+        auto lo = [&](long long v) { return total * v / V; };
+        auto range_of = [&](long long r) {   // largest v with lo(v) <= r
+            long long v = r * V / total;
+            while (v + 1 < V && lo(v + 1) <= r) ++v;
+            while (v > 0 && lo(v) > r) --v;
+            return v;
+        };
+        long long row0 = 0;
+        int blocks = 0;
+        for (int j = 0; j < pl.count; ++j) {
+            const SolveJob &sj = jobs[j0 + j];
+            PJob &pj = pl.job[j];
+            pj.p = sj.p;
+            pj.in = sj.in;
+            pj.out = sj.out;
+            pj.alpha = sj.alpha;
+            pj.beta = sj.beta;
+            pj.other = sj.other;
+            pj.row0 = row0;
+            const long long cf = range_of(row0), cl = range_of(row0 + sj.p.m - 1);
+            pj.c_first = (int)cf;
+            pj.nblk = (int)(cl - cf + 1);
+            pj.blk_base = blocks;
+            blocks += pj.nblk;
+            row0 += sj.p.m;
+        }
+        // items and segments per CTA (mirrors the kernel's enumeration)
+        int bstride = 1;
+        for (int c = 0; c < grid; ++c) {
+            int items = 0, segs_c = 0;
+            for (long long v = c; v < V; v += grid) {
+                const long long lo_v = lo(v), hi_v = lo(v + 1);
+                long long r0 = 0;
+                for (int j = 0; j < pl.count; ++j) {
+                    const long long r1 = r0 + jobs[j0 + j].p.m;
+                    if (r0 < hi_v && r1 > lo_v) {
+                        const long long len = std::min(hi_v, r1) - std::max(lo_v, r0);
+                        items += int((len + C::G - 1) / C::G);
+                        ++segs_c;
+                    }
+                    r0 = r1;
+                }
+            }
+            bstride = std::max(bstride, items + segs_c);
+        }
+        const size_t carry_sz = size_t(blocks) * kCarryVals * pl.n;
+        double *wsp = ws.get(carry_sz + size_t(grid) * bstride * pl.n);
+        pl.carry = wsp;
+        pl.bsave = wsp + carry_sz;
+        pl.bstride = bstride;
+        static const bool timing = getenv("FD_PHASE_TIMING") != nullptr;
+        unsigned long long *ts = nullptr;
+        if (timing) FD_CUDA(cudaMallocAsync(&ts, sizeof(unsigned long long) * 8 * grid, s));
+        pl.tstamp = ts;
+
+        static const bool tracing = getenv("FD_TRACE") != nullptr;
+        unsigned long long *tr = nullptr;
+        if (tracing) {
+            FD_CUDA(cudaMallocAsync(&tr, sizeof(unsigned long long) * 16 * 64 * 2, s));
+            FD_CUDA(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * 16 * 64 * 2, s));
+        }
+        pl.trace = tr;
+        pl.trace_cta = tracing ? atoi(getenv("FD_TRACE")) : 0;
+        void *args[] = {(void *)&pl};
+        FD_CUDA(cudaLaunchCooperativeKernel(K::fn(), dim3(grid), dim3(C::NT), args, C::SMEM, s));
+        if (tracing) {
+            std::vector<unsigned long long> h(16 * 64 * 2);
+            FD_CUDA(cudaMemcpyAsync(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost, s));
+            FD_CUDA(cudaStreamSynchronize(s));
+            FD_CUDA(cudaFreeAsync(tr, s));
+            unsigned long long t0 = ~0ull;
+            for (auto v : h)
+                if (v) t0 = std::min(t0, v);
+            for (int role = 0; role < 16; ++role) {
+                bool any = false;
+                for (int it = 0; it < 64; ++it)
+                    if (h[(role * 64 + it) * 2]) any = true;
+                if (!any) continue;
+                fprintf(stderr, "[trace role %2d]", role);
+                for (int it = 0; it < 64; ++it) {
+                    const auto a = h[(role * 64 + it) * 2], b = h[(role * 64 + it) * 2 + 1];
+                    if (a) fprintf(stderr, " %.1f/%.1f", (a - t0) * 1e-3, (b - t0) * 1e-3);
+                }
+                fprintf(stderr, "\n");
+            }
+        }
+        if (timing) {
+            std::vector<unsigned long long> h(8 * grid);
+            FD_CUDA(cudaMemcpyAsync(h.data(), ts, h.size() * 8, cudaMemcpyDeviceToHost, s));
+            FD_CUDA(cudaStreamSynchronize(s));
+            FD_CUDA(cudaFreeAsync(ts, s));
+            unsigned long long t0 = ~0ull;
+            for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[8 * c]);
+            double mx[6] = {0}, mn[6] = {1e30, 1e30, 1e30, 1e30, 1e30, 1e30};
+            for (int c = 0; c < grid; ++c)
+                for (int k = 0; k < 6; ++k) {
+                    double v = (h[8 * c + k] - t0) * 1e-3;
+                    mx[k] = std::max(mx[k], v);
+                    mn[k] = std::min(mn[k], v);
+                }
+            if (getenv("FD_PHASE_TIMING_CTA")) {
+                std::vector<std::pair<double, int>> d1;
+                for (int c = 0; c < grid; ++c) d1.push_back({(h[8 * c + 1] - h[8 * c]) * 1e-3, c});
+                std::sort(d1.begin(), d1.end());
+                for (size_t q = 0; q < d1.size(); q += std::max<size_t>(1, d1.size() / 24)) {
+                    const int c = d1[q].second;
+                    fprintf(stderr, "  cta %3d rows [%lld,%lld) p1 %.1f us p3 %.1f us\n", c, total * c / V,
+                            total * (c + 1) / V, d1[q].first, (h[8 * c + 5] - h[8 * c + 4]) * 1e-3);
+                }
+            }
+            fprintf(stderr, "[fd phase us] start %.1f-%.1f p1end %.1f-%.1f sync1 %.1f-%.1f p2end %.1f-%.1f sync2 %.1f-%.1f end %.1f-%.1f (grid %d, V %d, rows %lld)\n",
+                    mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[3], mx[3], mn[4], mx[4], mn[5], mx[5], grid, pl.V, total);
+        }
+    }
+}
+
+
+}  // namespace fd
