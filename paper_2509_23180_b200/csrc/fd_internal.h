@@ -58,7 +58,31 @@ struct PlanDev {
     double *fs;          // [nb][n] pass-1 local backward value at block start -> X carries
     const double *dense; // [n][n] sin table (dense transform) or nullptr
     const double2 *tw;   // FFT twiddles e^{-2 pi i t / L}, t < L = 2(n+1), or nullptr
+    const double *ralpha;// [n+1] real-DST pre-weights (rsolve.cu), alpha_j = s/2 sin(pi j/N) + s/4
 };
+
+// ---------------------------------------------------------------------------
+// Geometry of the real-symmetric persistent solve (rsolve.cu), shared with the
+// plan builder (long-transient table cap).  N = n + 1 = 2^NL; one CTA of
+// kRsThreads per SM; N/16 threads per row pair; the pair regions, twiddles,
+// pre-weights and scan scratch are fixed, the rest of the shared memory holds
+// one group's slice of the long-transient table (24 B per row and mode).
+constexpr int kRsThreads = 512;
+constexpr int kRsMinN = 256, kRsMaxN = 2048;
+constexpr size_t kRsSmem = 227 * 1024 - 2048;
+constexpr int rs_pairs(int N) { return kRsThreads / (N / 16); }
+constexpr int rs_rows_per_group(int N) { return 2 * rs_pairs(N); }
+constexpr size_t rs_fixed_smem(int N) {
+    return size_t(rs_pairs(N)) * size_t(N + N / 16) * 16 + 272 * 16 + size_t(N) * 8 +
+           size_t(rs_pairs(N)) * 16 * 8;
+}
+constexpr int rs_kt_cap(int N) {
+    return int((kRsSmem - rs_fixed_smem(N)) / (24 * size_t(rs_rows_per_group(N)))) & ~1;
+}
+inline bool rs_supported(int n) {
+    const int N = n + 1;
+    return N >= kRsMinN && N <= kRsMaxN && (N & (N - 1)) == 0;
+}
 
 enum Transform { kDense = 0, kFFT = 1 };
 

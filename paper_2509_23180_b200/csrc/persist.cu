@@ -74,6 +74,14 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
         }
     };
     stamp(0);
+    // FD_TRACE=<cta>: per-item timeline of one CTA -> pl.trace[role][item][2]
+    auto trace = [&](int role, int item, int which) {
+        if (pl.trace && tid == 0 && blockIdx.x == pl.trace_cta && item < 64) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+            pl.trace[(role * 64 + item) * 2 + which] = g;
+        }
+    };
 
     if (tid == 0) {
         int ns = 0, items = 0;
@@ -148,8 +156,10 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
             const PJob &J = pl.job[sg.job];
             const PlanDev &p = J.p;
             const double off = p.off;
+            trace(0, it, 0);
             mbar_wait(&bar, parity);
             parity ^= 1u;
+            trace(0, it, 1);
             if (has_tail(J.in, g0, rows, n, p.m)) {
                 if (tid == 0) stg[tail.idx] = tail.v;
                 __syncthreads();
@@ -178,6 +188,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                 });
                 __syncthreads();   // all rows of the group transformed
             }
+            trace(1, it, 0);
             const bool first = (g0 == sg.s), last = (g0 + rows - 1 == sg.e);
             double *outg = J.out + size_t(g0) * n;
             const int mlast = p.m - 1;
@@ -268,6 +279,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                 }
             }
             __syncthreads();   // rowbuf and the table slice consumed
+            trace(1, it, 1);
             if (tid == 0 && it + 1 < nitems) {
                 int si2, g2, rows2;
                 item_of(it + 1, si2, g2, rows2, false);
@@ -386,8 +398,10 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
             const bool top = (g0 + rows - 1 == sg.e);
             const bool has_in = sg.blk > J.blk_base;                 // block does not start at row 0
             const bool has_next = sg.blk < J.blk_base + J.nblk - 1;  // a block below carries X
+            trace(2, it, 0);
             mbar_wait(&bar, parity);
             parity ^= 1u;
+            trace(2, it, 1);
             if (has_tail(J.out, g0, rows, n, p.m)) {
                 if (tid == 0) stg[tail.idx] = tail.v;
                 __syncthreads();
@@ -482,6 +496,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                 pcs[u] = Pc;
             }
             __syncthreads();   // staging consumed, rowbuf complete
+            trace(3, it, 0);
             if (tid == 0 && it + 1 < nitems) {
                 int si2, g2, rows2;
                 item_of(it + 1, si2, g2, rows2, true);
@@ -516,6 +531,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
                 }
                 __syncthreads();
             }
+            trace(3, it, 1);
         }
     }
     stamp(5);
@@ -531,9 +547,11 @@ struct PersistA {
 };
 
 bool launch_persist_ws(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
+bool launch_rsolve(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
     if (launch_persist_ws(jobs, s, ws)) return true;
+    if (launch_rsolve(jobs, s, ws)) return true;
     const int n = jobs[0].p.n;
     int lg = 0;
     while ((1 << lg) < 2 * (n + 1)) ++lg;

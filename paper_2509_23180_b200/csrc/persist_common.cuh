@@ -286,12 +286,12 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
             for (int role = 0; role < 16; ++role) {
                 bool any = false;
                 for (int it = 0; it < 64; ++it)
-                    if (h[(role * 64 + it) * 2]) any = true;
+                    if (h[(role * 64 + it) * 2] || h[(role * 64 + it) * 2 + 1]) any = true;
                 if (!any) continue;
                 fprintf(stderr, "[trace role %2d]", role);
                 for (int it = 0; it < 64; ++it) {
                     const auto a = h[(role * 64 + it) * 2], b = h[(role * 64 + it) * 2 + 1];
-                    if (a) fprintf(stderr, " %.1f/%.1f", (a - t0) * 1e-3, (b - t0) * 1e-3);
+                    if (a || b) fprintf(stderr, " %.1f/%.1f", a ? (a - t0) * 1e-3 : -1.0, b ? (b - t0) * 1e-3 : -1.0);
                 }
                 fprintf(stderr, "\n");
             }
@@ -311,13 +311,17 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
                     mn[k] = std::min(mn[k], v);
                 }
             if (getenv("FD_PHASE_TIMING_CTA")) {
-                std::vector<std::pair<double, int>> d1;
-                for (int c = 0; c < grid; ++c) d1.push_back({(h[8 * c + 1] - h[8 * c]) * 1e-3, c});
-                std::sort(d1.begin(), d1.end());
-                for (size_t q = 0; q < d1.size(); q += std::max<size_t>(1, d1.size() / 24)) {
-                    const int c = d1[q].second;
-                    fprintf(stderr, "  cta %3d rows [%lld,%lld) p1 %.1f us p3 %.1f us\n", c, total * c / V,
-                            total * (c + 1) / V, d1[q].first, (h[8 * c + 5] - h[8 * c + 4]) * 1e-3);
+                // slowest CTAs of phase 1 and of phase 3
+                for (int ph = 0; ph < 2; ++ph) {
+                    std::vector<std::pair<double, int>> d;
+                    for (int c = 0; c < grid; ++c)
+                        d.push_back({ph == 0 ? (h[8 * c + 1] - h[8 * c]) * 1e-3 : (h[8 * c + 5] - h[8 * c + 4]) * 1e-3, c});
+                    std::sort(d.rbegin(), d.rend());
+                    fprintf(stderr, "  slowest p%d:", ph ? 3 : 1);
+                    for (int q = 0; q < 12 && q < (int)d.size(); ++q)
+                        fprintf(stderr, " cta%d[%lld,%lld)=%.1f", d[q].second, total * d[q].second / V,
+                                total * (d[q].second + 1) / V, d[q].first);
+                    fprintf(stderr, "  median %.1f\n", d[d.size() / 2].first);
                 }
             }
             fprintf(stderr, "[fd phase us] start %.1f-%.1f p1end %.1f-%.1f sync1 %.1f-%.1f p2end %.1f-%.1f sync2 %.1f-%.1f end %.1f-%.1f (grid %d, V %d, rows %lld)\n",

@@ -7,6 +7,7 @@
 // rectsolver._factor_tridiag (rectsolver.py:62-77), plan_rect diag/end
 // modifiers and pivot tolerance (rectsolver.py:122-135,153-163).
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -244,17 +245,21 @@ const double2 *twiddles_for(int device, int n) {
     auto key = std::make_pair(device, n);
     auto it = g_tw.find(key);
     if (it != g_tw.end()) return (const double2 *)it->second;
-    const int L = 2 * (n + 1);
-    std::vector<double2> h(L);
+    const int L = 2 * (n + 1), N = n + 1;
+    const long double PI = 3.141592653589793238462643383279502884L;
+    // [L] twiddles, then [N] real-DST pre-weights (PlanDev::ralpha)
+    std::vector<double2> h(L + (N + 1) / 2);
     for (int t = 0; t < L; ++t) {
-        // e^{-2 pi i t / L} with the angle reduced to the first octant in long double
-        long double a = 2.0L * 3.141592653589793238462643383279502884L * (long double)t / (long double)L;
+        long double a = 2.0L * PI * (long double)t / (long double)L;
         h[t].x = (double)cosl(a);
         h[t].y = (double)(-sinl(a));
     }
+    double *al = reinterpret_cast<double *>(h.data() + L);
+    const long double sc = sqrtl(2.0L / (long double)N);
+    for (int j = 0; j < N; ++j) al[j] = (double)(0.5L * sc * sinl(PI * (long double)j / (long double)N) + 0.25L * sc);
     void *d = nullptr;
-    FD_CUDA(cudaMalloc(&d, sizeof(double2) * L));
-    FD_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
+    FD_CUDA(cudaMalloc(&d, sizeof(double2) * h.size()));
+    FD_CUDA(cudaMemcpy(d, h.data(), sizeof(double2) * h.size(), cudaMemcpyHostToDevice));
     g_tw[key] = d;
     return (const double2 *)d;
 }
@@ -366,11 +371,15 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
         d.dib = upload(p, dib);
         d.db = upload(p, db);
         if (tk == kFFT) {
-            // smem budget of the persistent kernel for one group's slice: 13 KB
-            int lg = 0;
-            while ((1 << lg) < 2 * (n + 1)) ++lg;
-            const int G = 16384 >> lg;                     // rows per group at 512 threads
-            build_long_table(T, m, n, d.off, std::max(0, (13 * 1024 / (G * 24)) & ~1));
+            if (rs_supported(n) && !getenv("FD_OLD")) {
+                build_long_table(T, m, n, d.off, rs_kt_cap(n + 1));
+            } else {
+                // smem budget of the complex-FFT persistent kernel for one group's slice: 13 KB
+                int lg = 0;
+                while ((1 << lg) < 2 * (n + 1)) ++lg;
+                const int G = 16384 >> lg;                     // rows per group at 512 threads
+                build_long_table(T, m, n, d.off, std::max(0, (13 * 1024 / (G * 24)) & ~1));
+            }
         }
         d.kt = T.kt;
         d.ktp = T.ktp;
@@ -380,6 +389,7 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
         d.ye = upload(p, zeros);
         d.fs = upload(p, zeros);
         d.tw = twiddles_for(device, n);
+        d.ralpha = d.tw ? reinterpret_cast<const double *>(d.tw + 2 * (n + 1)) : nullptr;
         d.dense = dense_table_for(device, n);
     } catch (...) {
         for (void *a : p->allocs) cudaFree(a);

@@ -1,0 +1,808 @@
+// Persistent fused rectangle solve with a real-symmetric DST-I
+// (n + 1 = N = 2^NL, 256 <= N <= 2048).
+//
+// Same three phases as persist.cu (DST + local forward elimination | block
+// carries | back-substitution + inverse DST), but the transform of a row pair
+// is ONE N-point complex FFT instead of a 2N-point FFT of the odd extension:
+//
+//   y_j = alpha_j x_j + (alpha_j - s/2) x_{N-j},  alpha_j = s/2 sin(pi j/N) + s/4
+//   c   = y_a + i y_b,  C = FFT_N(c)
+//   X_{2k}   = -(Im C_k - Im C_{N-k})      (row a),   Re C_k - Re C_{N-k}   (row b)
+//   X_{2k+1} = X_{2k-1} + Re C_k + Re C_{N-k} (row a), ... Im (row b),  X_1 = Re C_0
+//
+// (s = sqrt(2/N) the orthonormal factor; the odd outputs are a prefix sum over
+// k, done per pair with a serial/warp-shuffle/cross-warp scan).  This halves the
+// fp64 work of the transform, which bounds the complex-FFT kernel.
+//
+// Shared memory per CTA (one CTA of 512 threads per SM):
+//   P pair regions of (N + N/16) complex: a row pair is TMA-copied into its
+//   region (unpadded, at offset so in {0,1}), transformed in place (padded
+//   Stockham radix-16 passes, pad16(q) = q + q/16), and the transformed rows
+//   are written back padded (xi(q) = q + q/16) for the mode-parallel Thomas
+//   sweep; phase 3 runs the sweep in place on the staged yhat rows first.
+//   Every pair has its own mbarrier, so a pair starts transforming as soon as
+//   its rows have landed.
+#include "persist_common.cuh"
+
+namespace fd {
+
+__device__ __forceinline__ int xi(int q) { return q + (q >> 4); }
+
+template <int NL>
+struct RS {
+    static constexpr int N = 1 << NL;
+    static constexpr int NT = kRsThreads;
+    static constexpr int T = N / 16;                  // threads per row pair
+    static constexpr int P = NT / T;                  // pairs per CTA
+    static constexpr int G = 2 * P;                   // rows per group
+    static constexpr int PADN = N + N / 16;           // complex entries per pair region
+    static constexpr int NMID = (NL - 1) / 4 - 1;
+    static constexpr int RL = 1 << (NL - 4 * ((NL - 1) / 4));
+    static constexpr int NB = N / RL;                 // last-pass butterflies
+    static constexpr int PER = NB / T;                // ... per thread
+    static constexpr int MPT = (N - 1 + NT - 1) / NT; // modes per thread in the sweeps
+    static constexpr int XR = (N - 1) + ((N - 2) >> 4);   // row b of the padded X layout
+    static constexpr size_t REG = size_t(PADN) * 16;
+    static constexpr size_t OFF_TW = size_t(P) * REG;     // m16[16], la[256]
+    static constexpr size_t OFF_AL = OFF_TW + 272 * 16;   // alpha[N]
+    static constexpr size_t OFF_SC = OFF_AL + size_t(N) * 8;
+    static constexpr size_t OFF_LT = OFF_SC + size_t(P) * 16 * 8;
+    static constexpr size_t SMEM = kRsSmem;
+    static_assert(OFF_LT == rs_fixed_smem(N), "layout shared with the plan builder");
+    static_assert(PER * RL == 16, "16 points per thread in the last pass");
+    static_assert(XR * 2 <= PADN * 2, "transformed rows fit the pair region");
+    static_assert(NMID <= 1, "N <= 4096");
+};
+
+// barrier over the T threads of one pair (T = 16: half warp)
+template <int T>
+__device__ __forceinline__ unsigned pair_mask(int pr) {
+    if constexpr (T >= 32) return 0xffffffffu;
+    else return 0xffffu << (16 * (pr & 1));
+}
+template <int T>
+__device__ __forceinline__ void rsync(int pr) {
+    if constexpr (T <= 32) __syncwarp(pair_mask<T>(pr));
+    else asm volatile("bar.sync %0, %1;" ::"r"(1 + pr), "r"(T) : "memory");
+}
+
+template <int NL>
+struct RFft {
+    using C = RS<NL>;
+    static constexpr int N = C::N, T = C::T, RL = C::RL, NB = C::NB, PER = C::PER;
+
+    // pre-weighted input of the first pass: v[r] = y_a(j) + i y_b(j), j = t + r T
+    __device__ static void load(double2 (&v)[16], const double *A, const double *B, const double *al,
+                                double h2, int t) {
+        const bool HB = B != nullptr;
+        if (!HB) B = A;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int j = t + r * T;
+            if (r == 0 && t == 0) {
+                v[0] = make_double2(0.0, 0.0);   // x_0 = x_N = 0
+                continue;
+            }
+            const double a = al[j], b = a - h2;
+            const int i1 = j - 1, i2 = N - 1 - j;
+            v[r].x = fma(a, A[i1], b * A[i2]);
+            v[r].y = HB ? fma(a, B[i1], b * B[i2]) : 0.0;
+        }
+    }
+    __device__ static void first(double2 *buf, double2 (&v)[16], int t, int pr) {
+        dft<16>(v);
+        double2 *w = buf + 17 * t;   // pad16(16 t + r)
+#pragma unroll
+        for (int r = 0; r < 16; ++r) w[r] = v[r];
+        rsync<T>(pr);
+    }
+    __device__ static void mid(double2 *buf, const double2 *m16, int t, int pr) {
+        constexpr int RS_ = T + T / 16;
+        double2 v[16];
+        const double2 *rd = buf + xi(t);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = rd[r * RS_];
+        const int jm = t & 15;
+        const double2 w = m16[jm];
+        rsync<T>(pr);
+        apply_powers<16>(v, w);
+        dft<16>(v);
+        double2 *wr = buf + xi((t >> 4) * 256 + jm);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) wr[r * 17] = v[r];
+        rsync<T>(pr);
+    }
+    // last pass, in place: output o = j + r NB lands where its input was read
+    __device__ static void last(double2 *buf, const double2 *la, int t, int pr) {
+        constexpr int RS_ = NB + NB / 16, US = T + T / 16;
+        double2 v[PER][RL];
+        double2 *rd = buf + xi(t);
+#pragma unroll
+        for (int u = 0; u < PER; ++u)
+#pragma unroll
+            for (int r = 0; r < RL; ++r) v[u][r] = rd[u * US + r * RS_];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            apply_powers<RL>(v[u], la[t + u * T]);
+            dft<RL>(v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u)
+#pragma unroll
+            for (int r = 0; r < RL; ++r) rd[u * US + r * RS_] = v[u][r];
+        rsync<T>(pr);
+    }
+    // C -> transformed rows (padded X layout) of A (and B when HB)
+    __device__ static void post(double2 *buf, double *scr, int t, int pr, int lane, double *XA, double *XB) {
+        const bool HB = XB != nullptr;
+        double ea[8], eb[8], da[8], db[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = 8 * t + i;
+            const double2 c = buf[xi(k)];
+            double2 c2 = make_double2(0.0, 0.0);
+            if (i > 0 || t > 0) c2 = buf[xi(N - k)];
+            ea[i] = c2.y - c.y;
+            eb[i] = c.x - c2.x;
+            da[i] = c.x + c2.x;
+            db[i] = c.y + c2.y;
+        }
+#pragma unroll
+        for (int i = 1; i < 8; ++i) {
+            da[i] += da[i - 1];
+            db[i] += db[i - 1];
+        }
+        constexpr int W = T < 32 ? T : 32;
+        const unsigned mask = pair_mask<T>(pr);
+        double ia = da[7], ib = db[7];
+#pragma unroll
+        for (int o = 1; o < W; o <<= 1) {
+            const double xa = __shfl_up_sync(mask, ia, o, W), xb = __shfl_up_sync(mask, ib, o, W);
+            if ((lane & (W - 1)) >= o) {
+                ia += xa;
+                ib += xb;
+            }
+        }
+        double pa = __shfl_up_sync(mask, ia, 1, W), pb = __shfl_up_sync(mask, ib, 1, W);
+        if ((lane & (W - 1)) == 0) {
+            pa = 0.0;
+            pb = 0.0;
+        }
+        if constexpr (T > 32) {
+            const int w = t >> 5;
+            if (lane == 31) {
+                scr[(pr * 8 + w) * 2] = ia;
+                scr[(pr * 8 + w) * 2 + 1] = ib;
+            }
+            rsync<T>(pr);
+            double sa = 0.0, sb = 0.0;
+#pragma unroll
+            for (int q = 0; q < T / 32 - 1; ++q)
+                if (q < w) {
+                    sa += scr[(pr * 8 + q) * 2];
+                    sb += scr[(pr * 8 + q) * 2 + 1];
+                }
+            pa += sa;
+            pb += sb;
+        } else {
+            rsync<T>(pr);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = 8 * t + i;
+            if (i > 0 || t > 0) XA[xi(2 * k - 1)] = ea[i];
+            XA[xi(2 * k)] = da[i] + pa;
+            if (HB) {
+                if (i > 0 || t > 0) XB[xi(2 * k - 1)] = eb[i];
+                XB[xi(2 * k)] = db[i] + pb;
+            }
+        }
+    }
+    // full transform of the staged rows A (, B) -> padded X rows in the same region
+    __device__ __forceinline__ static void run(double2 *buf, const double *A, const double *B, const double *al,
+                                            double h2, const double2 *m16, const double2 *la, double *scr, int t,
+                                            int pr, int lane, double *XA, double *XB) {
+        double2 v[16];
+        load(v, A, B, al, h2, t);
+        rsync<T>(pr);   // the staged rows alias the exchange buffer
+        first(buf, v, t, pr);
+        if constexpr (C::NMID > 0) mid(buf, m16, t, pr);
+        last(buf, la, t, pr);
+        post(buf, scr, t, pr, lane, XA, XB);
+    }
+};
+
+// Transient factors of mode k (modes >= kt, rows i < len): the row-major
+// tables hold rows < ecap; beyond them (only when the long-transient table was
+// capped) beta is rebuilt bitwise from the last table row with the reference
+// recurrence (rectsolver.py:72-73).
+__device__ __noinline__ double beta_rebuild(const PlanDev &p, int k, int i) {
+    const double lam = mode_lam(p, k);
+    double b = __ldg(p.db + size_t(p.ecap - 1) * p.n + k);
+    for (int q = p.ecap; q <= i; ++q) {
+        const double d = diag_at(p, lam, q);
+        b = __dsub_rn(d, __dmul_rn(p.off, __ddiv_rn(p.off, b)));
+    }
+    return b;
+}
+// beta_i for a row of a transient group (0 <= i < m)
+__device__ __forceinline__ double beta_tr(const PlanDev &p, int k, int i, int len, double blast, double binf) {
+    if (i == p.m - 1) return blast;
+    if (i >= len) return binf;
+    if (i < p.ecap) return __ldg(p.db + size_t(i) * p.n + k);
+    return beta_rebuild(p, k, i);
+}
+// Factors of row i of mode k (k >= kt) for rows beyond the row-major tables
+// (only when the long-transient table was capped): l_i, 1/beta_i, beta_{i-1}.
+__device__ __noinline__ void factors_slow(const PlanDev &p, int k, int i, int len, double l_inf, double ib_inf,
+                                          double ib_last, double b_inf, double *l, double *ib, double *bm1) {
+    if (i >= len) {
+        *l = l_inf;
+        *ib = (i == p.m - 1) ? ib_last : ib_inf;
+        *bm1 = (i - 1 < len) ? beta_tr(p, k, i - 1, len, 0.0, b_inf) : b_inf;
+        return;
+    }
+    const double bp = (i == 0) ? 0.0 : beta_tr(p, k, i - 1, len, 0.0, b_inf);
+    const double d = diag_at(p, mode_lam(p, k), i);
+    const double li = (i == 0) ? 0.0 : __ddiv_rn(p.off, bp);
+    *l = li;
+    *ib = 1.0 / ((i == 0) ? d : __dsub_rn(d, __dmul_rn(p.off, li)));
+    *bm1 = bp;
+}
+
+template <int NL>
+__global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_constant__ PList pl) {
+    using C = RS<NL>;
+    using F = RFft<NL>;
+    constexpr int NT = C::NT, G = C::G, P = C::P, T = C::T, MPT = C::MPT, XR = C::XR;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    auto regd = [&](int q) { return reinterpret_cast<double *>(smem_raw + size_t(q) * C::REG); };
+    auto regc = [&](int q) { return reinterpret_cast<double2 *>(smem_raw + size_t(q) * C::REG); };
+    double2 *m16 = reinterpret_cast<double2 *>(smem_raw + C::OFF_TW);
+    double2 *la = m16 + 16;
+    double *al = reinterpret_cast<double *>(smem_raw + C::OFF_AL);
+    double *scr = reinterpret_cast<double *>(smem_raw + C::OFF_SC);
+    double *lts = reinterpret_cast<double *>(smem_raw + C::OFF_LT);   // [G][3][ktp]
+    __shared__ __align__(8) uint64_t pbar[P];
+    __shared__ __align__(8) uint64_t ltbar;
+    __shared__ Seg segs[kMaxSegs];
+    __shared__ int nseg_s, nitems_s;
+
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int n = pl.n;
+    const int pr = tid / T, t = tid % T;
+    cg::grid_group grid = cg::this_grid();
+    auto stamp = [&](int slot) {
+        if (pl.tstamp && tid == 0) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g));
+            pl.tstamp[blockIdx.x * 8 + slot] = g;
+        }
+    };
+    auto trace = [&](int role, int item, int which) {   // FD_TRACE=<cta>
+        if (pl.trace && (role >= 8 ? t == 0 : tid == 0) && blockIdx.x == pl.trace_cta && item < 64 && role < 16) {
+            unsigned long long g;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g)::"memory");
+            pl.trace[(role * 64 + item) * 2 + which] = g;
+        }
+    };
+    stamp(0);
+
+    if (tid == 0) {
+        int ns = 0, items = 0;
+        for (int v = blockIdx.x; v < pl.V; v += gridDim.x) {
+            const long long lo = pl.total_rows * v / pl.V, hi = pl.total_rows * (v + 1) / pl.V;
+            for (int j = 0; j < pl.count; ++j) {
+                const long long r0 = pl.job[j].row0, r1 = r0 + pl.job[j].p.m;
+                if (r0 < hi && r1 > lo && ns < kMaxSegs) {
+                    Seg sg;
+                    sg.job = j;
+                    sg.s = int(max(lo, r0) - r0);
+                    sg.e = int(min(hi, r1) - r0) - 1;
+                    sg.blk = pl.job[j].blk_base + (v - pl.job[j].c_first);
+                    sg.ngroups = (sg.e - sg.s + G) / G;
+                    sg.item0 = items;
+                    items += sg.ngroups;
+                    segs[ns++] = sg;
+                }
+            }
+        }
+        nseg_s = ns;
+        nitems_s = items;
+        for (int q = 0; q < P; ++q) mbar_init(&pbar[q], 1);
+        mbar_init(&ltbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    {
+        constexpr int N = C::N;
+        const double2 *tw = pl.job[0].p.tw;   // e^{-2 pi i q / 2N}
+        const double *ra = pl.job[0].p.ralpha;
+        for (int q = tid; q < 16; q += NT) m16[q] = __ldg(tw + q * (N / 128));
+        for (int q = tid; q < C::NB; q += NT) la[q] = __ldg(tw + 2 * q);
+        for (int q = tid; q < N; q += NT) al[q] = __ldg(ra + q);
+    }
+    __syncthreads();
+    const int nseg = nseg_s, nitems = nitems_s;
+    uint32_t ppar = 0, ltpar = 0;
+
+    auto item_of = [&](int it, int &si, int &g0, int &rows, bool desc) {
+        si = 0;
+        while (si + 1 < nseg && it >= segs[si + 1].item0) ++si;
+        const Seg &sg = segs[si];
+        const int gi = it - sg.item0;
+        const int gg = desc ? (sg.ngroups - 1 - gi) : gi;
+        g0 = sg.s + gg * G;
+        rows = min(G, sg.e - g0 + 1);
+    };
+    auto group_mask = [&](int rows) {   // pairs holding rows of the group
+        const int np = (rows + 1) >> 1;
+        return np >= 32 ? 0xffffffffu : ((1u << np) - 1u);
+    };
+    // this pair's rows [g0 + 2 pr, +rp) of base -> its region (lands at offset so)
+    auto issue_pair = [&](const double *base, int g0, int rows, int m) {
+        Tail tl{0.0, -1};
+        const int r0 = 2 * pr, rp = min(2, rows - r0);
+        if (rp <= 0) return tl;
+        const uintptr_t start = reinterpret_cast<uintptr_t>(base + size_t(g0 + r0) * n);
+        const uintptr_t end = start + uintptr_t(rp) * n * sizeof(double);
+        const uintptr_t a = start & ~uintptr_t(15);
+        const uintptr_t e = (g0 + r0 + rp >= m) ? (end & ~uintptr_t(15)) : ((end + 15) & ~uintptr_t(15));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&pbar[pr], uint32_t(e - a));
+        tma_load_1d(regd(pr), reinterpret_cast<const void *>(a), uint32_t(e - a), &pbar[pr]);
+        if (end != e) {
+            tl.v = __ldcg(reinterpret_cast<const double *>(e));
+            tl.idx = int((e - a) / 8);
+        }
+        return tl;
+    };
+    auto issue_lts = [&](const PlanDev &p, int g0, int rows) {
+        const uint32_t bytes = uint32_t(rows) * 3u * uint32_t(p.ktp) * 8u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&ltbar, bytes);
+        tma_load_1d(lts, p.lt + size_t(g0) * 3 * p.ktp, bytes, &ltbar);
+    };
+    auto pair_tail = [&](const double *base, int g0, int rows, int m) {
+        const int r0 = 2 * pr, rp = min(2, rows - r0);
+        if (rp <= 0) return false;
+        const uintptr_t end = reinterpret_cast<uintptr_t>(base + size_t(g0 + r0 + rp) * n);
+        return (g0 + r0 + rp >= m) && (end & 15);
+    };
+
+    // ===================== phase 1: DST + local forward elimination ===================
+    {
+        double ys[MPT], pis[MPT], fss[MPT], s2s[MPT], ccs[MPT];
+        double cl[MPT], cib[MPT], cbl[MPT], cibl[MPT];
+        int clen[MPT];
+        Tail tail{0.0, -1};
+        if (nitems > 0) {
+            int si, g0, rows;
+            item_of(0, si, g0, rows, false);
+            const PJob &J = pl.job[segs[si].job];
+            if (t == 0) tail = issue_pair(J.in, g0, rows, J.p.m);
+            if (tid == 0 && J.p.lt) issue_lts(J.p, g0, rows);
+        }
+#pragma unroll 1
+        for (int it = 0; it < nitems; ++it) {
+            int si, g0, rows;
+            item_of(it, si, g0, rows, false);
+            const Seg sg = segs[si];
+            const PJob &J = pl.job[sg.job];
+            const PlanDev &p = J.p;
+            const double off = p.off;
+            const int so = stg_off(J.in, g0, n);
+            const int rp = min(2, rows - 2 * pr);
+            trace(0, it, 0);
+            if (rp > 0) {
+                mbar_wait(&pbar[pr], (ppar >> pr) & 1u);
+                if (pair_tail(J.in, g0, rows, p.m)) {
+                    if (t == 0) regd(pr)[tail.idx] = tail.v;
+                    rsync<T>(pr);
+                }
+                double *base = regd(pr) + so;
+                F::run(regc(pr), base, rp > 1 ? base + n : nullptr, al, 0.5 * p.scale, m16, la, scr, t, pr, lane,
+                       regd(pr), rp > 1 ? regd(pr) + XR : nullptr);
+            }
+            ppar ^= group_mask(rows);
+            if (p.lt) {
+                mbar_wait(&ltbar, ltpar);
+                ltpar ^= 1u;
+            }
+            __syncthreads();   // all rows of the group transformed
+            trace(0, it, 1);
+            auto xrow = [&](int rr) { return regd(rr >> 1) + (rr & 1) * XR; };
+            const bool first = (g0 == sg.s), last = (g0 + rows - 1 == sg.e);
+            double *outg = J.out + size_t(g0) * n;
+            const int mlast = p.m - 1;
+#pragma unroll
+            for (int u = 0; u < MPT; ++u) {
+                const int k = tid + u * NT;
+                if (k >= n) continue;
+                double y = ys[u], w = pis[u], f = fss[u], s2 = s2s[u];
+                if (first) {
+                    ModeRec c;
+                    c.load(p, k);
+                    cl[u] = c.l_inf;
+                    cib[u] = c.ib_inf;
+                    cbl[u] = c.b_last;
+                    cibl[u] = 1.0 / c.b_last;
+                    clen[u] = c.len;
+                }
+                const int len = clen[u];
+                const double l_inf = cl[u], ib_inf = cib[u], ibm = cibl[u];
+                const int xk = xi(k);
+                double *og = outg + k;
+                // one row of the local forward elimination (rectsolver.py:86) with
+                // factors (l, 1/beta), accumulating the block scalars
+                auto step = [&](int rr, double l, double ib) {
+                    y = __dsub_rn(xrow(rr)[xk], __dmul_rn(l, y));
+                    w = -l * w;
+                    const double W = w * ib;
+                    f = fma(y, W, f);
+                    s2 = fma(w, W, s2);
+                    og[rr * n] = y;
+                };
+                int rr = 0;
+                if (first) {   // block start: y = r, pi = 1, P_i = -l_s pi_i
+                    double l0 = l_inf, ib0 = (g0 == mlast) ? ibm : ib_inf;
+                    if (k < p.kt) {
+                        l0 = lts[k];
+                        ib0 = lts[p.ktp + k];
+                    } else if (g0 < len) {
+                        if (g0 < p.ecap) {
+                            l0 = __ldg(p.dl + size_t(g0) * n + k);
+                            ib0 = __ldg(p.dib + size_t(g0) * n + k);
+                        } else {
+                            double bm1;
+                            factors_slow(p, k, g0, len, l_inf, ib_inf, ibm, 0.0, &l0, &ib0, &bm1);
+                        }
+                    }
+                    y = xrow(0)[xk];
+                    w = 1.0;
+                    f = y * ib0;
+                    s2 = ib0;
+                    ccs[u] = (g0 == 0) ? 0.0 : -l0;
+                    og[0] = y;
+                    rr = 1;
+                }
+                if (k < p.kt) {
+                    // slowly converging low mode: reference factors from the table
+                    const double *tb = lts + k;
+#pragma unroll 4
+                    for (; rr < rows; ++rr) step(rr, tb[rr * 3 * p.ktp], tb[rr * 3 * p.ktp + p.ktp]);
+                } else if (g0 + rr < len && g0 + rows <= p.ecap) {
+                    // transient rows: the reference factors (rectsolver.py:72-73) from
+                    // the row-major tables, 8 rows of loads ahead of their sweep
+#pragma unroll 1
+                    for (; rr < rows; rr += 8) {
+                        double lv[8], ibv[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const int i = g0 + rr + q;
+                            const bool tr = (rr + q < rows) && (i < len);
+                            lv[q] = tr ? __ldg(p.dl + size_t(i) * n + k) : l_inf;
+                            ibv[q] = tr ? __ldg(p.dib + size_t(i) * n + k) : ((i == mlast) ? ibm : ib_inf);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            if (rr + q < rows) step(rr + q, lv[q], ibv[q]);
+                    }
+                } else if (g0 + rr < len) {
+#pragma unroll 1
+                    for (; rr < rows; ++rr) {   // beyond the tables (capped long-transient table)
+                        double l, ib, bm1;
+                        factors_slow(p, k, g0 + rr, len, l_inf, ib_inf, ibm, 0.0, &l, &ib, &bm1);
+                        step(rr, l, ib);
+                    }
+                } else {
+#pragma unroll 4
+                    for (; rr < rows; ++rr) step(rr, l_inf, (g0 + rr == mlast) ? ibm : ib_inf);
+                }
+                const double cc = ccs[u];
+                ys[u] = y;
+                pis[u] = w;
+                fss[u] = f;
+                s2s[u] = s2;
+                if (last) {
+                    double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
+                    const int e = sg.e;
+                    // Q = pi_e * (-l_{e+1}),  l_{e+1} = delta / beta_e
+                    double lnext = l_inf;
+                    if (k < p.kt) lnext = (e + 1 < p.m) ? __ldg(p.lt + size_t(e + 1) * 3 * p.ktp + k) : 0.0;
+                    else if (e + 1 < len && e + 1 < p.ecap)
+                        lnext = __ldg(p.dl + size_t(e + 1) * n + k);
+                    else if (e + 1 < len) {
+                        double ib_, bm1_;
+                        factors_slow(p, k, e + 1, len, l_inf, ib_inf, ibm, 0.0, &lnext, &ib_, &bm1_);
+                    }
+                    const double Q = (e < p.m - 1) ? w * (-lnext) : 0.0;
+                    __stcg(cb + 0 * n, y);
+                    __stcg(cb + 1 * n, f);
+                    __stcg(cb + 2 * n, cc * w);
+                    __stcg(cb + 3 * n, cc * s2);
+                    __stcg(cb + 4 * n, Q);
+                }
+            }
+            __syncthreads();   // regions and the table slice consumed
+            trace(1, it, 1);
+            if (it + 1 < nitems) {
+                int si2, g2, rows2;
+                item_of(it + 1, si2, g2, rows2, false);
+                const PJob &J2 = pl.job[segs[si2].job];
+                if (t == 0) tail = issue_pair(J2.in, g2, rows2, J2.p.m);
+                if (tid == 0 && J2.p.lt) issue_lts(J2.p, g2, rows2);
+            }
+        }
+    }
+    stamp(1);
+    grid.sync();
+    stamp(2);
+
+    // ===================== phase 2: block carries =====================================
+    // One CTA per (job, 32 modes): every block's scalars staged through shared
+    // memory (inside the pair regions; the tables behind them stay intact), warp 0
+    // (lane = mode) runs both short recurrences, then Y and X go back.
+    {
+        constexpr int CHB = int(C::OFF_TW / (7 * 32 * 8)) < 96 ? int(C::OFF_TW / (7 * 32 * 8)) : 96;
+        double *sv = reinterpret_cast<double *>(smem_raw);   // [CHB][7][32]
+        const int chunks = (n + 31) / 32;
+        const size_t bs = size_t(kCarryVals) * n;
+        for (int item = blockIdx.x; item < pl.count * chunks; item += gridDim.x) {
+            const PJob &J = pl.job[item / chunks];
+            const int k0 = (item % chunks) * 32;
+            double *cb = pl.carry + size_t(J.blk_base) * bs + k0;
+            const int nb = J.nblk;
+            const bool lane_ok = (tid < 32) && (k0 + lane < n);
+            double prev = 0.0, next = 0.0;
+            if (nb <= CHB) {
+                for (int idx = tid; idx < nb * 160; idx += NT) {   // 5 values x 32 modes per block
+                    const int b = idx / 160, v = (idx >> 5) % 5, kk = idx & 31;
+                    sv[(b * 7 + v) * 32 + kk] = (k0 + kk < n) ? __ldcg(cb + b * bs + v * n + kk) : 0.0;
+                }
+                __syncthreads();
+                if (lane_ok) {
+                    for (int b = 0; b < nb; ++b) {
+                        const double *q = sv + b * 7 * 32 + lane;
+                        const double y = (b == 0) ? q[0] : fma(q[2 * 32], prev, q[0]);
+                        sv[(b * 7 + 5) * 32 + lane] = y;
+                        prev = y;
+                    }
+                    for (int b = nb - 1; b >= 0; --b) {
+                        const double *q = sv + b * 7 * 32 + lane;
+                        double x = q[1 * 32];
+                        if (b > 0) x = fma(sv[((b - 1) * 7 + 5) * 32 + lane], q[3 * 32], x);
+                        if (b < nb - 1) x = fma(q[4 * 32], next, x);
+                        sv[(b * 7 + 6) * 32 + lane] = x;
+                        next = x;
+                    }
+                }
+                __syncthreads();
+                for (int idx = tid; idx < nb * 64; idx += NT) {
+                    const int b = idx >> 6, v = 5 + ((idx >> 5) & 1), kk = idx & 31;
+                    if (k0 + kk < n) __stcg(cb + b * bs + v * n + kk, sv[(b * 7 + v) * 32 + kk]);
+                }
+                __syncthreads();
+            } else if (lane_ok) {
+                for (int b = 0; b < nb; ++b) {
+                    const double ye = __ldcg(cb + b * bs + lane), pe = __ldcg(cb + b * bs + 2 * n + lane);
+                    const double y = (b == 0) ? ye : fma(pe, prev, ye);
+                    __stcg(cb + b * bs + 5 * n + lane, y);
+                    prev = y;
+                }
+                for (int b = nb - 1; b >= 0; --b) {
+                    double x = __ldcg(cb + b * bs + 1 * n + lane);
+                    if (b > 0) x = fma(__ldcg(cb + (b - 1) * bs + 5 * n + lane), __ldcg(cb + b * bs + 3 * n + lane), x);
+                    if (b < nb - 1) x = fma(__ldcg(cb + b * bs + 4 * n + lane), next, x);
+                    __stcg(cb + b * bs + 6 * n + lane, x);
+                    next = x;
+                }
+            }
+        }
+    }
+    stamp(3);
+    grid.sync();
+    stamp(4);
+
+    // ===================== phase 3: back-substitution + inverse DST ===================
+    {
+        double xs[MPT], yins[MPT], pcs[MPT];
+        double cib_inf[MPT], cinv[MPT], cibl[MPT];
+        int clen[MPT];
+        Tail tail{0.0, -1};
+        if (nitems > 0) {
+            int si, g0, rows;
+            item_of(0, si, g0, rows, true);
+            const PJob &J = pl.job[segs[si].job];
+            if (t == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                tail = issue_pair(J.out, g0, rows, J.p.m);
+            }
+            if (tid == 0 && J.p.lt) issue_lts(J.p, g0, rows);
+        }
+#pragma unroll 1
+        for (int it = 0; it < nitems; ++it) {
+            int si, g0, rows;
+            item_of(it, si, g0, rows, true);
+            const Seg sg = segs[si];
+            const PJob &J = pl.job[sg.job];
+            const PlanDev &p = J.p;
+            const double off = p.off;
+            const bool top = (g0 + rows - 1 == sg.e);
+            const bool has_in = sg.blk > J.blk_base;                 // block does not start at row 0
+            const bool has_next = sg.blk < J.blk_base + J.nblk - 1;  // a block below carries X
+            const int so = stg_off(J.out, g0, n);
+            trace(2, it, 0);
+            const uint32_t gm = group_mask(rows);
+#pragma unroll 1
+            for (int q = 0; q < P; ++q)
+                if ((gm >> q) & 1u) mbar_wait(&pbar[q], (ppar >> q) & 1u);
+            ppar ^= gm;
+            if (p.lt) {
+                mbar_wait(&ltbar, ltpar);
+                ltpar ^= 1u;
+            }
+            if (has_tail(J.out, g0, rows, n, p.m)) {
+                if (t == 0 && tail.idx >= 0) regd(pr)[tail.idx] = tail.v;
+                __syncthreads();
+            }
+            trace(2, it, 1);
+            auto yrow = [&](int rr) { return regd(rr >> 1) + so + (rr & 1) * n; };
+#pragma unroll
+            for (int u = 0; u < MPT; ++u) {
+                const int k = tid + u * NT;
+                if (k >= n) continue;
+                if (top) {
+                    ModeRec c;
+                    c.load(p, k);
+                    cib_inf[u] = c.ib_inf;
+                    cinv[u] = c.inv_nl;
+                    cibl[u] = 1.0 / c.b_last;
+                    clen[u] = c.len;
+                    const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
+                    const size_t bs = size_t(kCarryVals) * n;
+                    xs[u] = has_next ? __ldcg(cb + bs + 6 * n) : 0.0;
+                    yins[u] = has_in ? __ldcg(cb - bs + 5 * n) : 0.0;
+                    pcs[u] = __ldcg(cb + 2 * n);
+                }
+                double x = xs[u], Pc = pcs[u];
+                const double yin = yins[u];
+                const int len = clen[u];
+                const double ib_inf = cib_inf[u];
+                if (k < p.kt) {
+                    const double *tb = lts + k;
+#pragma unroll 4
+                    for (int rr = rows - 1; rr >= 0; --rr) {
+                        double *yp = yrow(rr) + k;
+                        double y = *yp;
+                        if (has_in) {
+                            y = fma(Pc, yin, y);
+                            Pc *= tb[rr * 3 * p.ktp + 2 * p.ktp];   // P_{i-1} = -P_i beta_{i-1} / delta
+                        }
+                        x = __dsub_rn(y, __dmul_rn(off, x)) * tb[rr * 3 * p.ktp + p.ktp];   // rectsolver.py:90
+                        *yp = x;
+                    }
+                } else if (g0 < len && g0 + rows <= p.ecap) {
+                    // transient rows: reference factors from the row-major tables,
+                    // 8 rows of loads ahead of their sweep
+                    const double ib_m = cibl[u], inl = cinv[u], nio = -1.0 / off;
+                    const int mlast = p.m - 1;
+#pragma unroll 1
+                    for (int r1 = rows; r1 > 0; r1 -= 8) {   // rows r1 - 1, r1 - 2, ... descending
+                        double ibv[8], pmv[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const int i = g0 + r1 - 1 - q;
+                            const bool in = q < r1;
+                            ibv[q] = (in && i < len) ? __ldg(p.dib + size_t(i) * n + k) : ((i == mlast) ? ib_m : ib_inf);
+                            pmv[q] = (in && i >= 1 && i - 1 < len) ? __ldg(p.db + size_t(i - 1) * n + k) * nio : inl;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            if (q < r1) {
+                                double *yp = yrow(r1 - 1 - q) + k;
+                                double y = *yp;
+                                if (has_in) {
+                                    y = fma(Pc, yin, y);
+                                    Pc *= pmv[q];   // P_{i-1} = P_i / (-l_i) = -P_i beta_{i-1} / delta
+                                }
+                                x = __dsub_rn(y, __dmul_rn(off, x)) * ibv[q];   // rectsolver.py:90
+                                *yp = x;
+                            }
+                        }
+                    }
+                } else if (g0 < len) {
+                    const double nio = -1.0 / off;
+#pragma unroll 1
+                    for (int rr = rows - 1; rr >= 0; --rr) {   // beyond the tables (rare)
+                        double l, ib, bm1;
+                        factors_slow(p, k, g0 + rr, len, 0.0, cib_inf[u], cibl[u], mode_binf(p, k), &l, &ib, &bm1);
+                        double *yp = yrow(rr) + k;
+                        double y = *yp;
+                        if (has_in) {
+                            y = fma(Pc, yin, y);
+                            Pc *= bm1 * nio;
+                        }
+                        x = __dsub_rn(y, __dmul_rn(off, x)) * ib;   // rectsolver.py:90
+                        *yp = x;
+                    }
+                } else {
+                    const double ib_m = cibl[u], inl = cinv[u];
+                    const int mlast = p.m - 1;
+#pragma unroll 4
+                    for (int rr = rows - 1; rr >= 0; --rr) {
+                        double *yp = yrow(rr) + k;
+                        double y = *yp;
+                        if (has_in) {
+                            y = fma(Pc, yin, y);
+                            Pc *= inl;
+                        }
+                        const double ib = (g0 + rr == mlast) ? ib_m : ib_inf;
+                        x = __dsub_rn(y, __dmul_rn(off, x)) * ib;   // rectsolver.py:90
+                        *yp = x;
+                    }
+                }
+                xs[u] = x;
+                pcs[u] = Pc;
+            }
+            trace(5, it, 0);
+            __syncthreads();   // swept rows complete, table slice consumed
+            trace(3, it, 0);
+            int si2 = 0, g2 = 0, rows2 = 0;
+            const bool more = it + 1 < nitems;
+            if (more) item_of(it + 1, si2, g2, rows2, true);
+            if (tid == 0 && more && pl.job[segs[si2].job].p.lt) issue_lts(pl.job[segs[si2].job].p, g2, rows2);
+            const int rp = min(2, rows - 2 * pr);
+            if (rp > 0) {
+                trace(8 + pr, it, 0);
+                double *base = regd(pr) + so;
+                double *XA = regd(pr), *XB = regd(pr) + XR;
+                F::run(regc(pr), base, rp > 1 ? base + n : nullptr, al, 0.5 * p.scale, m16, la, scr, t, pr, lane,
+                       XA, rp > 1 ? XB : nullptr);
+                rsync<T>(pr);
+                trace(8 + pr, it, 1);
+                const double al_ = J.alpha, be_ = J.beta;
+#pragma unroll 1
+                for (int h = 0; h < rp; ++h) {
+                    const double *X = h ? XB : XA;
+                    double *o = J.out + size_t(g0 + 2 * pr + h) * n;
+                    if (J.other) {
+                        const double *qo = J.other + size_t(g0 + 2 * pr + h) * n;
+                        for (int k = t; k < n; k += T) o[k] = fma(be_, __ldg(qo + k), al_ * X[xi(k)]);
+                    } else if (al_ == 1.0) {
+                        for (int k = t; k < n; k += T) o[k] = X[xi(k)];
+                    } else {
+                        for (int k = t; k < n; k += T) o[k] = al_ * X[xi(k)];
+                    }
+                }
+                rsync<T>(pr);   // region free
+                trace(4, it, 1);
+            }
+            if (more && t == 0) tail = issue_pair(pl.job[segs[si2].job].out, g2, rows2, pl.job[segs[si2].job].p.m);
+            trace(3, it, 1);
+        }
+    }
+    stamp(5);
+}
+
+// ---------------------------------------------------------------------------
+template <int NL>
+struct RsK {
+    static constexpr int NT = kRsThreads, G = RS<NL>::G;
+    static constexpr size_t SMEM = RS<NL>::SMEM;
+    static const void *fn() { return (const void *)rsolve_kernel<NL>; }
+};
+
+bool launch_rsolve(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
+    static const bool old = getenv("FD_OLD") != nullptr;
+    const int n = jobs[0].p.n;
+    if (old || !rs_supported(n) || !jobs[0].p.ralpha) return false;
+    switch (n + 1) {
+        case 256: run_persist<RsK<8>>(jobs, s, ws); return true;
+        case 512: run_persist<RsK<9>>(jobs, s, ws); return true;
+        case 1024: run_persist<RsK<10>>(jobs, s, ws); return true;
+        case 2048: run_persist<RsK<11>>(jobs, s, ws); return true;
+        default: return false;
+    }
+}
+
+}  // namespace fd

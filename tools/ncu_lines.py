@@ -1,49 +1,26 @@
-"""Aggregate ncu source-page stall samples by CUDA source line:
-   python tools/ncu_lines.py report.ncu-rep [N]"""
-import collections
-import csv
-import io
-import subprocess
-import sys
-
-rep = sys.argv[1]
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(out)))
-cur, hdr = None, None
-agg = collections.defaultdict(collections.Counter)
-text = {}
+"""Top source lines of an ncu source export (--page source --csv --print-source cuda,sass)."""
+import csv, sys
+rows = list(csv.reader(open(sys.argv[1])))
+f = None; out = []; hdr = None
 for r in rows:
-    if not r:
-        continue
-    if r[0] == "File Path":
-        cur = r[1].split("/")[-1]
-        continue
-    if r[0] in ("Function Name",):
-        continue
-    if r[0] == "Line No":
-        hdr = r
-        continue
-    if hdr is None:
-        continue
-    try:
-        ln = int(r[0])
-    except ValueError:
-        continue
-    text[(cur, ln)] = r[1]
-    wi = hdr.index("Warp Stall Sampling (All Samples)")
-    v = r[wi] if len(r) > wi else ""
-    if v and v.replace(".", "").isdigit():
-        agg[(cur, ln)]["all"] += float(v)
-        for i, name in enumerate(hdr):
-            if name.startswith("stall_") and "Not Issued" not in name:
-                x = r[i]
-                if x and x.replace(".", "").isdigit():
-                    agg[(cur, ln)][name[6:]] += float(x)
-tot = sum(c["all"] for c in agg.values())
-print("total samples", tot)
-for k, c in sorted(agg.items(), key=lambda kv: -kv[1]["all"])[:top]:
-    st = sorted([(n, v) for n, v in c.items() if n != "all"], key=lambda x: -x[1])[:3]
-    print(f"{c['all']:6.0f} {100*c['all']/tot:5.1f}% {k[0]}:{k[1]} {text.get(k,'').strip()[:60]} | " +
-          " ".join(f"{n}={v:.0f}" for n, v in st))
+    if r and r[0] == "File Path": f = r[1].split("/")[-1]; continue
+    if r and r[0] == "Line No": hdr = r; continue
+    if hdr and len(r) > 8 and r[2] == "-":
+        try: out.append((int(r[4]), int(r[7]), f, r[0], r[1][:90]))
+        except ValueError: pass
+tot = sum(o[0] for o in out); ti = sum(o[1] for o in out)
+print("total samples", tot, "warp insts", ti)
+for s, i, f, ln, src in sorted(out, reverse=True)[: int(sys.argv[2]) if len(sys.argv) > 2 else 40]:
+    print(f"{100*s/tot:5.1f}% {100*i/ti:5.1f}%i {f}:{ln} {src}")
+if len(sys.argv) > 3:
+    import collections
+    agg = collections.defaultdict(lambda: [0, 0])
+    for s, i, f, ln, src in out:
+        key = f
+        if f == "persist.cu":
+            l = int(ln)
+            for lo, hi, name in [(0, 150, "setup"), (150, 200, "p1 wait/fft"), (200, 295, "p1 thomas"), (295, 365, "p2"), (365, 418, "p3 setup"), (418, 505, "p3 thomas"), (505, 540, "p3 fft")]:
+                if lo <= l < hi: key = "persist.cu " + name
+        agg[key][0] += s; agg[key][1] += i
+    for k, (s, i) in sorted(agg.items(), key=lambda x: -x[1][0]):
+        print(f"{100*s/tot:5.1f}% {100*i/ti:5.1f}%i {k}")
