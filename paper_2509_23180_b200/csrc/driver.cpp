@@ -142,6 +142,8 @@ static SolveJob job_of(const Plan *p, const double *in, double *out) {
     j.beta = 0.0;
     j.other = nullptr;
     j.ws = const_cast<Workspace *>(&p->ws);
+    j.tprof = p->tprof.data();
+    j.tlen = (int)p->tprof.size();
     return j;
 }
 

@@ -114,6 +114,7 @@ struct Plan {
     int transform;
     long long explicit_rows;
     PlanDev dev;
+    std::vector<float> tprof;   // see SolveJob::tprof
     std::vector<void *> allocs;
     Workspace ws;
 };
@@ -127,6 +128,10 @@ struct SolveJob {
     double alpha, beta;
     const double *other;
     Workspace *ws;   // host-side: scratch owner for the batch (unused on device)
+    // host-side cost profile of the sweep rows (row partition of the persistent
+    // solves): tprof[i] = fraction of modes still in their transient at row i
+    const float *tprof = nullptr;
+    int tlen = 0;
 };
 
 constexpr int kMaxJobs = 8;

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(PCfg<LG>::NT, 1) persist_kernel(const __grid_c
     if (tid == 0) {
         int ns = 0, items = 0;
         for (int v = blockIdx.x; v < pl.V; v += gridDim.x) {
-            const long long lo = pl.total_rows * v / pl.V, hi = pl.total_rows * (v + 1) / pl.V;
+            const long long lo = pl.vstart[v], hi = pl.vstart[v + 1];
             for (int j = 0; j < pl.count; ++j) {
                 const long long r0 = pl.job[j].row0, r1 = r0 + pl.job[j].p.m;
                 if (r0 < hi && r1 > lo && ns < kMaxSegs) {

@@ -34,6 +34,7 @@ constexpr int kMaxPJobs = 8;
 constexpr int kMaxSegs = 48;
 constexpr int kMaxRowsPerBlock = 256;   // keeps block products P_e far from underflow
 constexpr int kCarryVals = 7;           // yhat_e, F_s, P_e, xi_s, Q, Y, X
+constexpr int kMaxV = 512;              // virtual row ranges per launch
 
 struct PList {
     int count;
@@ -47,6 +48,7 @@ struct PList {
     double *bsave;       // [gridDim][bstride][n] beta checkpoints (phase 1 -> phase 3)
     int bstride;
     PJob job[kMaxPJobs];
+    int vstart[kMaxV + 1];   // global first row of virtual range v (cost-balanced)
 };
 
 struct Seg {
@@ -69,7 +71,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
     do {
         asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n"
             " selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
             : "r"(smem_u32(bar)), "r"(parity)
@@ -208,14 +210,64 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
         for (int j = 0; j < pl.count; ++j) total += jobs[j0 + j].p.m;
         pl.total_rows = total;
         long long V = std::max<long long>(grid, (total + kMaxRowsPerBlock - 1) / kMaxRowsPerBlock);
-        V = std::min<long long>(V, total);
+        V = std::min<long long>(std::min<long long>(V, total), kMaxV);
         pl.V = (int)V;
-        auto lo = [&](long long v) { return total * v / V; };
+        // Cost-balanced ranges: a row weighs 1 + tau1 * (fraction of modes in
+        // their transient at that row); a subdomain's first row carries the
+        // extra group/segment set-up (tau0 rows).
+        {
+            static const double tau1 = getenv("FD_TAU1") ? atof(getenv("FD_TAU1")) : 1.2;
+            static const double tau0 = getenv("FD_TAU0") ? atof(getenv("FD_TAU0")) : 4.0;
+            struct JW {
+                long long r0;
+                int m, t;
+                double start;
+                std::vector<double> pre;   // cumulative weight of rows [0, i), i <= t
+            };
+            std::vector<JW> jw(pl.count);
+            double W = 0.0;
+            long long r0 = 0;
+            for (int j = 0; j < pl.count; ++j) {
+                const SolveJob &sj = jobs[j0 + j];
+                JW &q = jw[j];
+                q.r0 = r0;
+                q.m = sj.p.m;
+                q.t = std::min(sj.tlen, q.m);
+                q.start = W;
+                q.pre.assign(q.t + 1, 0.0);
+                for (int i = 0; i < q.t; ++i)
+                    q.pre[i + 1] = q.pre[i] + 1.0 + tau1 * sj.tprof[i] + (i == 0 ? tau0 : 0.0);
+                const double wj = (q.t > 0 ? q.pre[q.t] : tau0) + double(q.m - q.t);
+                W += wj;
+                r0 += q.m;
+            }
+            auto row_at = [&](double target) -> long long {   // first row whose cumulative weight reaches target
+                int j = 0;
+                while (j + 1 < pl.count && jw[j + 1].start <= target) ++j;
+                const JW &q = jw[j];
+                double x = target - q.start;
+                if (q.t > 0 && x <= q.pre[q.t]) {
+                    const int i = int(std::lower_bound(q.pre.begin(), q.pre.end(), x) - q.pre.begin());
+                    return q.r0 + std::min(i, q.m);
+                }
+                x -= (q.t > 0 ? q.pre[q.t] : tau0);
+                return q.r0 + std::min<long long>(q.m, q.t + (long long)std::ceil(x));
+            };
+            pl.vstart[0] = 0;
+            for (long long v = 1; v < V; ++v) {
+                long long r = row_at(W * double(v) / double(V));
+                // snap to a subdomain start within 3 rows: no tiny extra segment
+                for (int j = 1; j < pl.count; ++j)
+                    if (std::llabs(r - jw[j].r0) <= 3) r = jw[j].r0;
+                r = std::max<long long>(r, pl.vstart[v - 1] + 1);             // non-empty ranges
+                r = std::min<long long>(r, total - (V - v));
+                pl.vstart[v] = (int)r;
+            }
+            pl.vstart[V] = (int)total;
+        }
+        auto lo = [&](long long v) { return (long long)pl.vstart[v]; };
         auto range_of = [&](long long r) {   // largest v with lo(v) <= r
-            long long v = r * V / total;
-            while (v + 1 < V && lo(v + 1) <= r) ++v;
-            while (v > 0 && lo(v) > r) --v;
-            return v;
+            return (long long)(std::upper_bound(pl.vstart, pl.vstart + V + 1, (int)r) - pl.vstart) - 1;
         };
         long long row0 = 0;
         int blocks = 0;
@@ -312,15 +364,15 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
                 }
             if (getenv("FD_PHASE_TIMING_CTA")) {
                 // slowest CTAs of phase 1 and of phase 3
-                for (int ph = 0; ph < 2; ++ph) {
+                for (int ph = 0; ph < 3; ++ph) {
                     std::vector<std::pair<double, int>> d;
-                    for (int c = 0; c < grid; ++c)
-                        d.push_back({ph == 0 ? (h[8 * c + 1] - h[8 * c]) * 1e-3 : (h[8 * c + 5] - h[8 * c + 4]) * 1e-3, c});
+                    const int s0 = ph == 0 ? 0 : ph == 1 ? 2 : 4;
+                    for (int c = 0; c < grid; ++c) d.push_back({(h[8 * c + s0 + 1] - h[8 * c + s0]) * 1e-3, c});
                     std::sort(d.rbegin(), d.rend());
-                    fprintf(stderr, "  slowest p%d:", ph ? 3 : 1);
+                    fprintf(stderr, "  slowest p%d:", ph + 1);
                     for (int q = 0; q < 12 && q < (int)d.size(); ++q)
-                        fprintf(stderr, " cta%d[%lld,%lld)=%.1f", d[q].second, total * d[q].second / V,
-                                total * (d[q].second + 1) / V, d[q].first);
+                        fprintf(stderr, " cta%d[%d,%d)=%.1f", d[q].second, pl.vstart[d[q].second],
+                                pl.vstart[d[q].second + 1], d[q].first);
                     fprintf(stderr, "  median %.1f\n", d[d.size() / 2].first);
                 }
             }

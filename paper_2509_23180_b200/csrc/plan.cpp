@@ -383,6 +383,19 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
         }
         d.kt = T.kt;
         d.ktp = T.ktp;
+        {   // transient profile of the table-free modes (row partition cost model)
+            int tl = 0;
+            for (int k = T.kt; k < n; ++k) tl = std::max(tl, T.len[k]);
+            tl = std::min(tl, 512);
+            std::vector<int> cnt(tl + 1, 0);
+            for (int k = T.kt; k < n; ++k) cnt[std::min(T.len[k], tl)]++;
+            p->tprof.assign(tl, 0.0f);
+            int alive = n - T.kt;   // modes with len > i
+            for (int i = 0; i < tl; ++i) {
+                alive -= cnt[i];
+                p->tprof[i] = float(alive) / float(n);
+            }
+        }
         d.lt = T.kt ? upload(p, T.lt) : nullptr;
         d.blk = upload(p, T.blk);
         std::vector<double> zeros(size_t(d.nb) * n, 0.0);

@@ -282,7 +282,12 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
     auto trace = [&](int role, int item, int which) {   // FD_TRACE=<cta>
         if (pl.trace && (role >= 8 ? t == 0 : tid == 0) && blockIdx.x == pl.trace_cta && item < 64 && role < 16) {
             unsigned long long g;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g)::"memory");
+            if (role >= 10 && role < 15) {   // phase 2 points: SM cycles (as ns at 1 GHz)
+                asm volatile("mov.u64 %0, %clock64;" : "=l"(g)::"memory");
+                g = g / 2;   // ~ns at 1.965 GHz, shown relative to the first trace stamp
+            } else {
+                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g)::"memory");
+            }
             pl.trace[(role * 64 + item) * 2 + which] = g;
         }
     };
@@ -291,7 +296,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
     if (tid == 0) {
         int ns = 0, items = 0;
         for (int v = blockIdx.x; v < pl.V; v += gridDim.x) {
-            const long long lo = pl.total_rows * v / pl.V, hi = pl.total_rows * (v + 1) / pl.V;
+            const long long lo = pl.vstart[v], hi = pl.vstart[v + 1];
             for (int j = 0; j < pl.count; ++j) {
                 const long long r0 = pl.job[j].row0, r1 = r0 + pl.job[j].p.m;
                 if (r0 < hi && r1 > lo && ns < kMaxSegs) {
@@ -389,7 +394,6 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
             const Seg sg = segs[si];
             const PJob &J = pl.job[sg.job];
             const PlanDev &p = J.p;
-            const double off = p.off;
             const int so = stg_off(J.in, g0, n);
             const int rp = min(2, rows - 2 * pr);
             trace(0, it, 0);
@@ -529,74 +533,114 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
                 int si2, g2, rows2;
                 item_of(it + 1, si2, g2, rows2, false);
                 const PJob &J2 = pl.job[segs[si2].job];
+                trace(6, it, 0);
                 if (t == 0) tail = issue_pair(J2.in, g2, rows2, J2.p.m);
+                trace(6, it, 1);
                 if (tid == 0 && J2.p.lt) issue_lts(J2.p, g2, rows2);
+                trace(7, it, 0);
             }
         }
     }
     stamp(1);
     grid.sync();
     stamp(2);
+    trace(11, 0, 0);
 
     // ===================== phase 2: block carries =====================================
-    // One CTA per (job, 32 modes): every block's scalars staged through shared
-    // memory (inside the pair regions; the tables behind them stay intact), warp 0
-    // (lane = mode) runs both short recurrences, then Y and X go back.
+    // Per (job, mode) chain over the job's blocks b:
+    //   Y_b = yhat_b + P_b Y_{b-1}                  (forward)
+    //   X_b = F_b + Y_{b-1} xi_b + Q_b X_{b+1}      (backward)
+    // Items of (job, W modes), W ~ chains / grid so every CTA takes about one: the
+    // item's block scalars are staged in shared memory (coalesced over modes), then
+    // every warp evaluates chains as inclusive scans of the composed affine maps
+    // y -> A y + B over 32 blocks at a time (lane = block), and Y, X go back.
     {
-        constexpr int CHB = int(C::OFF_TW / (7 * 32 * 8)) < 96 ? int(C::OFF_TW / (7 * 32 * 8)) : 96;
-        double *sv = reinterpret_cast<double *>(smem_raw);   // [CHB][7][32]
-        const int chunks = (n + 31) / 32;
+        const int warp = tid >> 5;
+        constexpr int NW = NT / 32;
         const size_t bs = size_t(kCarryVals) * n;
-        for (int item = blockIdx.x; item < pl.count * chunks; item += gridDim.x) {
-            const PJob &J = pl.job[item / chunks];
-            const int k0 = (item % chunks) * 32;
-            double *cb = pl.carry + size_t(J.blk_base) * bs + k0;
-            const int nb = J.nblk;
-            const bool lane_ok = (tid < 32) && (k0 + lane < n);
-            double prev = 0.0, next = 0.0;
-            if (nb <= CHB) {
-                for (int idx = tid; idx < nb * 160; idx += NT) {   // 5 values x 32 modes per block
-                    const int b = idx / 160, v = (idx >> 5) % 5, kk = idx & 31;
-                    sv[(b * 7 + v) * 32 + kk] = (k0 + kk < n) ? __ldcg(cb + b * bs + v * n + kk) : 0.0;
-                }
-                __syncthreads();
-                if (lane_ok) {
-                    for (int b = 0; b < nb; ++b) {
-                        const double *q = sv + b * 7 * 32 + lane;
-                        const double y = (b == 0) ? q[0] : fma(q[2 * 32], prev, q[0]);
-                        sv[(b * 7 + 5) * 32 + lane] = y;
-                        prev = y;
-                    }
-                    for (int b = nb - 1; b >= 0; --b) {
-                        const double *q = sv + b * 7 * 32 + lane;
-                        double x = q[1 * 32];
-                        if (b > 0) x = fma(sv[((b - 1) * 7 + 5) * 32 + lane], q[3 * 32], x);
-                        if (b < nb - 1) x = fma(q[4 * 32], next, x);
-                        sv[(b * 7 + 6) * 32 + lane] = x;
-                        next = x;
-                    }
-                }
-                __syncthreads();
-                for (int idx = tid; idx < nb * 64; idx += NT) {
-                    const int b = idx >> 6, v = 5 + ((idx >> 5) & 1), kk = idx & 31;
-                    if (k0 + kk < n) __stcg(cb + b * bs + v * n + kk, sv[(b * 7 + v) * 32 + kk]);
-                }
-                __syncthreads();
-            } else if (lane_ok) {
-                for (int b = 0; b < nb; ++b) {
-                    const double ye = __ldcg(cb + b * bs + lane), pe = __ldcg(cb + b * bs + 2 * n + lane);
-                    const double y = (b == 0) ? ye : fma(pe, prev, ye);
-                    __stcg(cb + b * bs + 5 * n + lane, y);
-                    prev = y;
-                }
-                for (int b = nb - 1; b >= 0; --b) {
-                    double x = __ldcg(cb + b * bs + 1 * n + lane);
-                    if (b > 0) x = fma(__ldcg(cb + (b - 1) * bs + 5 * n + lane), __ldcg(cb + b * bs + 3 * n + lane), x);
-                    if (b < nb - 1) x = fma(__ldcg(cb + b * bs + 4 * n + lane), next, x);
-                    __stcg(cb + b * bs + 6 * n + lane, x);
-                    next = x;
+        int nbmax = 1;
+        for (int j = 0; j < pl.count; ++j) nbmax = max(nbmax, pl.job[j].nblk);
+        const int cap = int(C::OFF_TW / (7 * 8)) / nbmax;   // modes per item that fit the regions
+        int W = (pl.count * n + gridDim.x - 1) / gridDim.x;
+        W = max(1, min(min(W, 64), cap - 1));
+        const int WP = W | 1;                               // odd stride: lane-per-block reads conflict-free
+        const int per_job = (n + W - 1) / W;
+        double *sv = reinterpret_cast<double *>(smem_raw);   // [nb][7][WP]
+        auto scan = [&](double &A, double &B) {   // lane l ends with f_l o ... o f_0
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double Ao = __shfl_up_sync(0xffffffffu, A, o), Bo = __shfl_up_sync(0xffffffffu, B, o);
+                if (lane >= o) {
+                    B = fma(A, Bo, B);
+                    A *= Ao;
                 }
             }
+        };
+            for (int item = blockIdx.x; item < pl.count * per_job; item += gridDim.x) {
+            const PJob &J = pl.job[item / per_job];
+            const int k0 = (item % per_job) * W, w = min(W, n - k0);
+            double *cb = pl.carry + size_t(J.blk_base) * bs + k0;
+            const int nb = J.nblk;
+            // async copies global -> shared (no register round trip): every load of
+            // the item in flight at once from a small loop
+#pragma unroll 1
+            for (int bv = warp; bv < nb * 5; bv += NW) {
+                const int b = bv / 5, v = bv - 5 * b;
+                const double *src = cb + b * bs + v * n;
+                double *dst = sv + (b * 7 + v) * WP;
+#pragma unroll 1
+                for (int m = lane; m < w; m += 32)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + m)), "l"(src + m)
+                                 : "memory");
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            trace(12, item / gridDim.x, 0);
+            __syncthreads();
+            trace(12, item / gridDim.x, 1);
+#pragma unroll 1
+            for (int m = warp; m < w; m += NW) {
+                double carry = 0.0;
+#pragma unroll 1
+                for (int b0 = 0; b0 < nb; b0 += 32) {
+                    const int b = b0 + lane;
+                    double A = 1.0, B = 0.0;
+                    if (b < nb) {
+                        B = sv[(b * 7 + 0) * WP + m];
+                        A = (b == 0) ? 0.0 : sv[(b * 7 + 2) * WP + m];
+                    }
+                    scan(A, B);
+                    const double Y = fma(A, carry, B);
+                    if (b < nb) sv[(b * 7 + 5) * WP + m] = Y;
+                    carry = __shfl_sync(0xffffffffu, Y, 31);
+                }
+                __syncwarp();
+                carry = 0.0;
+#pragma unroll 1
+                for (int b1 = nb; b1 > 0; b1 -= 32) {
+                    const int b = b1 - 1 - lane;   // lane 0 = highest block of the chunk
+                    double A = 1.0, B = 0.0;
+                    if (b >= 0) {
+                        B = sv[(b * 7 + 1) * WP + m];
+                        if (b > 0) B = fma(sv[((b - 1) * 7 + 5) * WP + m], sv[(b * 7 + 3) * WP + m], B);
+                        A = (b < nb - 1) ? sv[(b * 7 + 4) * WP + m] : 0.0;
+                    }
+                    scan(A, B);
+                    const double X = fma(A, carry, B);
+                    if (b >= 0) sv[(b * 7 + 6) * WP + m] = X;
+                    carry = __shfl_sync(0xffffffffu, X, 31);
+                }
+            }
+            trace(13, item / gridDim.x, 0);
+            __syncthreads();
+            trace(13, item / gridDim.x, 1);
+#pragma unroll 1
+            for (int bv = warp; bv < nb * 2; bv += NW) {
+                const int b = bv >> 1, v = 5 + (bv & 1);
+#pragma unroll 1
+                for (int m = lane; m < w; m += 32) __stcg(cb + b * bs + v * n + m, sv[(b * 7 + v) * WP + m]);
+            }
+            __syncthreads();
+            trace(14, item / gridDim.x, 0);
         }
     }
     stamp(3);
@@ -778,6 +822,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
                 trace(4, it, 1);
             }
             if (more && t == 0) tail = issue_pair(pl.job[segs[si2].job].out, g2, rows2, pl.job[segs[si2].job].p.m);
+            __syncthreads();   // idle pairs wait here, not on the mbarriers
             trace(3, it, 1);
         }
     }
