@@ -45,6 +45,7 @@ struct PList {
     unsigned long long *tstamp;   // optional [gridDim][8] phase timestamps (FD_PHASE_TIMING)
     unsigned long long *trace;    // optional per-item timeline of one CTA (FD_TRACE=cta)
     int trace_cta;
+    int dbg;             // FD_DBG experiment bits (timing studies only; 0 in production)
     double *bsave;       // [gridDim][bstride][n] beta checkpoints (phase 1 -> phase 3)
     int bstride;
     PJob job[kMaxPJobs];
@@ -320,21 +321,31 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
         static const bool tracing = getenv("FD_TRACE") != nullptr;
         unsigned long long *tr = nullptr;
         if (tracing) {
-            FD_CUDA(cudaMallocAsync(&tr, sizeof(unsigned long long) * 16 * 64 * 2, s));
-            FD_CUDA(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * 16 * 64 * 2, s));
+            FD_CUDA(cudaMallocAsync(&tr, sizeof(unsigned long long) * (16 * 64 * 2 + 64), s));
+            FD_CUDA(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * (16 * 64 * 2 + 64), s));
         }
         pl.trace = tr;
         pl.trace_cta = tracing ? atoi(getenv("FD_TRACE")) : 0;
+        static const int dbg = getenv("FD_DBG") ? atoi(getenv("FD_DBG")) : 0;
+        pl.dbg = dbg;
         void *args[] = {(void *)&pl};
         FD_CUDA(cudaLaunchCooperativeKernel(K::fn(), dim3(grid), dim3(C::NT), args, C::SMEM, s));
         if (tracing) {
-            std::vector<unsigned long long> h(16 * 64 * 2);
+            std::vector<unsigned long long> h(16 * 64 * 2 + 64);
             FD_CUDA(cudaMemcpyAsync(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost, s));
             FD_CUDA(cudaStreamSynchronize(s));
             FD_CUDA(cudaFreeAsync(tr, s));
             unsigned long long t0 = ~0ull;
             for (auto v : h)
                 if (v) t0 = std::min(t0, v);
+            if (pl.dbg & 4) {   // per-pass cycle stamps of pair 0 (rsolve)
+                for (int it = 0; it < 4; ++it) {
+                    const long long *c = reinterpret_cast<const long long *>(h.data()) + 2048 + it * 8;
+                    if (!c[0]) continue;
+                    fprintf(stderr, "[fft cycles it %d] load %lld first %lld mid %lld last %lld post %lld\n", it,
+                            c[1] - c[0], c[2] - c[1], c[3] - c[2], c[4] - c[3], c[5] - c[4]);
+                }
+            }
             for (int role = 0; role < 16; ++role) {
                 bool any = false;
                 for (int it = 0; it < 64; ++it)

@@ -201,14 +201,28 @@ struct RFft {
     // full transform of the staged rows A (, B) -> padded X rows in the same region
     __device__ __forceinline__ static void run(double2 *buf, const double *A, const double *B, const double *al,
                                             double h2, const double2 *m16, const double2 *la, double *scr, int t,
-                                            int pr, int lane, double *XA, double *XB) {
+                                            int pr, int lane, double *XA, double *XB,
+                                            long long *dbgp = nullptr) {
         double2 v[16];
+        auto ck = [&](int s) {   // FD_DBG & 4: per-pass cycle stamps of pair 0 (timing studies)
+            if (dbgp && t == 0 && pr == 0) {
+                long long c;
+                asm volatile("mov.u64 %0, %clock64;" : "=l"(c)::"memory");
+                dbgp[s] = c;
+            }
+        };
+        ck(0);
         load(v, A, B, al, h2, t);
+        ck(1);
         rsync<T>(pr);   // the staged rows alias the exchange buffer
         first(buf, v, t, pr);
+        ck(2);
         if constexpr (C::NMID > 0) mid(buf, m16, t, pr);
+        ck(3);
         last(buf, la, t, pr);
+        ck(4);
         post(buf, scr, t, pr, lane, XA, XB);
+        ck(5);
     }
 };
 
@@ -282,12 +296,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
     auto trace = [&](int role, int item, int which) {   // FD_TRACE=<cta>
         if (pl.trace && (role >= 8 ? t == 0 : tid == 0) && blockIdx.x == pl.trace_cta && item < 64 && role < 16) {
             unsigned long long g;
-            if (role >= 10 && role < 15) {   // phase 2 points: SM cycles (as ns at 1 GHz)
-                asm volatile("mov.u64 %0, %clock64;" : "=l"(g)::"memory");
-                g = g / 2;   // ~ns at 1.965 GHz, shown relative to the first trace stamp
-            } else {
-                asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g)::"memory");
-            }
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g)::"memory");
             pl.trace[(role * 64 + item) * 2 + which] = g;
         }
     };
@@ -405,7 +414,9 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
                 }
                 double *base = regd(pr) + so;
                 F::run(regc(pr), base, rp > 1 ? base + n : nullptr, al, 0.5 * p.scale, m16, la, scr, t, pr, lane,
-                       regd(pr), rp > 1 ? regd(pr) + XR : nullptr);
+                       regd(pr), rp > 1 ? regd(pr) + XR : nullptr,
+                       (pl.trace && (pl.dbg & 4) && blockIdx.x == pl.trace_cta && it < 4)
+                           ? reinterpret_cast<long long *>(pl.trace) + 2048 + it * 8 : nullptr);
             }
             ppar ^= group_mask(rows);
             if (p.lt) {
@@ -418,12 +429,18 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
             const bool first = (g0 == sg.s), last = (g0 + rows - 1 == sg.e);
             double *outg = J.out + size_t(g0) * n;
             const int mlast = p.m - 1;
+            // two parts (rows [0, half), [half, rows)): the first half's regions are
+            // refilled with the next group while the second half is swept
+            const int half = (rows > 8) ? ((rows / 2 + 1) & ~1) : rows;
+#pragma unroll 1
+            for (int part = 0; part < 2; ++part) {
+            const int ra = part ? half : 0, rb = part ? rows : half;
 #pragma unroll
             for (int u = 0; u < MPT; ++u) {
                 const int k = tid + u * NT;
-                if (k >= n) continue;
+                if (k >= n || ra >= rb) continue;
                 double y = ys[u], w = pis[u], f = fss[u], s2 = s2s[u];
-                if (first) {
+                if (first && part == 0) {
                     ModeRec c;
                     c.load(p, k);
                     cl[u] = c.l_inf;
@@ -444,10 +461,10 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
                     const double W = w * ib;
                     f = fma(y, W, f);
                     s2 = fma(w, W, s2);
-                    og[rr * n] = y;
+                    if (!(pl.dbg & 2)) og[rr * n] = y;
                 };
-                int rr = 0;
-                if (first) {   // block start: y = r, pi = 1, P_i = -l_s pi_i
+                int rr = ra;
+                if (first && ra == 0) {   // block start: y = r, pi = 1, P_i = -l_s pi_i
                     double l0 = l_inf, ib0 = (g0 == mlast) ? ibm : ib_inf;
                     if (k < p.kt) {
                         l0 = lts[k];
@@ -473,41 +490,41 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
                     // slowly converging low mode: reference factors from the table
                     const double *tb = lts + k;
 #pragma unroll 4
-                    for (; rr < rows; ++rr) step(rr, tb[rr * 3 * p.ktp], tb[rr * 3 * p.ktp + p.ktp]);
-                } else if (g0 + rr < len && g0 + rows <= p.ecap) {
+                    for (; rr < rb; ++rr) step(rr, tb[rr * 3 * p.ktp], tb[rr * 3 * p.ktp + p.ktp]);
+                } else if (g0 + rr < len && g0 + rb <= p.ecap) {
                     // transient rows: the reference factors (rectsolver.py:72-73) from
                     // the row-major tables, 8 rows of loads ahead of their sweep
 #pragma unroll 1
-                    for (; rr < rows; rr += 8) {
+                    for (; rr < rb; rr += 8) {
                         double lv[8], ibv[8];
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             const int i = g0 + rr + q;
-                            const bool tr = (rr + q < rows) && (i < len);
+                            const bool tr = (rr + q < rb) && (i < len);
                             lv[q] = tr ? __ldg(p.dl + size_t(i) * n + k) : l_inf;
                             ibv[q] = tr ? __ldg(p.dib + size_t(i) * n + k) : ((i == mlast) ? ibm : ib_inf);
                         }
 #pragma unroll
                         for (int q = 0; q < 8; ++q)
-                            if (rr + q < rows) step(rr + q, lv[q], ibv[q]);
+                            if (rr + q < rb) step(rr + q, lv[q], ibv[q]);
                     }
                 } else if (g0 + rr < len) {
 #pragma unroll 1
-                    for (; rr < rows; ++rr) {   // beyond the tables (capped long-transient table)
+                    for (; rr < rb; ++rr) {   // beyond the tables (capped long-transient table)
                         double l, ib, bm1;
                         factors_slow(p, k, g0 + rr, len, l_inf, ib_inf, ibm, 0.0, &l, &ib, &bm1);
                         step(rr, l, ib);
                     }
                 } else {
 #pragma unroll 4
-                    for (; rr < rows; ++rr) step(rr, l_inf, (g0 + rr == mlast) ? ibm : ib_inf);
+                    for (; rr < rb; ++rr) step(rr, l_inf, (g0 + rr == mlast) ? ibm : ib_inf);
                 }
                 const double cc = ccs[u];
                 ys[u] = y;
                 pis[u] = w;
                 fss[u] = f;
                 s2s[u] = s2;
-                if (last) {
+                if (last && rb == rows) {
                     double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
                     const int e = sg.e;
                     // Q = pi_e * (-l_{e+1}),  l_{e+1} = delta / beta_e
@@ -527,18 +544,16 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
                     __stcg(cb + 4 * n, Q);
                 }
             }
-            __syncthreads();   // regions and the table slice consumed
-            trace(1, it, 1);
+            __syncthreads();   // this part's rows consumed (after part 1: the table slice too)
             if (it + 1 < nitems) {
                 int si2, g2, rows2;
                 item_of(it + 1, si2, g2, rows2, false);
                 const PJob &J2 = pl.job[segs[si2].job];
-                trace(6, it, 0);
-                if (t == 0) tail = issue_pair(J2.in, g2, rows2, J2.p.m);
-                trace(6, it, 1);
-                if (tid == 0 && J2.p.lt) issue_lts(J2.p, g2, rows2);
-                trace(7, it, 0);
+                if (t == 0 && (part ? 2 * pr >= half : 2 * pr < half)) tail = issue_pair(J2.in, g2, rows2, J2.p.m);
+                if (part == 1 && tid == 0 && J2.p.lt) issue_lts(J2.p, g2, rows2);
             }
+            }   // parts
+            trace(1, it, 1);
         }
     }
     stamp(1);
@@ -561,7 +576,8 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
         int nbmax = 1;
         for (int j = 0; j < pl.count; ++j) nbmax = max(nbmax, pl.job[j].nblk);
         const int cap = int(C::OFF_TW / (7 * 8)) / nbmax;   // modes per item that fit the regions
-        int W = (pl.count * n + gridDim.x - 1) / gridDim.x;
+        const int cpj = max(1, int(gridDim.x) / pl.count);   // CTAs per job
+        int W = (n + cpj - 1) / cpj;
         W = max(1, min(min(W, 64), cap - 1));
         const int WP = W | 1;                               // odd stride: lane-per-block reads conflict-free
         const int per_job = (n + W - 1) / W;
@@ -804,18 +820,25 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
                        XA, rp > 1 ? XB : nullptr);
                 rsync<T>(pr);
                 trace(8 + pr, it, 1);
+                // epilogue out = alpha x + beta other over the pair's rows (adjacent in
+                // global memory), 8 shared-memory reads in flight per thread
                 const double al_ = J.alpha, be_ = J.beta;
+                double *o0 = J.out + size_t(g0 + 2 * pr) * n;
+                const double *q0p = J.other ? J.other + size_t(g0 + 2 * pr) * n : nullptr;
+                const int tot = rp * n;
 #pragma unroll 1
-                for (int h = 0; h < rp; ++h) {
-                    const double *X = h ? XB : XA;
-                    double *o = J.out + size_t(g0 + 2 * pr + h) * n;
-                    if (J.other) {
-                        const double *qo = J.other + size_t(g0 + 2 * pr + h) * n;
-                        for (int k = t; k < n; k += T) o[k] = fma(be_, __ldg(qo + k), al_ * X[xi(k)]);
-                    } else if (al_ == 1.0) {
-                        for (int k = t; k < n; k += T) o[k] = X[xi(k)];
-                    } else {
-                        for (int k = t; k < n; k += T) o[k] = al_ * X[xi(k)];
+                for (int q0 = t; q0 < tot; q0 += 8 * T) {
+                    double v[8], w8[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int q = q0 + u * T, h = q >= n;
+                        v[u] = (q < tot) ? XA[h * XR + xi(q - h * n)] : 0.0;
+                        w8[u] = (q < tot && q0p) ? __ldg(q0p + q) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int q = q0 + u * T;
+                        if (q < tot && !(pl.dbg & 1)) o0[q] = q0p ? fma(be_, w8[u], al_ * v[u]) : al_ * v[u];
                     }
                 }
                 rsync<T>(pr);   // region free
