@@ -40,6 +40,17 @@ METRIC = "grid points solved/sec (fp64, 1e-10 res); precond-apply HBM GB/s vs pe
 WORKLOAD = "c1: batched precond apply, 5 x 1023^2 fp64 Dirichlet, kappa=0, DST-I->Thomas->DST-I"
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_rsolve_c1_ncu_full.json")
+    try:
+        d = json.load(open(path))
+        mb = lambda s: float(s.split()[0]) * (1e6 if "Mbyte" in s else 1e3 if "Kbyte" in s else 1e9 if "Gbyte" in s else 1.0)
+        return mb(d["dram__bytes_read.sum"]) + mb(d["dram__bytes_write.sum"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -282,11 +293,11 @@ def run_gpu(args, world, rank, local):
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak,
                              # dram__bytes_read.sum + dram__bytes_write.sum per launch from
-                             # profiles/r01_persist_c1_ncu_full.json (ncu --set full, cold L2)
-                             "traffic": 63.0e6,
+                             # the committed ncu --set full capture (cold L2)
+                             "traffic": ncu_traffic(),
                              "peak_kind": peak_kind,
                              "algorithmic_bytes_per_point": B_ALG,
-                             "kernel": "persist_kernel<11> (fused batched apply, 1 launch)"},
+                             "kernel": "rsolve_kernel<10> (fused batched apply, 1 launch)"},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "grid_points/s",
                         "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
