@@ -116,6 +116,33 @@ class TestRectSolve:
         assert torch.equal(f, ref)
 
 
+class TestPersistentGeometry:
+    """The fused persistent solve's row partition: every FFT length, single and
+    odd rows (a pair with one row), multi-group carry blocks, subdomain starts
+    inside a CTA range, the misaligned array end (TMA tail), and batches of
+    rectangles with different m (against the oracle, 1e-12)."""
+
+    @pytest.mark.parametrize("n", [255, 511, 1023, 2047, 4095])
+    @pytest.mark.parametrize("m", [1, 3, 17, 149, 1185])
+    def test_rows(self, n, m, rng):
+        if n == 4095 and m == 1185:
+            pytest.skip("covered by the full-size properties")
+        sub = make((m, n, 1.0 / n, 1.0 / n, -10.0, "DDDD", ()))
+        f = rng.uniform(-1, 1, m * n)
+        p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f)
+        assert rel(p.values, O.solve(O.plan(sub), f)) < 1e-12
+
+    @pytest.mark.parametrize("n", [511, 1023, 2047])
+    def test_mixed_batch(self, n, rng):
+        ms = [7, 300, 1, 64, 513]
+        subs = [make((m, n, 1.0 / n, 1.0 / n, k, "DDDD", ("west",) if i % 2 else ()), sid=i)
+                for i, (m, k) in enumerate(zip(ms, [0.0, -10.0, 3.0, -100.0, 0.0]))]
+        fs = [rng.uniform(-1, 1, s.size) for s in subs]
+        outs = rectsolver.solve_rect_batched([rectsolver.plan_rect(s) for s in subs], fs)
+        for s, f, o in zip(subs, fs, outs):
+            assert rel(o.cpu().numpy(), O.solve(O.plan(s), f)) < 1e-12
+
+
 class TestSchur:
     @pytest.mark.parametrize("N", [4, 8, 15, 31])
     @pytest.mark.parametrize("kappa", [0.0, -100.0])
