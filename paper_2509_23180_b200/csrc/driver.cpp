@@ -5,12 +5,14 @@
 // like the reference's numpy scalars; every vector-sized operation runs in a
 // kernel on the caller's stream.
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
 #include <chrono>
 #include <map>
 #include <mutex>
+#include <set>
 #include <sstream>
 
 #include "fd_internal.h"
@@ -22,6 +24,29 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
 void plan_destroy(Plan *p);
 void factor_tables_host(int m, int n, double dx, double dy, double kappa, double mod_w,
                         double mod_e, double *beta, double *lower);
+
+void *dmalloc(size_t bytes) {
+    static std::mutex mu;
+    static std::set<int> configured;
+    int dev = 0;
+    FD_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (configured.insert(dev).second) {
+            cudaMemPool_t pool;
+            FD_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+            uint64_t keep = UINT64_MAX;
+            FD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        }
+    }
+    void *p = nullptr;
+    FD_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), 0));
+    FD_CUDA(cudaStreamSynchronize(0));
+    return p;
+}
+void dfree(void *p) {
+    if (p) cudaFreeAsync(p, 0);
+}
 
 static thread_local std::string g_last_error;
 void set_error(const std::string &msg) { g_last_error = msg; }
@@ -114,6 +139,9 @@ struct fd_schur_s {
     int vcap = 0;
     double *w = nullptr, *r = nullptr, *ydev = nullptr;
     fd::Scratch sc{};
+    // low-synchronisation Arnoldi: Gram rows, partials, results (device) + pinned mirror
+    fd::ArnWork arn{};
+    double *arn_out = nullptr, *arn_host = nullptr;
     std::vector<void *> allocs;
 };
 
@@ -121,7 +149,7 @@ namespace fd {
 
 static void *dalloc(fd_schur_s *op, size_t bytes) {
     void *d = nullptr;
-    FD_CUDA(cudaMalloc(&d, bytes));
+    d = dmalloc(bytes);
     op->allocs.push_back(d);
     return d;
 }
@@ -191,11 +219,46 @@ static void unprecond_apply(fd_schur_s *op, const double *p, double *out, cudaSt
     launch_axpby(N, 1.0, op->tmp2, -1.0, out, out, s);
 }
 
+static void ensure_arnoldi(fd_schur_s *op) {
+    if (op->arn.partials) return;
+    op->arn.partials = (double *)dalloc(op, sizeof(double) * kArnPartials);
+    op->arn.counter = (unsigned int *)dalloc(op, sizeof(unsigned int));
+    FD_CUDA(cudaMemset(op->arn.counter, 0, sizeof(unsigned int)));
+    op->arn.G = (double *)dalloc(op, sizeof(double) * kMaxArnoldi * kMaxArnoldi);
+    op->arn_out = (double *)dalloc(op, sizeof(double) * (2 * kMaxArnoldi + 4));
+    FD_CUDA(cudaMallocHost(&op->arn_host, sizeof(double) * (2 * kMaxArnoldi + 4)));
+}
+
+// Arnoldi step on the operator's basis with the low-synchronisation MGS of
+// ops.cu (two passes over V instead of k + 1): h[0..k] projections, h[k+1] =
+// ||w|| after, *w_norm = ||w|| before; V[k+1] = w / h[k+1] is formed on the
+// device (unused by the caller on breakdown, like the reference).
+static void arnoldi_step_ls(fd_schur_s *op, long long N, int k, double *h, double *w_norm,
+                            cudaStream_t s) {
+    ArnWork a = op->arn;
+    a.out = op->arn_out;
+    launch_arnoldi_dots(N, k, op->V, op->w, a, kMaxArnoldi, s);
+    ArnWork b = op->arn;
+    b.out = op->arn_out + kMaxArnoldi + 2;
+    launch_arnoldi_update(N, k, op->V, op->w, a.out, b, s);
+    launch_scale_sqrt(N, op->w, b.out, op->V + (long long)(k + 1) * N, s);
+    FD_CUDA(cudaMemcpyAsync(op->arn_host, op->arn_out, sizeof(double) * (kMaxArnoldi + 3),
+                            cudaMemcpyDeviceToHost, s));
+    FD_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i <= k; ++i) h[i] = op->arn_host[i];
+    *w_norm = sqrt(op->arn_host[k + 1]);
+    h[k + 1] = sqrt(op->arn_host[kMaxArnoldi + 2]);
+}
+
 static void ensure_basis(fd_schur_s *op, int m) {
+    ensure_arnoldi(op);
     if (op->vcap >= m + 1) return;
-    if (op->V) cudaFree(op->V);
+    if (op->V) {
+        FD_CUDA(cudaDeviceSynchronize());
+        dfree(op->V);
+    }
     const long long N = (long long)op->center->m * op->center->n;
-    FD_CUDA(cudaMalloc(&op->V, sizeof(double) * N * (m + 1)));
+    op->V = (double *)dmalloc(sizeof(double) * N * (m + 1));
     op->vcap = m + 1;
     if (op->sc.cap < m + 8) {
         if (op->sc.cap) free_scratch(op->sc);
@@ -215,6 +278,8 @@ static int gmres_precond(fd_schur_s *op, const double *rhs, double *x, int x_is_
     const long long N = (long long)op->center->m * op->center->n;
     const int m = (int)std::min<long long>(mcfg, N);
     ensure_basis(op, m);
+    static const bool force_mgs = getenv("FD_MGS") != nullptr;   // A/B switch: classic k+1-pass MGS
+    const bool lowsync = m + 1 <= kMaxArnoldi && !force_mgs;
     Scratch &sc = op->sc;
     double *r = op->r, *w = op->w;
     if (x_is_zero) {
@@ -254,7 +319,10 @@ static int gmres_precond(fd_schur_s *op, const double *rhs, double *x, int x_is_
         for (int k = 0; k < m; ++k) {
             precond_apply(op, op->V + (long long)k * N, w, s);
             double w_norm = 0.0;
-            arnoldi_step(N, k, op->V, w, hcol.data(), &w_norm, sc, s);
+            if (lowsync)
+                arnoldi_step_ls(op, N, k, hcol.data(), &w_norm, s);
+            else
+                arnoldi_step(N, k, op->V, w, hcol.data(), &w_norm, sc, s);
             for (int i = 0; i <= k; ++i) Hat(i, k) = hcol[i];
             const double h_next = hcol[k + 1];
             Hat(k + 1, k) = h_next;
@@ -277,9 +345,11 @@ static int gmres_precond(fd_schur_s *op, const double *rhs, double *x, int x_is_
                 breakdown = true;
                 break;
             }
-            sc.hval[0] = h_next;
-            FD_CUDA(cudaMemcpyAsync(sc.dval, sc.hval, sizeof(double), cudaMemcpyHostToDevice, s));
-            launch_scale(N, w, sc.dval, op->V + (long long)(k + 1) * N, s);
+            if (!lowsync) {
+                sc.hval[0] = h_next;
+                FD_CUDA(cudaMemcpyAsync(sc.dval, sc.hval, sizeof(double), cudaMemcpyHostToDevice, s));
+                launch_scale(N, w, sc.dval, op->V + (long long)(k + 1) * N, s);
+            }
             if (hist.back() <= tol) break;
         }
         for (int i = k_used - 1; i >= 0; --i) {   // krylov.py:138-140
@@ -455,7 +525,8 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, doub
         op->ydev = (double *)dalloc(op, sizeof(double) * 4096);
         op->sc = make_scratch(128);
     } catch (...) {
-        for (void *a : op->allocs) cudaFree(a);
+        cudaDeviceSynchronize();
+        for (void *a : op->allocs) dfree(a);
         delete op;
         throw;
     }
@@ -467,9 +538,11 @@ int fd_schur_destroy(fd_schur op) {
     FD_API_BEGIN
     if (op) {
         cudaSetDevice(op->device);
-        for (void *a : op->allocs) cudaFree(a);
-        if (op->V) cudaFree(op->V);
+        cudaDeviceSynchronize();
+        for (void *a : op->allocs) dfree(a);
+        if (op->V) dfree(op->V);
         if (op->sc.cap) free_scratch(op->sc);
+        if (op->arn_host) cudaFreeHost(op->arn_host);
         delete op;
     }
     FD_API_END

@@ -426,15 +426,20 @@ struct Fft2 {
 };
 
 // ---------------------------------------------------------------------------
-// Dense DST-I (any n <= kDenseMax): out_k = scale * sum_j S[j][k] in_j,
-// S[j][k] = sin(pi (j+1)(k+1)/(n+1)) from a host-built table.
+// Dense DST-I (any n <= kDenseMax): out_k = scale * sum_j sin(pi (j+1)(k+1)/N) in_j,
+// N = n + 1.  The sine is periodic in (j+1)(k+1) mod 2N, so a 2N-entry table
+// (host-built, exact argument reduction) staged in shared memory serves every
+// (j, k); each thread walks its index by k + 1 per j.  MPT modes per thread
+// (n <= 128 MPT), G rows per group share every table load.
 constexpr int kDenseMax = 1024;
-struct DenseDst {
+template <int MPT_>
+struct DenseDstT {
     static constexpr int NT = 128;
-    static constexpr int G = 4;
+    static constexpr int G = 8;
     static constexpr int MINB = 2;
-    static constexpr int MPT = kDenseMax / NT;
-    static constexpr size_t SMEM = size_t(G) * kDenseMax * sizeof(double);
+    static constexpr int MPT = MPT_;
+    static constexpr int NMAX = NT * MPT_;
+    static constexpr size_t SMEM = size_t(G) * NMAX * sizeof(double) + size_t(2) * (NMAX + 1) * sizeof(double);
 };
 
 // ---------------------------------------------------------------------------

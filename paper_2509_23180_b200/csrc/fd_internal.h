@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -70,14 +71,21 @@ struct PlanDev {
 constexpr int kRsThreads = 512;
 constexpr int kRsMinN = 256, kRsMaxN = 2048;
 constexpr size_t kRsSmem = 227 * 1024 - 2048;
-constexpr int rs_pairs(int N) { return kRsThreads / (N / 16); }
+#ifndef FD_RS_SMALL_N
+#define FD_RS_SMALL_N 0
+#endif
+// N <= FD_RS_SMALL_N: two CTAs of 256 threads per SM (one CTA's barriers and
+// copy waits overlap the other's transforms); larger N: one CTA of 512.
+constexpr int rs_threads(int N) { return N <= FD_RS_SMALL_N ? 256 : kRsThreads; }
+constexpr size_t rs_smem(int N) { return rs_threads(N) == 256 ? size_t(110) * 1024 : kRsSmem; }
+constexpr int rs_pairs(int N) { return rs_threads(N) / (N / 16); }
 constexpr int rs_rows_per_group(int N) { return 2 * rs_pairs(N); }
 constexpr size_t rs_fixed_smem(int N) {
     return size_t(rs_pairs(N)) * size_t(N + N / 16) * 16 + 272 * 16 + size_t(N) * 8 +
            size_t(rs_pairs(N)) * 16 * 8;
 }
 constexpr int rs_kt_cap(int N) {
-    return int((kRsSmem - rs_fixed_smem(N)) / (24 * size_t(rs_rows_per_group(N)))) & ~1;
+    return int((rs_smem(N) - rs_fixed_smem(N)) / (24 * size_t(rs_rows_per_group(N)))) & ~1;
 }
 inline bool rs_supported(int n) {
     const int N = n + 1;
@@ -86,23 +94,34 @@ inline bool rs_supported(int n) {
 
 enum Transform { kDense = 0, kFFT = 1 };
 
+// Device allocations of plans, operators and the Krylov basis come from the
+// device's stream-ordered pool with an unbounded release threshold, so the
+// gigabytes a c3/c4 solve allocates are recycled by the next solve instead of
+// going back to the driver (cudaMalloc + cudaFree of the 6.8 GB basis cost
+// ~0.9 s per solve).  dfree() callers synchronise the device first (destroy
+// paths), like cudaFree would.
+void *dmalloc(size_t bytes);
+void dfree(void *p);
+
 // grow-only device scratch (block carries of the persistent solve)
 struct Workspace {
     double *ptr = nullptr;
     size_t cap = 0;
     double *get(size_t count) {
         if (count > cap) {
-            if (ptr) cudaFree(ptr);
+            if (ptr) {
+                cudaDeviceSynchronize();
+                dfree(ptr);
+            }
             ptr = nullptr;
             cap = 0;
-            if (cudaMalloc(&ptr, count * sizeof(double)) != cudaSuccess)
-                throw Error{FD_ERR_CUDA, "workspace allocation failed"};
+            ptr = static_cast<double *>(dmalloc(count * sizeof(double)));
             cap = count;
         }
         return ptr;
     }
     ~Workspace() {
-        if (ptr) cudaFree(ptr);
+        if (ptr) dfree(ptr);
     }
 };
 
@@ -117,6 +136,7 @@ struct Plan {
     std::vector<float> tprof;   // see SolveJob::tprof
     std::vector<void *> allocs;
     Workspace ws;
+    std::shared_ptr<Plan> shared;   // immutable device tables shared by identical plans (plan.cpp)
 };
 
 // one job of a batched rectangle launch
@@ -173,6 +193,22 @@ void launch_dot(long long N, const double *x, const double *y, double *out, RedW
 // fused MGS step: w -= (*h_prev) * vprev (if vprev); *h_out = vi . w   (vi may be null -> ||w||^2)
 void launch_mgs(long long N, double *w, const double *vprev, const double *h_prev,
                 const double *vi, double *h_out, RedWork wk, cudaStream_t s);
+// low-synchronisation MGS Arnoldi (see ops.cu)
+constexpr int kMaxArnoldi = 64;            // basis vectors V_0..V_k per step, k + 1 <= 64
+struct ArnWork {
+    double *partials;        // [grid][2 * kMaxArnoldi + 2]
+    unsigned int *counter;
+    double *G;               // Gram rows: G[i * ldg + j] = V_i . V_j, j < i
+    double *out;             // results of the launch
+};
+constexpr size_t kArnPartials = size_t(148) * 16 * (2 * kMaxArnoldi + 2);
+// out[0..k] = h (MGS projections), out[k+1] = ||w||^2 before orthogonalisation; Gram row k stored
+void launch_arnoldi_dots(long long N, int k, const double *V, const double *w, ArnWork a, int ldg,
+                         cudaStream_t s);
+// w -= sum_j h_j V_j (j ascending); out[0] = ||w||^2 after
+void launch_arnoldi_update(long long N, int k, const double *V, double *w, const double *h, ArnWork a,
+                           cudaStream_t s);
+void launch_scale_sqrt(long long N, const double *x, const double *nrm2, double *out, cudaStream_t s);
 void launch_basis_update(long long N, int k, const double *V, const double *y_dev, double *x,
                          cudaStream_t s);
 void launch_scale(long long N, const double *x, const double *s_dev, double *out, cudaStream_t s);

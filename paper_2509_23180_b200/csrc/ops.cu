@@ -7,6 +7,8 @@
 // reductions are deterministic (fixed grid, fixed combine order: per-block
 // warp-shuffle trees, then the last block to finish combines the per-block
 // partials in index order), so repeated runs give bitwise-equal results.
+#include <algorithm>
+
 #include "fd_internal.h"
 
 namespace fd {
@@ -206,6 +208,214 @@ __global__ void basis_update_kernel(long long N, int k, const double *__restrict
 void launch_basis_update(long long N, int k, const double *V, const double *y_dev, double *x,
                          cudaStream_t s) {
     basis_update_kernel<<<grid_for(N, 256), 256, 0, s>>>(N, k, V, y_dev, x);
+    FD_CUDA(cudaGetLastError());
+}
+
+}  // namespace fd
+
+namespace fd {
+
+// ---------------------------------------------------------------------------
+// Low-synchronisation MGS Arnoldi step (restates krylov.py:105-111).
+//
+// MGS computes h_i = V_i . (w - sum_{j<i} h_j V_j) one projection at a time,
+// i.e. k+1 dependent passes over the basis.  In exact arithmetic
+//   h_i = s_i - sum_{j<i} G_ij h_j,   s_i = V_i . w,  G_ij = V_i . V_j  (i > j),
+// so one pass computes every s_i plus the new Gram row G_k. = V_k . V_{j<k},
+// a (k+1)-step forward substitution (the last block, subtraction order j
+// ascending as in MGS) gives h, and a second pass forms
+//   w' = w - h_0 V_0 - h_1 V_1 - ... - h_k V_k  (same order)   and ||w'||^2.
+// Bytes per centre point: 8(k+2) + 8(k+1) + 16 instead of 32(k+1) + 8.
+//
+// dots pass: each CTA stages a chunk of w and V_k in shared memory; warp q
+// owns the basis vectors j = q, q + 16, ... and keeps their two running sums
+// in registers across all chunks, so no per-chunk block reductions are needed.
+constexpr int kArnThreads = 512;
+constexpr int kArnWarps = kArnThreads / 32;
+constexpr int kArnChunk = 2048;
+constexpr int kArnJPW = (kMaxArnoldi + kArnWarps - 1) / kArnWarps;   // basis vectors per warp
+
+__device__ __forceinline__ void arn_finish(ArnWork a, int nd, const double *bacc, int k, int ldg,
+                                           bool want_h) {
+    __shared__ bool last;
+    __syncthreads();
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) a.partials[size_t(blockIdx.x) * nd + d] = bacc[d];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int done = atomicAdd(a.counter, 1u);
+        last = (done == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    __shared__ double tot[2 * kMaxArnoldi + 2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const volatile double *pp = a.partials;
+    for (int d = wid; d < nd; d += int(blockDim.x >> 5)) {   // fixed order: lanes stride blocks, then a tree
+        double v = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) v += pp[size_t(b) * nd + d];
+        v = warp_sum(v);
+        if (lane == 0) tot[d] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *a.counter = 0u;
+    if (!want_h) {
+        if (threadIdx.x < nd) a.out[threadIdx.x] = tot[threadIdx.x];
+        return;
+    }
+    // tot = [s_0..s_k | c_0..c_{k-1} | w.w]; Gram row k <- c; h by forward substitution
+    if (wid == 0) {
+        double *G = a.G;
+        for (int j = lane; j < k; j += 32) G[size_t(k) * ldg + j] = tot[k + 1 + j];
+        __syncwarp();
+        // lane owns rows i = lane, lane + 32 (k + 1 <= 64)
+        double h0 = lane <= k ? tot[lane] : 0.0, h1 = lane + 32 <= k ? tot[lane + 32] : 0.0;
+        for (int j = 0; j < k; ++j) {
+            const double hj = __shfl_sync(0xffffffffu, j < 32 ? h0 : h1, j & 31);
+            const int i0 = lane, i1 = lane + 32;
+            if (i0 > j && i0 <= k) h0 = __dsub_rn(h0, __dmul_rn(G[size_t(i0) * ldg + j], hj));
+            if (i1 > j && i1 <= k) h1 = __dsub_rn(h1, __dmul_rn(G[size_t(i1) * ldg + j], hj));
+        }
+        if (lane <= k) a.out[lane] = h0;
+        if (lane + 32 <= k) a.out[lane + 32] = h1;
+        if (lane == 0) a.out[k + 1] = tot[2 * k + 1];   // ||w||^2 before orthogonalisation
+    }
+}
+
+__global__ void __launch_bounds__(kArnThreads) arnoldi_dots_kernel(long long N, int k, const double *__restrict__ V,
+                                                                    const double *__restrict__ w, ArnWork a, int ldg) {
+    __shared__ double sw[kArnChunk], sv[kArnChunk];
+    __shared__ double bacc[2 * kMaxArnoldi + 2];
+    __shared__ double wred[kArnWarps];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nd = 2 * k + 2;
+    const double *vk = V + (long long)k * N;
+    double as[kArnJPW], ac[kArnJPW];
+#pragma unroll
+    for (int q = 0; q < kArnJPW; ++q) as[q] = ac[q] = 0.0;
+    double ww = 0.0;
+    for (long long c0 = (long long)blockIdx.x * kArnChunk; c0 < N; c0 += (long long)gridDim.x * kArnChunk) {
+        const int len = (int)min((long long)kArnChunk, N - c0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < len; t += kArnThreads) {
+            const double wv = w[c0 + t];
+            sw[t] = wv;
+            sv[t] = vk[c0 + t];
+            ww = fma(wv, wv, ww);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kArnJPW; ++q) {
+            const int j = wid + q * kArnWarps;
+            if (j > k) break;
+            const double *vj = V + (long long)j * N + c0;
+            double s = as[q], c = ac[q];
+            const bool gram = j < k;
+            int t = lane;
+#pragma unroll 4
+            for (; t + 96 < len; t += 128) {
+                const double x0 = vj[t], x1 = vj[t + 32], x2 = vj[t + 64], x3 = vj[t + 96];
+                s = fma(x0, sw[t], s);
+                s = fma(x1, sw[t + 32], s);
+                s = fma(x2, sw[t + 64], s);
+                s = fma(x3, sw[t + 96], s);
+                if (gram) {
+                    c = fma(x0, sv[t], c);
+                    c = fma(x1, sv[t + 32], c);
+                    c = fma(x2, sv[t + 64], c);
+                    c = fma(x3, sv[t + 96], c);
+                }
+            }
+            for (; t < len; t += 32) {
+                const double x = vj[t];
+                s = fma(x, sw[t], s);
+                if (gram) c = fma(x, sv[t], c);
+            }
+            as[q] = s;
+            ac[q] = c;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kArnJPW; ++q) {
+        const int j = wid + q * kArnWarps;
+        const double s = warp_sum(as[q]), c = warp_sum(ac[q]);
+        if (lane == 0 && j <= k) {
+            bacc[j] = s;
+            if (j < k) bacc[k + 1 + j] = c;
+        }
+    }
+    ww = warp_sum(ww);
+    if (lane == 0) wred[wid] = ww;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < kArnWarps; ++q) t += wred[q];
+        bacc[2 * k + 1] = t;
+    }
+    arn_finish(a, nd, bacc, k, ldg, true);
+}
+
+// w <- w - h_0 V_0 - ... - h_k V_k (MGS subtraction order); out[0] = ||w||^2
+__global__ void __launch_bounds__(256) arnoldi_update_kernel(long long N, int k, const double *__restrict__ V,
+                                                             double *__restrict__ w, const double *__restrict__ h,
+                                                             ArnWork a) {
+    __shared__ double sh[kMaxArnoldi + 1];
+    __shared__ double bacc[1];
+    __shared__ double red[32];
+    for (int j = threadIdx.x; j <= k; j += blockDim.x) sh[j] = h[j];
+    __syncthreads();
+    double acc = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x) {
+        double x = w[i];
+        int j = 0;
+        for (; j + 3 <= k; j += 4) {
+            const double v0 = V[(long long)j * N + i], v1 = V[(long long)(j + 1) * N + i];
+            const double v2 = V[(long long)(j + 2) * N + i], v3 = V[(long long)(j + 3) * N + i];
+            x = __dsub_rn(x, __dmul_rn(sh[j], v0));
+            x = __dsub_rn(x, __dmul_rn(sh[j + 1], v1));
+            x = __dsub_rn(x, __dmul_rn(sh[j + 2], v2));
+            x = __dsub_rn(x, __dmul_rn(sh[j + 3], v3));
+        }
+        for (; j <= k; ++j) x = __dsub_rn(x, __dmul_rn(sh[j], V[(long long)j * N + i]));
+        w[i] = x;
+        acc = fma(x, x, acc);
+    }
+    acc = block_sum(acc, red);
+    if (threadIdx.x == 0) bacc[0] = acc;
+    arn_finish(a, 1, bacc, k, 0, false);
+}
+
+// out = x / sqrt(*nrm2)  (reference: V[k+1] = w / h[k+1, k], h = ||w||)
+__global__ void scale_sqrt_kernel(long long N, const double *__restrict__ x, const double *__restrict__ nrm2,
+                                  double *out) {
+    const double s = sqrt(*nrm2);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = x[i] / s;
+}
+
+static int arn_grid(long long N) {
+    long long g = (N + kArnChunk - 1) / kArnChunk;
+    return (int)std::min<long long>(std::max<long long>(g, 1), 148LL * 4);
+}
+
+void launch_arnoldi_dots(long long N, int k, const double *V, const double *w, ArnWork a, int ldg,
+                         cudaStream_t s) {
+    if (k + 1 > kMaxArnoldi) throw Error{FD_ERR_VALIDATION, "arnoldi: restart length above 64"};
+    arnoldi_dots_kernel<<<arn_grid(N), kArnThreads, 0, s>>>(N, k, V, w, a, ldg);
+    FD_CUDA(cudaGetLastError());
+}
+
+void launch_arnoldi_update(long long N, int k, const double *V, double *w, const double *h, ArnWork a,
+                           cudaStream_t s) {
+    arnoldi_update_kernel<<<grid_for(N, 256), 256, 0, s>>>(N, k, V, w, h, a);
+    FD_CUDA(cudaGetLastError());
+}
+
+void launch_scale_sqrt(long long N, const double *x, const double *nrm2, double *out, cudaStream_t s) {
+    scale_sqrt_kernel<<<grid_for(N, 256), 256, 0, s>>>(N, x, nrm2, out);
     FD_CUDA(cudaGetLastError());
 }
 

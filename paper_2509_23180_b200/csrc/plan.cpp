@@ -11,9 +11,12 @@
 #include <string.h>
 
 #include <algorithm>
+#include <list>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <sstream>
+#include <thread>
 
 #include "fd_internal.h"
 
@@ -135,12 +138,30 @@ struct HostTables {
     std::vector<double> lam;   // eigenvalues lambda_k (+ kappa)
     std::vector<int> fix;      // first row of the bitwise fixed point (m if none)
     std::vector<double> lt;    // [m][3][ktp] l_i, 1/beta_i, -beta_{i-1}/delta for modes < kt
+    std::vector<std::vector<double>> fl, fb;   // per mode: explicit l_i, beta_i (i < len)
     int kt = 0, ktp = 0;
     long long explicit_rows = 0;
 };
 
+// parallel loop over [0, n) in contiguous chunks on the host's cores
+template <class F>
+static void parallel_for(int n, F fn) {
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int nt = std::min(std::min(hw, 32), std::max(1, n / 64));
+    if (nt <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+        const int lo = int((long long)n * t / nt), hi = int((long long)n * (t + 1) / nt);
+        th.emplace_back([=] { fn(lo, hi); });
+    }
+    for (auto &x : th) x.join();
+}
+
 static HostTables build_tables(int m, int n, double dx, double dy, double kappa, double mod_w,
-                               double mod_e, int R) {
+                               double mod_e, int R, bool carry_tables) {
     const double delta_x = 1.0 / (dx * dx), delta_y = 1.0 / (dy * dy);
     const double off = delta_x;
     std::vector<double> lam(n);
@@ -157,44 +178,75 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
     T.len.resize(n);
     T.cv.resize(4 * size_t(n));
     T.last.resize(2 * size_t(n));
-    T.blk.assign(size_t(nb) * 3 * n, 0.0);
-    for (int k = 0; k < n; ++k) {
-        ModeFactors f = factor_mode(m, lam[k], mod_w, mod_e, off, tol, R);
-        if (f.bad) T.bad_modes.push_back(k);
-        T.fix.push_back(f.fix >= 0 ? f.fix : m);
-        const int len = (int)f.l.size();
-        T.off[k] = (int)(T.ex.size() / 4);
-        T.len[k] = len;
-        T.explicit_rows += len;
-        auto gl = [&](int i) { return i < len ? f.l[i] : f.l_inf; };
-        auto gb = [&](int i) { return i == m - 1 ? f.b_last : (i < len ? f.b[i] : f.b_inf); };
-        T.cv[4 * k + 0] = f.l_inf;
-        T.cv[4 * k + 1] = 1.0 / f.b_inf;
-        T.cv[4 * k + 2] = f.b_inf;
-        T.cv[4 * k + 3] = 1.0 / (-f.l_inf);
-        T.last[2 * k + 0] = f.b_last;
-        T.last[2 * k + 1] = 1.0 / f.b_last;
-        std::vector<double> Pcol(R);
-        const size_t base = T.ex.size();
-        T.ex.resize(base + 4 * size_t(len));
-        // explicit blocks
-        double conv[3];
-        bool conv_done = false;
-        for (int b = 0; b < nb; ++b) {
-            const int s = b * R, e = std::min(m, s + R) - 1;
-            double Pe, xi, Q;
-            if (s < len || e == m - 1 || !conv_done) {
-                if (s >= len && e < m - 1) {
-                    block_scalars(s, e, m, off, gl, gb, &conv[0], &conv[1], &conv[2], nullptr);
-                    conv_done = true;
-                    Pe = conv[0], xi = conv[1], Q = conv[2];
-                } else {
-                    block_scalars(s, e, m, off, gl, gb, &Pe, &xi, &Q, Pcol.data());
-                }
-            } else {
-                Pe = conv[0], xi = conv[1], Q = conv[2];
+    T.fix.resize(n);
+    // per mode (independent, on all host cores): factors until the fixed point,
+    // block scalars of the explicit blocks, of a converged block and of the last
+    std::vector<ModeFactors> mf(n);
+    struct BlkS {
+        std::vector<double> tr;   // [nbt][3] explicit blocks
+        double conv[3], last[3];
+        int nbt;
+        bool has_conv;
+    };
+    std::vector<BlkS> bs(n);
+    parallel_for(n, [&](int k0, int k1) {
+        for (int k = k0; k < k1; ++k) {
+            mf[k] = factor_mode(m, lam[k], mod_w, mod_e, off, tol, R);
+            if (!carry_tables) continue;
+            const ModeFactors &f = mf[k];
+            const int len = (int)f.l.size();
+            auto gl = [&](int i) { return i < len ? f.l[i] : f.l_inf; };
+            auto gb = [&](int i) { return i == m - 1 ? f.b_last : (i < len ? f.b[i] : f.b_inf); };
+            BlkS &q = bs[k];
+            q.nbt = std::min(nb, (len + R - 1) / R);
+            q.tr.resize(3 * size_t(q.nbt));
+            for (int b = 0; b < q.nbt; ++b) {
+                const int s = b * R, e = std::min(m, s + R) - 1;
+                block_scalars(s, e, m, off, gl, gb, &q.tr[3 * b], &q.tr[3 * b + 1], &q.tr[3 * b + 2], nullptr);
             }
-            if (s < len) {
+            q.has_conv = false;
+            for (int b = q.nbt; b < nb - 1; ++b) {   // first converged (non-last) block: all equal
+                const int s = b * R, e = std::min(m, s + R) - 1;
+                block_scalars(s, e, m, off, gl, gb, &q.conv[0], &q.conv[1], &q.conv[2], nullptr);
+                q.has_conv = true;
+                break;
+            }
+            if (q.nbt < nb) {
+                const int s = (nb - 1) * R, e = m - 1;
+                block_scalars(s, e, m, off, gl, gb, &q.last[0], &q.last[1], &q.last[2], nullptr);
+            }
+        }
+    });
+    size_t total = 0;
+    for (int k = 0; k < n; ++k) {
+        const ModeFactors &f = mf[k];
+        if (f.bad) T.bad_modes.push_back(k);
+        T.fix[k] = f.fix >= 0 ? f.fix : m;
+        T.off[k] = (int)total;
+        T.len[k] = (int)f.l.size();
+        total += f.l.size();
+    }
+    T.explicit_rows = (long long)total;
+    T.ex.resize(4 * (carry_tables ? total : 0));
+    parallel_for(n, [&](int k0, int k1) {
+        std::vector<double> Pcol(R);
+        for (int k = k0; k < k1; ++k) {
+            const ModeFactors &f = mf[k];
+            const int len = T.len[k];
+            auto gl = [&](int i) { return i < len ? f.l[i] : f.l_inf; };
+            auto gb = [&](int i) { return i == m - 1 ? f.b_last : (i < len ? f.b[i] : f.b_inf); };
+            T.cv[4 * k + 0] = f.l_inf;
+            T.cv[4 * k + 1] = 1.0 / f.b_inf;
+            T.cv[4 * k + 2] = f.b_inf;
+            T.cv[4 * k + 3] = 1.0 / (-f.l_inf);
+            T.last[2 * k + 0] = f.b_last;
+            T.last[2 * k + 1] = 1.0 / f.b_last;
+            if (!carry_tables) continue;
+            const size_t base = 4 * size_t(T.off[k]);
+            for (int b = 0; b * R < len; ++b) {   // explicit rows with their block-relative P
+                const int s = b * R, e = std::min(m, s + R) - 1;
+                double Pe, xi, Q;
+                block_scalars(s, e, m, off, gl, gb, &Pe, &xi, &Q, Pcol.data());
                 for (int i = s; i <= e && i < len; ++i) {
                     double *r = &T.ex[base + 4 * size_t(i)];
                     r[0] = f.l[i];
@@ -203,11 +255,28 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
                     r[3] = Pcol[i - s];
                 }
             }
-            T.blk[(size_t(b) * 3 + 0) * n + k] = Pe;
-            T.blk[(size_t(b) * 3 + 1) * n + k] = xi;
-            T.blk[(size_t(b) * 3 + 2) * n + k] = Q;
         }
+    });
+    // per-mode factor rows kept for the row-major device tables
+    T.fl.resize(n);
+    T.fb.resize(n);
+    for (int k = 0; k < n; ++k) {
+        T.fl[k] = std::move(mf[k].l);
+        T.fb[k] = std::move(mf[k].b);
     }
+    if (!carry_tables) return T;
+    // block table [nb][3][n], rows written contiguously
+    T.blk.resize(size_t(nb) * 3 * n);
+    parallel_for(nb, [&](int b0, int b1) {
+        for (int b = b0; b < b1; ++b)
+            for (int c = 0; c < 3; ++c) {
+                double *row = &T.blk[(size_t(b) * 3 + c) * n];
+                for (int k = 0; k < n; ++k) {
+                    const BlkS &q = bs[k];
+                    row[k] = b < q.nbt ? q.tr[3 * b + c] : (b == nb - 1 || !q.has_conv) ? q.last[c] : q.conv[c];
+                }
+            }
+    });
     return T;
 }
 
@@ -223,18 +292,20 @@ static void build_long_table(HostTables &T, int m, int n, double off, int kt_cap
     T.ktp = (kt + 1) & ~1;
     if (kt == 0) return;
     T.lt.assign(size_t(m) * 3 * T.ktp, 0.0);
-    for (int k = 0; k < kt; ++k) {
-        const int len = T.len[k];
-        const double *ex = &T.ex[4 * size_t(T.off[k])];
-        auto gl = [&](int i) { return i < len ? ex[4 * i + 0] : T.cv[4 * k + 0]; };
-        auto gb = [&](int i) { return i == m - 1 ? T.last[2 * k] : (i < len ? ex[4 * i + 2] : T.cv[4 * k + 2]); };
-        for (int i = 0; i < m; ++i) {
-            double *r = &T.lt[size_t(i) * 3 * T.ktp];
-            r[k] = (i == 0) ? 0.0 : gl(i);
-            r[T.ktp + k] = 1.0 / gb(i);
-            r[2 * T.ktp + k] = (i == 0) ? 0.0 : -gb(i - 1) / off;
+    const int ktp = T.ktp;
+    parallel_for(m, [&](int i0, int i1) {
+        for (int i = i0; i < i1; ++i) {
+            double *r = &T.lt[size_t(i) * 3 * ktp];
+            for (int k = 0; k < kt; ++k) {
+                const int len = T.len[k];
+                auto gl = [&](int q) { return q < len ? T.fl[k][q] : T.cv[4 * k + 0]; };
+                auto gb = [&](int q) { return q == m - 1 ? T.last[2 * k] : (q < len ? T.fb[k][q] : T.cv[4 * k + 2]); };
+                r[k] = (i == 0) ? 0.0 : gl(i);
+                r[ktp + k] = 1.0 / gb(i);
+                r[2 * ktp + k] = (i == 0) ? 0.0 : -gb(i - 1) / off;
+            }
         }
-    }
+    });
 }
 
 // ---------------------------------------------------------------------------
@@ -270,14 +341,13 @@ const double *dense_table_for(int device, int n) {
     auto key = std::make_pair(device, n);
     auto it = g_dense.find(key);
     if (it != g_dense.end()) return (const double *)it->second;
-    std::vector<double> h(size_t(n) * n);
+    // sin(pi q / (n+1)), q < 2(n+1): the dense DST-I reads S[j][k] at q = (j+1)(k+1) mod 2(n+1)
     const long long P2 = 2LL * (n + 1);
-    for (int j = 0; j < n; ++j)
-        for (int k = 0; k < n; ++k) {
-            long long q = ((long long)(j + 1) * (k + 1)) % P2;   // sin(pi q/(n+1)), exact reduction
-            long double a = 3.141592653589793238462643383279502884L * (long double)q / (long double)(n + 1);
-            h[size_t(j) * n + k] = (double)sinl(a);
-        }
+    std::vector<double> h(P2);
+    for (long long q = 0; q < P2; ++q) {
+        long double a = 3.141592653589793238462643383279502884L * (long double)q / (long double)(n + 1);
+        h[q] = (double)sinl(a);
+    }
     void *d = nullptr;
     FD_CUDA(cudaMalloc(&d, sizeof(double) * h.size()));
     FD_CUDA(cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
@@ -287,16 +357,15 @@ const double *dense_table_for(int device, int n) {
 
 template <class T>
 static T *upload(Plan *p, const std::vector<T> &h) {
-    void *d = nullptr;
     size_t bytes = std::max<size_t>(sizeof(T), sizeof(T) * h.size());
-    FD_CUDA(cudaMalloc(&d, bytes));
+    void *d = dmalloc(bytes);
     p->allocs.push_back(d);
     if (!h.empty()) FD_CUDA(cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
     return (T *)d;
 }
 
-Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
-                  int device) {
+static Plan *build_proto(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
+                         int device) {
     if (m < 1 || n < 1) FD_FAIL(FD_ERR_VALIDATION, "plan: empty grid");
     if (!(dx > 0) || !(dy > 0)) FD_FAIL(FD_ERR_VALIDATION, "plan: nonpositive spacing");
     const int tk = transform_kind(n);
@@ -307,7 +376,7 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
         FD_FAIL(FD_ERR_UNSUPPORTED, os.str());
     }
     const int R = rows_per_block(n);
-    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R);
+    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R, tk == kDense);
     if (!T.bad_modes.empty()) {
         std::ostringstream os;
         os << "operator singular in spectral modes (";
@@ -358,15 +427,16 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
         // row-major copies of the first ecap rows (the transient region of most modes)
         d.ecap = std::min(m, 128);
         std::vector<double> dl(size_t(d.ecap) * n), dib(size_t(d.ecap) * n), db(size_t(d.ecap) * n);
-        for (int k = 0; k < n; ++k)
-            for (int i = 0; i < d.ecap; ++i) {
-                const bool ex = i < T.len[k];
-                const double *r = &T.ex[4 * size_t(T.off[k] + (ex ? i : 0))];
-                const double b = (i == m - 1) ? T.last[2 * k] : (ex ? r[2] : T.cv[4 * k + 2]);
-                dl[size_t(i) * n + k] = ex ? r[0] : T.cv[4 * k + 0];
-                db[size_t(i) * n + k] = b;
-                dib[size_t(i) * n + k] = (i == m - 1) ? T.last[2 * k + 1] : (ex ? r[1] : T.cv[4 * k + 1]);
-            }
+        parallel_for(d.ecap, [&](int i0, int i1) {
+            for (int i = i0; i < i1; ++i)
+                for (int k = 0; k < n; ++k) {
+                    const bool ex = i < T.len[k];
+                    const double b = (i == m - 1) ? T.last[2 * k] : (ex ? T.fb[k][i] : T.cv[4 * k + 2]);
+                    dl[size_t(i) * n + k] = ex ? T.fl[k][i] : T.cv[4 * k + 0];
+                    db[size_t(i) * n + k] = b;
+                    dib[size_t(i) * n + k] = (i == m - 1) ? T.last[2 * k + 1] : (ex ? 1.0 / b : T.cv[4 * k + 1]);
+                }
+        });
         d.dl = upload(p, dl);
         d.dib = upload(p, dib);
         d.db = upload(p, db);
@@ -397,17 +467,95 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
             }
         }
         d.lt = T.kt ? upload(p, T.lt) : nullptr;
-        d.blk = upload(p, T.blk);
-        std::vector<double> zeros(size_t(d.nb) * n, 0.0);
-        d.ye = upload(p, zeros);
-        d.fs = upload(p, zeros);
+        d.blk = T.blk.empty() ? nullptr : upload(p, T.blk);
+        d.ye = d.fs = nullptr;   // per-plan scratch (plan_create)
         d.tw = twiddles_for(device, n);
         d.ralpha = d.tw ? reinterpret_cast<const double *>(d.tw + 2 * (n + 1)) : nullptr;
         d.dense = dense_table_for(device, n);
     } catch (...) {
-        for (void *a : p->allocs) cudaFree(a);
+        cudaDeviceSynchronize();
+        for (void *a : p->allocs) dfree(a);
         delete p;
         throw;
+    }
+    return p;
+}
+
+static void free_tables(Plan *p) {
+    if (!p) return;
+    cudaSetDevice(p->device);
+    cudaDeviceSynchronize();
+    for (void *a : p->allocs) dfree(a);
+    delete p;
+}
+
+// Plans are immutable once built, so identical (device, grid, spacing, kappa,
+// end modifiers) requests share one set of device tables: the centre and the
+// four arms of the BASELINE crosses need one table build instead of five, and
+// repeated solves on the same geometry reuse the last few builds (LRU).
+namespace {
+struct PlanKey {
+    int device, m, n;
+    double v[5];
+    bool operator==(const PlanKey &o) const {
+        return device == o.device && m == o.m && n == o.n && memcmp(v, o.v, sizeof(v)) == 0;
+    }
+};
+constexpr size_t kPlanCache = 8;
+std::mutex g_plan_mu;
+auto *g_plan_lru = new std::list<std::pair<PlanKey, std::shared_ptr<Plan>>>();   // never destroyed
+}  // namespace
+
+Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
+                  int device) {
+    PlanKey key{device, m, n, {dx, dy, kappa, mod_w, mod_e}};
+    std::shared_ptr<Plan> proto;
+    {
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        for (auto it = g_plan_lru->begin(); it != g_plan_lru->end(); ++it)
+            if (it->first == key) {
+                g_plan_lru->splice(g_plan_lru->begin(), *g_plan_lru, it);
+                proto = g_plan_lru->front().second;
+                break;
+            }
+    }
+    if (!proto) {
+        proto = std::shared_ptr<Plan>(build_proto(m, n, dx, dy, kappa, mod_w, mod_e, device), free_tables);
+        std::lock_guard<std::mutex> g(g_plan_mu);
+        g_plan_lru->emplace_front(key, proto);
+        if (g_plan_lru->size() > kPlanCache) g_plan_lru->pop_back();
+    }
+    FD_CUDA(cudaSetDevice(device));
+    Plan *p = new Plan();
+    p->device = proto->device;
+    p->m = proto->m;
+    p->n = proto->n;
+    p->dx = proto->dx;
+    p->dy = proto->dy;
+    p->kappa = proto->kappa;
+    p->mod_w = proto->mod_w;
+    p->mod_e = proto->mod_e;
+    p->delta_x = proto->delta_x;
+    p->delta_y = proto->delta_y;
+    p->transform = proto->transform;
+    p->explicit_rows = proto->explicit_rows;
+    p->dev = proto->dev;
+    p->tprof = proto->tprof;
+    p->shared = proto;
+    if (p->transform == kDense) {   // pass-1/carry scratch of the three-kernel solve
+        try {
+            const size_t bytes = sizeof(double) * size_t(p->dev.nb) * n;
+            p->dev.ye = static_cast<double *>(dmalloc(bytes));
+            p->allocs.push_back(p->dev.ye);
+            p->dev.fs = static_cast<double *>(dmalloc(bytes));
+            p->allocs.push_back(p->dev.fs);
+            FD_CUDA(cudaMemset(p->dev.ye, 0, bytes));
+            FD_CUDA(cudaMemset(p->dev.fs, 0, bytes));
+        } catch (...) {
+            for (void *a : p->allocs) dfree(a);
+            delete p;
+            throw;
+        }
     }
     return p;
 }
@@ -415,15 +563,16 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
 void plan_destroy(Plan *p) {
     if (!p) return;
     cudaSetDevice(p->device);
-    for (void *a : p->allocs) cudaFree(a);
-    delete p;
+    cudaDeviceSynchronize();
+    for (void *a : p->allocs) dfree(a);
+    delete p;   // drops the shared tables reference
 }
 
 void factor_tables_host(int m, int n, double dx, double dy, double kappa, double mod_w,
                         double mod_e, double *beta, double *lower) {
     if (m < 1 || n < 1) FD_FAIL(FD_ERR_VALIDATION, "factor: empty grid");
     const int R = (transform_kind(n) >= 0) ? rows_per_block(n) : 16;
-    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R);
+    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R, true);
     for (int k = 0; k < n; ++k) {
         for (int i = 0; i < m; ++i) {
             const bool ex = i < T.len[k];

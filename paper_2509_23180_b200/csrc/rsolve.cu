@@ -31,7 +31,7 @@ __device__ __forceinline__ int xi(int q) { return q + (q >> 4); }
 template <int NL>
 struct RS {
     static constexpr int N = 1 << NL;
-    static constexpr int NT = kRsThreads;
+    static constexpr int NT = rs_threads(1 << NL);
     static constexpr int T = N / 16;                  // threads per row pair
     static constexpr int P = NT / T;                  // pairs per CTA
     static constexpr int G = 2 * P;                   // rows per group
@@ -47,7 +47,7 @@ struct RS {
     static constexpr size_t OFF_AL = OFF_TW + 272 * 16;   // alpha[N]
     static constexpr size_t OFF_SC = OFF_AL + size_t(N) * 8;
     static constexpr size_t OFF_LT = OFF_SC + size_t(P) * 16 * 8;
-    static constexpr size_t SMEM = kRsSmem;
+    static constexpr size_t SMEM = rs_smem(1 << NL);
     static_assert(OFF_LT == rs_fixed_smem(N), "layout shared with the plan builder");
     static_assert(PER * RL == 16, "16 points per thread in the last pass");
     static_assert(XR * 2 <= PADN * 2, "transformed rows fit the pair region");
@@ -265,7 +265,7 @@ __device__ __noinline__ void factors_slow(const PlanDev &p, int k, int i, int le
 }
 
 template <int NL>
-__global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_constant__ PList pl) {
+__global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(const __grid_constant__ PList pl) {
     using C = RS<NL>;
     using F = RFft<NL>;
     constexpr int NT = C::NT, G = C::G, P = C::P, T = C::T, MPT = C::MPT, XR = C::XR;
@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rsolve_kernel(const __grid_cons
 // ---------------------------------------------------------------------------
 template <int NL>
 struct RsK {
-    static constexpr int NT = kRsThreads, G = RS<NL>::G;
+    static constexpr int NT = RS<NL>::NT, G = RS<NL>::G;
     static constexpr size_t SMEM = RS<NL>::SMEM;
     static const void *fn() { return (const void *)rsolve_kernel<NL>; }
 };

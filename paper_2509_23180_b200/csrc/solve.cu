@@ -83,37 +83,64 @@ struct InvT<FftDst<LG>> {
     }
 };
 
-template <>
-struct FwdT<DenseDst> {
-    __device__ static void run(const double *in, int rows, int n, double *rowbuf, double2 *,
-                               const PlanDev &p) {
-        constexpr int NT = DenseDst::NT, G = DenseDst::G;
-        for (int idx = threadIdx.x; idx < rows * n; idx += NT) rowbuf[idx] = __ldg(in + idx);
-        __syncthreads();
-        double acc[G][DenseDst::MPT];
+// Dense transform of the G-row group in rowbuf (shared) into acc (registers).
+template <int M>
+__device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const double *tab,
+                                           double (&acc)[DenseDstT<M>::G][M]) {
+    constexpr int NT = DenseDstT<M>::NT, G = DenseDstT<M>::G;
+    const int N2 = 2 * (n + 1);
+    int idx[M];
 #pragma unroll
-        for (int g = 0; g < G; ++g)
+    for (int u = 0; u < M; ++u) {
+        idx[u] = threadIdx.x + u * NT + 1;   // (j + 1)(k + 1) mod 2N at j = 0
 #pragma unroll
-            for (int u = 0; u < DenseDst::MPT; ++u) acc[g][u] = 0.0;
-#pragma unroll 1
-        for (int j = 0; j < n; ++j) {
-            double x[G];
+        for (int g = 0; g < G; ++g) acc[g][u] = 0.0;
+    }
+#pragma unroll 2
+    for (int j = 0; j < n; ++j) {
+        double x[G];
 #pragma unroll
-            for (int g = 0; g < G; ++g) x[g] = g < rows ? rowbuf[g * n + j] : 0.0;
+        for (int g = 0; g < G; ++g) x[g] = rowbuf[g * n + j];
 #pragma unroll
-            for (int u = 0; u < DenseDst::MPT; ++u) {
-                int k = threadIdx.x + u * NT;
-                if (k < n) {
-                    double s = __ldg(p.dense + size_t(j) * n + k);
+        for (int u = 0; u < M; ++u) {
+            const int k1 = threadIdx.x + u * NT + 1;
+            if (k1 <= n) {
+                const double sv = tab[idx[u]];
 #pragma unroll
-                    for (int g = 0; g < G; ++g) acc[g][u] = fma(s, x[g], acc[g][u]);
-                }
+                for (int g = 0; g < G; ++g) acc[g][u] = fma(sv, x[g], acc[g][u]);
+                idx[u] += k1;
+                if (idx[u] >= N2) idx[u] -= N2;
             }
         }
+    }
+}
+
+template <int M>
+__device__ __forceinline__ double *dense_tab(double2 *smem) {
+    return reinterpret_cast<double *>(smem) + DenseDstT<M>::G * DenseDstT<M>::NMAX;
+}
+
+template <int M>
+__device__ __forceinline__ void stage_tab(double *tab, int n, const PlanDev &p) {
+    for (int q = threadIdx.x; q < 2 * (n + 1); q += DenseDstT<M>::NT) tab[q] = __ldg(p.dense + q);
+}
+
+template <int M>
+struct FwdT<DenseDstT<M>> {
+    __device__ static void run(const double *in, int rows, int n, double *rowbuf, double2 *smem,
+                               const PlanDev &p) {
+        constexpr int NT = DenseDstT<M>::NT, G = DenseDstT<M>::G;
+        double *tab = dense_tab<M>(smem);
+        stage_tab<M>(tab, n, p);
+        for (int idx = threadIdx.x; idx < G * n; idx += NT)
+            rowbuf[idx] = idx < rows * n ? __ldg(in + idx) : 0.0;
+        __syncthreads();
+        double acc[G][M];
+        dense_rows<M>(rowbuf, n, tab, acc);
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < DenseDst::MPT; ++u) {
-            int k = threadIdx.x + u * NT;
+        for (int u = 0; u < M; ++u) {
+            const int k = threadIdx.x + u * NT;
             if (k < n)
 #pragma unroll
                 for (int g = 0; g < G; ++g)
@@ -123,34 +150,20 @@ struct FwdT<DenseDst> {
     }
 };
 
-template <>
-struct InvT<DenseDst> {
-    __device__ static void run(const double *rowbuf, int rows, int n, double *out, const double *other,
-                               double alpha, double beta, double2 *, const PlanDev &p) {
-        constexpr int NT = DenseDst::NT, G = DenseDst::G;
-        double acc[G][DenseDst::MPT];
+template <int M>
+struct InvT<DenseDstT<M>> {
+    __device__ static void run(double *rowbuf, int rows, int n, double *out, const double *other,
+                               double alpha, double beta, double2 *smem, const PlanDev &p) {
+        constexpr int NT = DenseDstT<M>::NT, G = DenseDstT<M>::G;
+        double *tab = dense_tab<M>(smem);
+        stage_tab<M>(tab, n, p);
+        for (int idx = rows * n + threadIdx.x; idx < G * n; idx += NT) rowbuf[idx] = 0.0;
+        __syncthreads();
+        double acc[G][M];
+        dense_rows<M>(rowbuf, n, tab, acc);
 #pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-            for (int u = 0; u < DenseDst::MPT; ++u) acc[g][u] = 0.0;
-#pragma unroll 1
-        for (int j = 0; j < n; ++j) {
-            double x[G];
-#pragma unroll
-            for (int g = 0; g < G; ++g) x[g] = g < rows ? rowbuf[g * n + j] : 0.0;
-#pragma unroll
-            for (int u = 0; u < DenseDst::MPT; ++u) {
-                int k = threadIdx.x + u * NT;
-                if (k < n) {
-                    double s = __ldg(p.dense + size_t(j) * n + k);
-#pragma unroll
-                    for (int g = 0; g < G; ++g) acc[g][u] = fma(s, x[g], acc[g][u]);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < DenseDst::MPT; ++u) {
-            int k = threadIdx.x + u * NT;
+        for (int u = 0; u < M; ++u) {
+            const int k = threadIdx.x + u * NT;
             if (k < n)
 #pragma unroll
                 for (int g = 0; g < G; ++g)
@@ -170,9 +183,9 @@ template <int LG>
 struct Cfg<FftDst<LG>> {
     static constexpr int MPT = ((1 << (LG - 1)) - 1 + FftDst<LG>::NT - 1) / FftDst<LG>::NT;
 };
-template <>
-struct Cfg<DenseDst> {
-    static constexpr int MPT = DenseDst::MPT;
+template <int M>
+struct Cfg<DenseDstT<M>> {
+    static constexpr int MPT = M;
 };
 
 // ---------------------------------------------------------------------------
@@ -404,7 +417,7 @@ int transform_kind(int n) {
 int rows_per_block(int n) {
     const int N = n + 1;
     if (transform_kind(n) == kFFT) return N >= 4096 ? 8 : 16;
-    return 16;
+    return DenseDstT<1>::G;   // one group per carry block: more CTAs for the small dense solves
 }
 
 template <class P>
@@ -478,7 +491,10 @@ void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
     for (auto &j : jobs)
         if (j.p.n != n) FD_FAIL(FD_ERR_VALIDATION, "launch_solve: mixed transform lengths in one batch");
     if (transform_kind(n) == kDense) {
-        run_solve<DenseDst>(jobs, s);
+        if (n <= 128) run_solve<DenseDstT<1>>(jobs, s);
+        else if (n <= 256) run_solve<DenseDstT<2>>(jobs, s);
+        else if (n <= 512) run_solve<DenseDstT<4>>(jobs, s);
+        else run_solve<DenseDstT<8>>(jobs, s);
         return;
     }
     if (jobs[0].ws && launch_persist(jobs, s, *jobs[0].ws)) return;
@@ -497,7 +513,10 @@ void launch_dst_rows(int rows, int n, const double *in, double *out, const doubl
                      const double *dense, cudaStream_t s) {
     if (rows <= 0) return;
     if (transform_kind(n) == kDense) {
-        run_dst<DenseDst>(rows, n, in, out, tw, dense, s);
+        if (n <= 128) run_dst<DenseDstT<1>>(rows, n, in, out, tw, dense, s);
+        else if (n <= 256) run_dst<DenseDstT<2>>(rows, n, in, out, tw, dense, s);
+        else if (n <= 512) run_dst<DenseDstT<4>>(rows, n, in, out, tw, dense, s);
+        else run_dst<DenseDstT<8>>(rows, n, in, out, tw, dense, s);
         return;
     }
     switch (lg_of(n)) {
