@@ -59,6 +59,19 @@ int fd_version(void);
  * of the two-pass Thomas solve.  FD_ERR_SINGULAR on a zero pivot. */
 int fd_plan_create(fd_plan *out, int m, int n, double dx, double dy, double kappa,
                    double mod_west, double mod_east, int device);
+/* Same with the transform axis chosen by the caller (reference
+ * rectsolver.plan_rect, rectsolver.py:102-123): transform_axis 0 = y (as
+ * fd_plan_create; south/north must be ghost-node ends), 1 = x (west/east must
+ * be ghost-node ends; the sweep runs along y with the south/north modifiers).
+ * Fields passed to the solves stay in the user's x-line-major layout; an
+ * x-axis plan transposes them on the device around the fused solve
+ * (rectsolver.py:198-199,211-212). */
+int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double kappa,
+                        double mod_west, double mod_east, double mod_south, double mod_north,
+                        int transform_axis, int device);
+/* GPU transform available for length n: 1 = FFT (n+1 = 2^p, 256..4096),
+ * 0 = dense (n <= 1024), -1 = none. */
+int fd_transform_kind(int n);
 int fd_plan_destroy(fd_plan plan);
 /* rows per carry block, explicit factor rows, transform kind (0 dense, 1 fft) */
 int fd_plan_info(fd_plan plan, int *block_rows, long long *explicit_rows, int *transform);

@@ -116,8 +116,9 @@ static double norm2(long long N, const double *x, Scratch &sc, cudaStream_t s) {
 // Schur operator
 struct Coupling {
     int len;
-    int64_t *from, *to;   // device
+    int64_t *from, *to;   // device, in the plans' internal layouts
     double c;
+    int64_t *from_user;   // R_ci only: neighbour indices in the user layout (== from unless transposed)
 };
 
 }  // namespace fd
@@ -175,6 +176,47 @@ static SolveJob job_of(const Plan *p, const double *in, double *out) {
     return j;
 }
 
+// Solves on fields in the caller's layout.  Plans with a transposed transform
+// axis get their field transposed into the plan's scratch, solved in place
+// there and transposed back with the epilogue out = alpha x + beta other.
+struct UJob {
+    Plan *p;
+    const double *in;
+    double *out;
+    double alpha = 1.0, beta = 0.0;
+    const double *other = nullptr;
+};
+static void solve_user(const std::vector<UJob> &uj, cudaStream_t s) {
+    std::vector<SolveJob> jobs;
+    std::vector<size_t> tr;
+    for (size_t i = 0; i < uj.size(); ++i) {
+        Plan *p = uj[i].p;
+        if (!p->transposed) {
+            SolveJob j = job_of(p, uj[i].in, uj[i].out);
+            j.alpha = uj[i].alpha;
+            j.beta = uj[i].beta;
+            j.other = uj[i].other;
+            jobs.push_back(j);
+            continue;
+        }
+        for (size_t q : tr)
+            if (uj[q].p == p) {   // one scratch per plan: a repeated plan runs on its own
+                for (const UJob &u : uj) solve_user({u}, s);
+                return;
+            }
+        const size_t cnt = size_t(p->m) * p->n;
+        double *t = p->tws.get(cnt);
+        launch_transpose(p->um, p->un, uj[i].in, t, 1.0, 0.0, nullptr, s);
+        jobs.push_back(job_of(p, t, t));
+        tr.push_back(i);
+    }
+    solve_batch(jobs, s);
+    for (size_t i : tr) {
+        Plan *p = uj[i].p;
+        launch_transpose(p->m, p->n, p->tws.ptr, uj[i].out, uj[i].alpha, uj[i].beta, uj[i].other, s);
+    }
+}
+
 // out = sum_i R_ci A_i^{-1} R_ic p   (ddm.py:108-123)
 static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
     const size_t nnb = op->nb.size();
@@ -198,11 +240,8 @@ static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream
 // out = alpha * A_c^{-1} r + beta * other
 static void center_solve(fd_schur_s *op, const double *r, double *out, double alpha, double beta,
                          const double *other, cudaStream_t s) {
-    SolveJob j = job_of(op->center, r, out);
-    j.alpha = alpha;
-    j.beta = beta;
-    j.other = other;
-    solve_batch({j}, s);
+    UJob j{op->center, r, out, alpha, beta, other};
+    solve_user({j}, s);
 }
 
 // (I - A_c^{-1} S) p   (ddm.py:133-136); out must not alias p
@@ -422,9 +461,38 @@ int fd_plan_create(fd_plan *out, int m, int n, double dx, double dy, double kapp
     if (!out) FD_FAIL(FD_ERR_VALIDATION, "null output handle");
     *out = nullptr;
     Plan *p = plan_create(m, n, dx, dy, kappa, mod_west, mod_east, device);
+    p->um = m;
+    p->un = n;
     *out = new fd_plan_s{p};
     FD_API_END
 }
+
+int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double kappa,
+                        double mod_west, double mod_east, double mod_south, double mod_north,
+                        int transform_axis, int device) {
+    FD_API_BEGIN
+    if (!out) FD_FAIL(FD_ERR_VALIDATION, "null output handle");
+    *out = nullptr;
+    Plan *p = nullptr;
+    if (transform_axis == 0) {
+        if (mod_south != 0.0 || mod_north != 0.0)
+            FD_FAIL(FD_ERR_UNSUPPORTED, "transform along y needs ghost-node ends on south/north");
+        p = plan_create(m, n, dx, dy, kappa, mod_west, mod_east, device);
+    } else if (transform_axis == 1) {
+        if (mod_west != 0.0 || mod_east != 0.0)
+            FD_FAIL(FD_ERR_UNSUPPORTED, "transform along x needs ghost-node ends on west/east");
+        p = plan_create(n, m, dy, dx, kappa, mod_south, mod_north, device);
+        p->transposed = true;
+    } else {
+        FD_FAIL(FD_ERR_VALIDATION, "transform_axis must be 0 (y) or 1 (x)");
+    }
+    p->um = m;
+    p->un = n;
+    *out = new fd_plan_s{p};
+    FD_API_END
+}
+
+int fd_transform_kind(int n) { return transform_kind(n); }
 
 int fd_plan_destroy(fd_plan plan) {
     FD_API_BEGIN
@@ -454,19 +522,19 @@ int fd_factor_tables_host(int m, int n, double dx, double dy, double kappa, doub
 int fd_rect_solve(fd_plan plan, const double *f, double *out, void *stream) {
     FD_API_BEGIN
     if (!plan || !f || !out) FD_FAIL(FD_ERR_VALIDATION, "null argument");
-    solve_batch({job_of(plan->p, f, out)}, S(stream));
+    solve_user({UJob{plan->p, f, out}}, S(stream));
     FD_API_END
 }
 
 int fd_rect_solve_batched(int count, const fd_plan *plans, const double *const *f, double *const *out,
                           void *stream) {
     FD_API_BEGIN
-    std::vector<SolveJob> jobs;
+    std::vector<UJob> jobs;
     for (int i = 0; i < count; ++i) {
         if (!plans[i] || !f[i] || !out[i]) FD_FAIL(FD_ERR_VALIDATION, "null argument");
-        jobs.push_back(job_of(plans[i]->p, f[i], out[i]));
+        jobs.push_back(UJob{plans[i]->p, f[i], out[i]});
     }
-    solve_batch(jobs, S(stream));
+    solve_user(jobs, S(stream));
     FD_API_END
 }
 
@@ -513,9 +581,19 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, doub
                 return d;
             };
             const int len = line_len[i];
-            op->to_c.push_back(Coupling{len, up(to_c_from[i], len), up(to_c_to[i], len), to_c_coupling[i]});
-            op->from_c.push_back(
-                Coupling{len, up(from_c_from[i], len), up(from_c_to[i], len), from_c_coupling[i]});
+            // neighbour-side indices in the plan's internal layout (transposed axis)
+            auto internal = [&](const int64_t *h) {
+                std::vector<int64_t> v(h, h + len);
+                if (q->transposed)
+                    for (auto &x : v) x = (x % q->un) * q->um + x / q->un;
+                return v;
+            };
+            const std::vector<int64_t> tcf = internal(to_c_from[i]), fct = internal(from_c_to[i]);
+            int64_t *tcf_user = up(to_c_from[i], len);
+            op->to_c.push_back(Coupling{len, q->transposed ? up(tcf.data(), len) : tcf_user, up(to_c_to[i], len),
+                                        to_c_coupling[i], tcf_user});
+            op->from_c.push_back(Coupling{len, up(from_c_from[i], len), up(fct.data(), len),
+                                          from_c_coupling[i], nullptr});
             op->nbf.push_back((double *)dalloc(op, sizeof(double) * q->m * q->n));
         }
         op->tmp = (double *)dalloc(op, sizeof(double) * Nc);
@@ -599,16 +677,16 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     const size_t nnb = op->nb.size();
     const long long Nc = (long long)op->center->m * op->center->n;
     // pre-solves q_i = A_i^{-1} f_i into the caller's output fields (ddm.py:249-250)
-    std::vector<SolveJob> jobs;
-    for (size_t i = 0; i < nnb; ++i) jobs.push_back(job_of(op->nb[i], f_nb[i], p_nb[i]));
-    solve_batch(jobs, s);
+    std::vector<UJob> ujobs;
+    for (size_t i = 0; i < nnb; ++i) ujobs.push_back(UJob{op->nb[i], f_nb[i], p_nb[i]});
+    solve_user(ujobs, s);
     // f' = f_c - sum_i R_ci q_i  (ddm.py:252-254); tmp2 holds f'
     double *fp = op->tmp2;
     FD_CUDA(cudaMemcpyAsync(fp, f_center, sizeof(double) * Nc, cudaMemcpyDeviceToDevice, s));
     for (size_t i = 0; i < nnb; ++i) {
         const Coupling &c = op->to_c[i];
         // fp[to] = fp[to] - c * q[from]
-        launch_scatter(c.len, c.from, c.to, -c.c, p_nb[i], fp, 1, s);
+        launch_scatter(c.len, c.from_user, c.to, -c.c, p_nb[i], fp, 1, s);
     }
     // solve_coupled fft branch: rhs = A_c^{-1} f'; GMRES on the preconditioned system
     // (krylov.py:176-187); fp must survive, so rhs goes to a fresh buffer
@@ -624,7 +702,7 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     rep->true_residual = norm2(Nc, rhs, op->sc, s);
     FD_CUDA(cudaFreeAsync(rhs, s));
     // back-substitution p_i = q_i - A_i^{-1} R_ic p_c (ddm.py:259-269)
-    jobs.clear();
+    std::vector<SolveJob> jobs;
     for (size_t i = 0; i < nnb; ++i) {
         const Plan *q = op->nb[i];
         FD_CUDA(cudaMemsetAsync(op->nbf[i], 0, sizeof(double) * q->m * q->n, s));
@@ -635,7 +713,10 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     solve_batch(jobs, s);
     for (size_t i = 0; i < nnb; ++i) {
         const Plan *q = op->nb[i];
-        launch_axpby((long long)q->m * q->n, 1.0, p_nb[i], -1.0, op->nbf[i], p_nb[i], s);
+        if (q->transposed)
+            launch_transpose(q->m, q->n, op->nbf[i], p_nb[i], -1.0, 1.0, p_nb[i], s);
+        else
+            launch_axpby((long long)q->m * q->n, 1.0, p_nb[i], -1.0, op->nbf[i], p_nb[i], s);
     }
     if (st != FD_OK) {
         std::ostringstream os;

@@ -69,7 +69,7 @@ struct PlanDev {
 // pre-weights and scan scratch are fixed, the rest of the shared memory holds
 // one group's slice of the long-transient table (24 B per row and mode).
 constexpr int kRsThreads = 512;
-constexpr int kRsMinN = 256, kRsMaxN = 2048;
+constexpr int kRsMinN = 256, kRsMaxN = 4096;
 constexpr size_t kRsSmem = 227 * 1024 - 2048;
 #ifndef FD_RS_SMALL_N
 #define FD_RS_SMALL_N 0
@@ -137,6 +137,12 @@ struct Plan {
     std::vector<void *> allocs;
     Workspace ws;
     std::shared_ptr<Plan> shared;   // immutable device tables shared by identical plans (plan.cpp)
+    // transform along x (reference transform_axis == "x"): the tables above are
+    // those of the transposed rectangle (m, n) = (user n, user m); user-layout
+    // fields are transposed into tws around the solve
+    bool transposed = false;
+    int um = 0, un = 0;   // user-layout rows (x-lines), columns (y)
+    Workspace tws;
 };
 
 // one job of a batched rectangle launch
@@ -209,6 +215,9 @@ void launch_arnoldi_dots(long long N, int k, const double *V, const double *w, A
 void launch_arnoldi_update(long long N, int k, const double *V, double *w, const double *h, ArnWork a,
                            cudaStream_t s);
 void launch_scale_sqrt(long long N, const double *x, const double *nrm2, double *out, cudaStream_t s);
+// out (C x R) = alpha * in^T + beta * other (other may be null); in is R x C
+void launch_transpose(int R, int C, const double *in, double *out, double alpha, double beta,
+                      const double *other, cudaStream_t s);
 void launch_basis_update(long long N, int k, const double *V, const double *y_dev, double *x,
                          cudaStream_t s);
 void launch_scale(long long N, const double *x, const double *s_dev, double *out, cudaStream_t s);

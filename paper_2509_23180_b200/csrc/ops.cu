@@ -420,3 +420,43 @@ void launch_scale_sqrt(long long N, const double *x, const double *nrm2, double 
 }
 
 }  // namespace fd
+
+namespace fd {
+
+// out (C x R) = alpha * in^T + beta * other, in (R x C) row-major.  32 x 32
+// tiles through padded shared memory: coalesced reads and writes, HBM-bound.
+// Used for the transposed transform axis (reference transform_axis == "x",
+// rectsolver.py:198-199,211-212): fields go to the plan's internal layout and
+// back; the epilogue folds the back-substitution's p_i = q_i - A_i^{-1}(...).
+__global__ void __launch_bounds__(256) transpose_kernel(int R, int C, const double *__restrict__ in,
+                                                        double *out, double alpha, double beta,
+                                                        const double *other) {
+    __shared__ double tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
+    const long long r0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const long long r = r0 + ty + 8 * q, c = c0 + tx;
+        if (r < R && c < C) tile[ty + 8 * q][tx] = in[r * C + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const long long c = c0 + ty + 8 * q, r = r0 + tx;
+        if (r < R && c < C) {
+            double v = alpha * tile[tx][ty + 8 * q];
+            if (other) v = __dadd_rn(v, __dmul_rn(beta, other[c * R + r]));
+            out[c * R + r] = v;
+        }
+    }
+}
+
+void launch_transpose(int R, int C, const double *in, double *out, double alpha, double beta,
+                      const double *other, cudaStream_t s) {
+    if (R <= 0 || C <= 0) return;
+    dim3 grid((C + 31) / 32, (R + 31) / 32);
+    transpose_kernel<<<grid, 256, 0, s>>>(R, C, in, out, alpha, beta, other);
+    FD_CUDA(cudaGetLastError());
+}
+
+}  // namespace fd

@@ -869,6 +869,7 @@ bool launch_rsolve(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace 
         case 512: run_persist<RsK<9>>(jobs, s, ws); return true;
         case 1024: run_persist<RsK<10>>(jobs, s, ws); return true;
         case 2048: run_persist<RsK<11>>(jobs, s, ws); return true;
+        case 4096: run_persist<RsK<12>>(jobs, s, ws); return true;
         default: return false;
     }
 }

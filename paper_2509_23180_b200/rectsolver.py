@@ -4,7 +4,9 @@ plan_rect builds a native plan (eigenvalues, compressed per-mode LU factors
 and block-carry tables, csrc/plan.cpp); solve_rect runs the fused
 DST-I -> Thomas -> DST-I pipeline (csrc/solve.cu).  Scope: the DD transform
 along y with ghost-node ends (the reference's default axis choice,
-rectsolver.py:24-29,102-109); the sweep axis x may carry any non-periodic
+rectsolver.py:24-29,102-109) or along x (the reference's transform_axis "x"
+branch, rectsolver.py:111-118,198-199,211-212; also taken when y has no GPU
+transform length, see _gpu_axis); the sweep axis may carry any non-periodic
 pair with end modifiers (half-cell Dirichlet, Neumann).  Other layouts raise
 UnsupportedError.
 """
@@ -22,24 +24,46 @@ from .errors import SingularOperatorError, ValidationError
 from .geometry import BoundaryKind, GridField, RectSubdomain
 
 
-def _check_supported(sub: RectSubdomain):
-    if sub.axis_pair("y") != "DD" or sub.end_modifier("south") or sub.end_modifier("north"):
+def _gpu_axis(sub: RectSubdomain) -> str:
+    """Transform axis of the GPU plan.  The reference transforms along y when
+    that axis is in pure DD form and along x otherwise (rectsolver.py:102-109);
+    the GPU follows it, except that a y length without a GPU transform (n + 1
+    above 4096, e.g. the c4 south/north arms, n = 16383) moves the transform to
+    a transformable x axis (the reference's own transform_axis = "x" branch):
+    the FFT stays within one SM's shared memory and the long axis becomes the
+    Thomas sweep.  Same operator, rounding-level differences only."""
+    def ok(axis):
+        lo, hi = ("south", "north") if axis == "y" else ("west", "east")
+        return sub.axis_pair(axis) == "DD" and not sub.end_modifier(lo) and not sub.end_modifier(hi)
+
+    def has_kernel(length):
+        return _native.lib().fd_transform_kind(int(length)) >= 0
+
+    y_ok, x_ok = ok("y"), ok("x")
+    if y_ok and (has_kernel(sub.n) or not (x_ok and has_kernel(sub.m))):
+        axis = "y"
+    elif x_ok:
+        axis = "x"
+    else:
         raise UnsupportedError(
-            f"subdomain {sub.id}: only a ghost-node Dirichlet/interface pair along y "
-            f"is on the GPU path (got {sub.axis_pair('y')} with end modifiers)")
-    if sub.axis_pair("x") == "PP":
+            f"subdomain {sub.id}: neither axis is a ghost-node Dirichlet/interface pair "
+            f"(got y {sub.axis_pair('y')}, x {sub.axis_pair('x')} with end modifiers)")
+    sweep = "x" if axis == "y" else "y"
+    if sub.axis_pair(sweep) == "PP":
         raise UnsupportedError(f"subdomain {sub.id}: periodic sweep axis is not on the GPU path")
+    return axis
 
 
 class _Handle:
     """Owns one native plan handle."""
 
-    def __init__(self, sub: RectSubdomain):
+    def __init__(self, sub: RectSubdomain, axis: str):
         _native.require_cuda()
         h = _native.P()
-        _native.call("fd_plan_create", ctypes_ref(h), sub.m, sub.n, float(sub.dx), float(sub.dy),
-                     float(sub.kappa), float(sub.end_modifier("west")),
-                     float(sub.end_modifier("east")), _native.torch().cuda.current_device())
+        _native.call("fd_plan_create_axis", ctypes_ref(h), sub.m, sub.n, float(sub.dx), float(sub.dy),
+                     float(sub.kappa), float(sub.end_modifier("west")), float(sub.end_modifier("east")),
+                     float(sub.end_modifier("south")), float(sub.end_modifier("north")),
+                     0 if axis == "y" else 1, _native.torch().cuda.current_device())
         self.ptr = h
 
     def __del__(self):
@@ -89,11 +113,17 @@ def plan_rect(subdomain: RectSubdomain, pin_mean: bool = False) -> RectPlan:
     sub = subdomain
     if pin_mean:
         raise UnsupportedError("pin_mean (singular all-Neumann operators) is not on the GPU path")
-    _check_supported(sub)
-    lam_plan = transforms.make_plan("DD", sub.n, sub.delta_y, sub.delta_x, sub.kappa)
-    handle = _Handle(sub)
-    return RectPlan(subdomain=sub, transform_axis="y", y_plan=lam_plan,
-                    solve_pair=sub.axis_pair("x"), off=sub.delta_x, handle=handle)
+    _native.require_cuda()
+    axis = _gpu_axis(sub)
+    if axis == "y":
+        lam_plan = transforms.make_plan("DD", sub.n, sub.delta_y, sub.delta_x, sub.kappa)
+        pair, off = sub.axis_pair("x"), sub.delta_x
+    else:
+        lam_plan = transforms.make_plan("DD", sub.m, sub.delta_x, sub.delta_y, sub.kappa)
+        pair, off = sub.axis_pair("y"), sub.delta_y
+    handle = _Handle(sub, axis)
+    return RectPlan(subdomain=sub, transform_axis=axis, y_plan=lam_plan,
+                    solve_pair=pair, off=off, handle=handle)
 
 
 def solve_rect(plan: RectPlan, f) -> GridField:

@@ -239,6 +239,82 @@ class TestDdmSolve:
             assert torch.linalg.norm(v).item() == pytest.approx(float(g[f"norm_{sid}"]), rel=1e-10)
 
 
+class TestTransposedAxis:
+    """Transform along x (reference transform_axis "x", rectsolver.py:102-118,
+    198-212): taken when y is not a ghost-node pair, or when the y length has
+    no GPU transform (c4 south/north arms, n = 16383).  Fields stay in the
+    caller's layout; the plan transposes on the device."""
+
+    @staticmethod
+    def _transposed_sub(m, n, dx, dy, kappa, half):
+        swap = {"south": "west", "north": "east", "west": "south", "east": "north"}
+        return make((n, m, dy, dx, kappa, "DDDD", tuple(swap[h] for h in half)))
+
+    @pytest.mark.parametrize("m,n,kappa,half", [(255, 127, -3.0, ("south",)),
+                                                (141, 63, 0.0, ("south", "north")),
+                                                (255, 1500, 0.0, ()), (141, 1100, -10.0, ()),
+                                                (1023, 2500, 2.0, ())])
+    def test_against_oracle(self, m, n, kappa, half, rng):
+        h = 1.0 / max(m, n)
+        sub = make((m, n, h, 0.5 * h, kappa, "DDDD", half))
+        pl = rectsolver.plan_rect(sub)
+        assert pl.transform_axis == "x"
+        f = rng.uniform(-1, 1, m * n)
+        p = rectsolver.solve_rect(pl, f).values
+        st = self._transposed_sub(m, n, h, 0.5 * h, kappa, half)
+        ref = O.solve(O.plan(st), f.reshape(m, n).T.ravel()).reshape(n, m).T.ravel()
+        assert rel(p, ref) < 1e-12
+
+    def test_c4_arm_residual_batched(self, rng):
+        """c4 south/north arm shape (4095 x 16383, h = 1/4095) next to a west/east
+        arm shape in one batched call: A p = f to rounding on the GPU stencil."""
+        N = 4095
+        h = 1.0 / N
+        subs = [make((16383, N, h, h, 0.0, "DDDD", ()), 0), make((N, 16383, h, h, 0.0, "DDDD", ()), 1)]
+        plans = [rectsolver.plan_rect(s) for s in subs]
+        assert [p.transform_axis for p in plans] == ["y", "x"]
+        f = [dev(rng.uniform(-1, 1, s.size)) for s in subs]
+        outs = rectsolver.solve_rect_batched(plans, f)
+        for s, fi, p in zip(subs, f, outs):
+            r = rectsolver.apply_rect_operator(s, p) - fi
+            assert (torch.linalg.norm(r) / torch.linalg.norm(fi)).item() < 1e-10
+        # alone vs batched: other block-carry partition, rounding-level difference only
+        p1 = rectsolver.solve_rect(plans[1], f[1]).values
+        assert (torch.linalg.norm(p1 - outs[1]) / torch.linalg.norm(p1)).item() < 1e-12
+
+    def test_cross_with_transposed_arms(self):
+        """Cross whose south/north arms (127 x 1100) take the x transform, against
+        the oracle's ddm_solve (which transforms them along y, like the reference)."""
+        comp = configs.cross_composite(127, arm=1100, kappa=-10.0)
+        f, exact = configs.manufactured_rhs(comp, "sin")
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+        ofields, orep = O.ddm_solve(comp, f, m=50, tol=1e-10)
+        assert rep.iterations == orep.iterations
+        num = sum(float(np.sum((fields[s].values - ofields[s]) ** 2)) for s in ofields)
+        den = sum(float(np.sum(ofields[s] ** 2)) for s in ofields)
+        assert (num / den) ** 0.5 < 1e-10
+
+    @pytest.mark.slow
+    def test_c4_golden(self):
+        """c4: elongated cross, 285M points, kappa = 0, manufactured sin x sin:
+        iteration count, sampled values and norms against the reference run,
+        and the reference's observed error against the exact solution."""
+        g = load_golden("c4")
+        comp, f, exact, _ = configs.build_cross_case("c4")
+        fd = {k: dev(v) for k, v in f.items()}
+        del f
+        fields, rep = ddm.ddm_solve(comp, fd, krylov.GmresConfig(m=50, tol=1e-10))
+        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        for sid in range(5):
+            v = fields[sid].values
+            idx = torch.as_tensor(g[f"idx_{sid}"], device="cuda")
+            assert rel(v[idx].cpu().numpy(), g[f"val_{sid}"]) < 1e-10
+            assert torch.linalg.norm(v).item() == pytest.approx(float(g[f"norm_{sid}"]), rel=1e-10)
+        num = sum(float(torch.sum((fields[s].values - dev(exact[s])) ** 2)) for s in exact)
+        den = sum(float(np.sum(exact[s] ** 2)) for s in exact)
+        assert (num / den) ** 0.5 == pytest.approx(float(g["rel_l2_exact"]), rel=1e-4)
+
+
 class TestDistDriver:
     def test_native_backend_single_rank(self, golden_small):
         """dist_ddm_solve with the GPU backend and no process group (one rank owns
