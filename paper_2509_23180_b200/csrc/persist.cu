@@ -548,9 +548,11 @@ struct PersistA {
 
 bool launch_persist_ws(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 bool launch_rsolve(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
+bool launch_rsws(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
     if (launch_persist_ws(jobs, s, ws)) return true;
+    if (launch_rsws(jobs, s, ws)) return true;
     if (launch_rsolve(jobs, s, ws)) return true;
     const int n = jobs[0].p.n;
     int lg = 0;
