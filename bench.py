@@ -182,6 +182,49 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def full_solve(dev, name="c2", reps=3):
+    """Algorithm 1 end to end on a BASELINE cross config (c2: 5 x 2047^2, 21M
+    points, manufactured solution, GMRES(50) to 1e-10): ddm_solve with the RHS
+    resident on the device (median of `reps` after a warm-up), and once with
+    host numpy RHS in and numpy solution out (H2D/D2H inside the call)."""
+    import torch
+
+    from paper_2509_23180_b200 import configs, ddm, krylov
+
+    comp, f, exact, meta = configs.build_cross_case(name)
+    fd = {k: torch.as_tensor(v, device=dev) for k, v in f.items()}
+    cfg = krylov.GmresConfig(m=50, tol=1e-10)
+    t0 = time.perf_counter()
+    fields, rep = ddm.ddm_solve(comp, fd, cfg)   # first call: plan tables built here
+    torch.cuda.synchronize()
+    cold = time.perf_counter() - t0
+    times = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fields, rep = ddm.ddm_solve(comp, fd, cfg)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    wall = statistics.median(times)
+    err = configs.rel_l2(fields, exact)
+    t0 = time.perf_counter()
+    hfields, hrep = ddm.ddm_solve(comp, f, cfg)
+    host_wall = time.perf_counter() - t0
+    out = {"config": name, "points": meta["points"], "iterations": rep.iterations,
+           "restarts": rep.restarts, "wall_s": wall, "value": meta["points"] / wall,
+           "unit": "grid_points/s", "first_call_wall_s": cold,
+           "host_io_wall_s": host_wall, "host_io_value": meta["points"] / host_wall,
+           "gmres_s_per_iteration": rep.wall_time / max(rep.iterations, 1),
+           "rel_l2_vs_exact": err, "timing": "device-resident RHS, median of 3 after a warm-up call"}
+    gpath = os.path.join(ROOT, "tests", "golden", f"{name}.npz")
+    if os.path.exists(gpath):
+        g = np.load(gpath)
+        out["reference"] = {"iterations": int(g["iterations"]), "wall_s": float(g["wall"]),
+                            "rel_l2_vs_exact": float(g["rel_l2_exact"]),
+                            "where": "reference fftddm on the build container's CPU (golden run)"}
+    return out
+
+
 def run_gpu(args, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -290,6 +333,8 @@ def run_gpu(args, world, rank, local):
     e2e_value = POINTS * world / (e_ms * 1e-3)
     io_bytes = sum(r.nbytes for r in rhs)
 
+    solve = None if args.no_solve else full_solve(dev)
+
     # kernels of ours per batched apply: one persistent cooperative launch on the
     # FFT path (n + 1 = 2^p), pass1 + carry + pass2 on the dense path
     launches_per_step = 1 if plans[0].info()["transform"] == "fft" else 3
@@ -326,7 +371,8 @@ def run_gpu(args, world, rank, local):
                         "pipeline": "2 buffer sets; H2D, solve, D2H on 3 streams (D2H of step i overlaps H2D of i+1)"},
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk.summary(),
-                "check": {"rel_residual_Ap_minus_f": resid}}
+                "check": {"rel_residual_Ap_minus_f": resid},
+                "full_solve": solve}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -340,6 +386,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-solve", action="store_true", help="skip the full-solve (c2) leg")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
