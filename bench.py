@@ -211,7 +211,7 @@ def full_solve(dev, name="c2", reps=3):
     hfields, hrep = ddm.ddm_solve(comp, f, cfg)
     host_wall = time.perf_counter() - t0
     out = {"config": name, "points": meta["points"], "iterations": rep.iterations,
-           "restarts": rep.restarts, "wall_s": wall, "value": meta["points"] / wall,
+           "wall_s": wall, "value": meta["points"] / wall,
            "unit": "grid_points/s", "first_call_wall_s": cold,
            "host_io_wall_s": host_wall, "host_io_value": meta["points"] / host_wall,
            "gmres_s_per_iteration": rep.wall_time / max(rep.iterations, 1),

@@ -48,6 +48,25 @@ void dfree(void *p) {
     if (p) cudaFreeAsync(p, 0);
 }
 
+// FD_HOST_TIMING=1: host-side phase times of the drivers on stderr (diagnostics)
+struct HostTimer {
+    const char *name;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    bool on;
+    explicit HostTimer(const char *n) : name(n) {
+        static const bool env = getenv("FD_HOST_TIMING") != nullptr;
+        on = env;
+    }
+    void mark(const char *what, cudaStream_t s = 0, bool sync = true) {
+        if (!on) return;
+        if (sync) cudaStreamSynchronize(s);
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[fd host] %s %s %.3f ms\n", name, what,
+                std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
+
 static thread_local std::string g_last_error;
 void set_error(const std::string &msg) { g_last_error = msg; }
 
@@ -615,6 +634,7 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, doub
 int fd_schur_destroy(fd_schur op) {
     FD_API_BEGIN
     if (op) {
+        HostTimer ht("schur_destroy");
         cudaSetDevice(op->device);
         cudaDeviceSynchronize();
         for (void *a : op->allocs) dfree(a);
@@ -622,6 +642,7 @@ int fd_schur_destroy(fd_schur op) {
         if (op->sc.cap) free_scratch(op->sc);
         if (op->arn_host) cudaFreeHost(op->arn_host);
         delete op;
+        ht.mark("done", 0, false);
     }
     FD_API_END
 }
@@ -674,6 +695,7 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     if (!op || !f_center || !p_center || !rep) FD_FAIL(FD_ERR_VALIDATION, "null argument");
     if (m < 1 || !(tol > 0) || max_restarts < 1) FD_FAIL(FD_ERR_VALIDATION, "bad GMRES config");
     cudaStream_t s = S(stream);
+    HostTimer ht("ddm_solve");
     const size_t nnb = op->nb.size();
     const long long Nc = (long long)op->center->m * op->center->n;
     // pre-solves q_i = A_i^{-1} f_i into the caller's output fields (ddm.py:249-250)
@@ -693,8 +715,10 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     double *rhs = nullptr;
     FD_CUDA(cudaMallocAsync(&rhs, sizeof(double) * Nc, s));
     center_solve(op, fp, rhs, 1.0, 0.0, nullptr, s);
+    ht.mark("presolves+rhs", s);
     std::vector<double> hist;
     int st = gmres_precond(op, rhs, p_center, 1, m, tol, max_restarts, hist, rep, s);
+    ht.mark("gmres", s);
     copy_hist(hist, history, hist_cap, rep);
     // true residual ||(A_c - S) x - f'|| (krylov.py:189); rhs buffer reused
     unprecond_apply(op, p_center, rhs, s);
@@ -718,6 +742,7 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
         else
             launch_axpby((long long)q->m * q->n, 1.0, p_nb[i], -1.0, op->nbf[i], p_nb[i], s);
     }
+    ht.mark("residual+backsub", s);
     if (st != FD_OK) {
         std::ostringstream os;
         os << "GMRES did not reach tol=" << tol << " in " << rep->iterations << " iterations";

@@ -19,7 +19,9 @@ from paper_2509_23180_b200 import configs, ddm, krylov  # noqa: E402
 
 
 def main():
-    names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["c0", "c2", "c3"]
+    argv = sys.argv[1:]
+    names = [a for i, a in enumerate(argv) if not a.startswith("--") and not (i and argv[i - 1] == "--reps")]
+    names = names or ["c0", "c2", "c3"]
     reps = 3
     if "--reps" in sys.argv:
         reps = int(sys.argv[sys.argv.index("--reps") + 1])
@@ -40,7 +42,7 @@ def main():
         wall = float(np.median(times))
         out = {"config": name, "points": meta["points"], "iterations": rep.iterations,
                "wall_s": wall, "mpts_per_s": meta["points"] / wall / 1e6,
-               "gmres_wall_s": rep.wall_time, "us_per_iteration": rep.wall_time / max(rep.iterations, 1) * 1e6,
+               "gmres_wall_s": rep.wall_time, "all_s": [round(t, 4) for t in times], "us_per_iteration": rep.wall_time / max(rep.iterations, 1) * 1e6,
                "true_residual": rep.true_residual}
         if exact is not None:
             out["rel_l2_exact"] = configs.rel_l2(fields, exact)
