@@ -97,3 +97,31 @@ def test_errors_map_to_reference_classes():
         _native.check(_native.FD_ERR_VALIDATION)
     with pytest.raises(NotImplementedError):
         _native.check(_native.FD_ERR_UNSUPPORTED)
+
+
+def test_transform_kind(lib):
+    """GPU transform availability per length (drives the axis choice)."""
+    assert [lib.fd_transform_kind(n) for n in (255, 511, 1023, 2047, 4095)] == [1] * 5
+    assert [lib.fd_transform_kind(n) for n in (1, 141, 1000, 1024)] == [0] * 4
+    assert [lib.fd_transform_kind(n) for n in (1025, 1500, 8191, 16383)] == [-1] * 4
+
+
+@pytest.mark.parametrize("m,n,bc,half,axis", [
+    (1023, 1023, "DDDD", (), "y"),          # c1: the reference's choice
+    (16383, 4095, "DDDD", (), "y"),         # c4 west/east arm
+    (4095, 16383, "DDDD", (), "x"),         # c4 south/north arm: no 16384-point transform -> x
+    (255, 127, "DDDD", ("south",), "x"),    # y half-cell -> x, as the reference
+    (9, 31, "IDDD", ("east",), "y"),        # sweep-axis modifiers only
+    (40, 1500, "DDDD", (), "x"),            # n without a GPU length, m with one -> x
+    (1500, 1500, "DDDD", (), "y"),          # neither: the reference's y (plan creation reports it)
+])
+def test_gpu_axis_choice(lib, m, n, bc, half, axis):
+    from paper_2509_23180_b200.rectsolver import _gpu_axis
+    assert _gpu_axis(make((m, n, 1.0 / n, 1.0 / n, 0.0, bc, half))) == axis
+
+
+def test_gpu_axis_unsupported(lib):
+    from paper_2509_23180_b200._native import UnsupportedError
+    from paper_2509_23180_b200.rectsolver import _gpu_axis
+    with pytest.raises(UnsupportedError):
+        _gpu_axis(make((12, 9, 1.0, 1.0, 0.0, "DDDD", ("west", "south"))))
