@@ -24,6 +24,13 @@
 //   its rows have landed.
 #include "rsolve_common.cuh"
 
+// FD_DIAG=1 (build flag) compiles in the per-item trace and the FD_DBG
+// component-skip bits used by the timing studies in DESIGN.md; off by default
+// so the production kernel carries no diagnostic code.
+#ifndef FD_DIAG
+#define FD_DIAG 0
+#endif
+
 namespace fd {
 
 template <int NL>
@@ -56,7 +63,8 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
         }
     };
     auto trace = [&](int role, int item, int which) {   // FD_TRACE=<cta>
-        if (pl.trace && (role >= 8 ? t == 0 : tid == 0) && blockIdx.x == pl.trace_cta && item < 64 && role < 16) {
+        if (FD_DIAG && pl.trace && (role >= 8 ? t == 0 : tid == 0) && blockIdx.x == pl.trace_cta && item < 64 &&
+            role < 16) {
             unsigned long long g;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g)::"memory");
             pl.trace[(role * 64 + item) * 2 + which] = g;
@@ -175,10 +183,10 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                     rsync<T>(pr);
                 }
                 double *base = regd(pr) + so;
-                if (!(pl.dbg & 8))
+                if (!(FD_DIAG && (pl.dbg & 8)))
                 F::run(regc(pr), base, rp > 1 ? base + n : nullptr, al, 0.5 * p.scale, m16, la, scr, t, pr, lane,
                        regd(pr), rp > 1 ? regd(pr) + XR : nullptr,
-                       (pl.trace && (pl.dbg & 4) && blockIdx.x == pl.trace_cta && it < 4)
+                       (FD_DIAG && pl.trace && (pl.dbg & 4) && blockIdx.x == pl.trace_cta && it < 4)
                            ? reinterpret_cast<long long *>(pl.trace) + 2048 + it * 8 : nullptr);
             }
             ppar ^= group_mask(rows);
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 #pragma unroll
             for (int u = 0; u < MPT; ++u) {
                 const int k = tid + u * NT;
-                if (k >= n || ra >= rb || (pl.dbg & 16)) continue;
+                if (k >= n || ra >= rb || (FD_DIAG && (pl.dbg & 16))) continue;
                 double y = ys[u], w = pis[u], f = fss[u], s2 = s2s[u];
                 if (first && part == 0) {
                     ModeRec c;
@@ -224,7 +232,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                     const double W = w * ib;
                     f = fma(y, W, f);
                     s2 = fma(w, W, s2);
-                    if (!(pl.dbg & 2)) og[rr * n] = y;
+                    if (!(FD_DIAG && (pl.dbg & 2))) og[rr * n] = y;
                 };
                 int rr = ra;
                 if (first && ra == 0) {   // block start: y = r, pi = 1, P_i = -l_s pi_i
@@ -473,7 +481,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 #pragma unroll
             for (int u = 0; u < MPT; ++u) {
                 const int k = tid + u * NT;
-                if (k >= n || (pl.dbg & 64)) continue;
+                if (k >= n || (FD_DIAG && (pl.dbg & 64))) continue;
                 if (top) {
                     ModeRec c;
                     c.load(p, k);
@@ -579,7 +587,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 trace(8 + pr, it, 0);
                 double *base = regd(pr) + so;
                 double *XA = regd(pr), *XB = regd(pr) + XR;
-                if (!(pl.dbg & 32))
+                if (!(FD_DIAG && (pl.dbg & 32)))
                 F::run(regc(pr), base, rp > 1 ? base + n : nullptr, al, 0.5 * p.scale, m16, la, scr, t, pr, lane,
                        XA, rp > 1 ? XB : nullptr);
                 rsync<T>(pr);
@@ -602,7 +610,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int q = q0 + u * T;
-                        if (q < tot && !(pl.dbg & 1)) o0[q] = q0p ? fma(be_, w8[u], al_ * v[u]) : al_ * v[u];
+                        if (q < tot && !(FD_DIAG && (pl.dbg & 1))) o0[q] = q0p ? fma(be_, w8[u], al_ * v[u]) : al_ * v[u];
                     }
                 }
                 rsync<T>(pr);   // region free
