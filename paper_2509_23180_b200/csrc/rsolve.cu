@@ -155,9 +155,10 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 
     // ===================== phase 1: DST + local forward elimination ===================
     {
+        constexpr bool kReload = MPT >= 4;
         double ys[MPT], pis[MPT], fss[MPT], s2s[MPT], ccs[MPT];
-        double cl[MPT], cib[MPT], cbl[MPT], cibl[MPT];
-        int clen[MPT];
+        double cl[kReload ? 1 : MPT], cib[kReload ? 1 : MPT], cibl[kReload ? 1 : MPT];
+        int clen[kReload ? 1 : MPT];
         Tail tail{0.0, -1};
         if (nitems > 0) {
             int si, g0, rows;
@@ -211,17 +212,32 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 const int k = tid + u * NT;
                 if (k >= n || ra >= rb || (FD_DIAG && (pl.dbg & 16))) continue;
                 double y = ys[u], w = pis[u], f = fss[u], s2 = s2s[u];
-                if (first && part == 0) {
-                    ModeRec c;
-                    c.load(p, k);
-                    cl[u] = c.l_inf;
-                    cib[u] = c.ib_inf;
-                    cbl[u] = c.b_last;
-                    cibl[u] = 1.0 / c.b_last;
-                    clen[u] = c.len;
+                int len;
+                double l_inf, ib_inf, ibm;
+                if constexpr (kReload) {
+                    // many modes per thread: the per-mode constants are re-read from
+                    // the (L2-resident) mode records each part instead of living in
+                    // registers across the transforms
+                    const double2 *rec = reinterpret_cast<const double2 *>(p.mode) + 4 * k;
+                    const double2 a = __ldg(rec), d = __ldg(rec + 3);
+                    l_inf = a.x;
+                    ib_inf = a.y;
+                    len = int(__double_as_longlong(d.y));
+                    ibm = (g0 + rb - 1 >= p.m - 1) ? 1.0 / mode_blast(p, k) : ib_inf;
+                } else {
+                    if (first && part == 0) {
+                        ModeRec c;
+                        c.load(p, k);
+                        cl[u] = c.l_inf;
+                        cib[u] = c.ib_inf;
+                        cibl[u] = 1.0 / c.b_last;
+                        clen[u] = c.len;
+                    }
+                    len = clen[u];
+                    l_inf = cl[u];
+                    ib_inf = cib[u];
+                    ibm = cibl[u];
                 }
-                const int len = clen[u];
-                const double l_inf = cl[u], ib_inf = cib[u], ibm = cibl[u];
                 const int xk = xi(k);
                 double *og = outg + k;
                 // one row of the local forward elimination (rectsolver.py:86) with
@@ -436,9 +452,10 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 
     // ===================== phase 3: back-substitution + inverse DST ===================
     {
+        constexpr bool kReload = MPT >= 4;
         double xs[MPT], yins[MPT], pcs[MPT];
-        double cib_inf[MPT], cinv[MPT], cibl[MPT];
-        int clen[MPT];
+        double cib_inf[kReload ? 1 : MPT], cinv[kReload ? 1 : MPT], cibl[kReload ? 1 : MPT];
+        int clen[kReload ? 1 : MPT];
         Tail tail{0.0, -1};
         if (nitems > 0) {
             int si, g0, rows;
@@ -483,12 +500,14 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 const int k = tid + u * NT;
                 if (k >= n || (FD_DIAG && (pl.dbg & 64))) continue;
                 if (top) {
-                    ModeRec c;
-                    c.load(p, k);
-                    cib_inf[u] = c.ib_inf;
-                    cinv[u] = c.inv_nl;
-                    cibl[u] = 1.0 / c.b_last;
-                    clen[u] = c.len;
+                    if constexpr (!kReload) {
+                        ModeRec c;
+                        c.load(p, k);
+                        cib_inf[u] = c.ib_inf;
+                        cinv[u] = c.inv_nl;
+                        cibl[u] = 1.0 / c.b_last;
+                        clen[u] = c.len;
+                    }
                     const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
                     const size_t bs = size_t(kCarryVals) * n;
                     xs[u] = has_next ? __ldcg(cb + bs + 6 * n) : 0.0;
@@ -497,8 +516,21 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 }
                 double x = xs[u], Pc = pcs[u];
                 const double yin = yins[u];
-                const int len = clen[u];
-                const double ib_inf = cib_inf[u];
+                int len;
+                double ib_inf, inl_, iblast;
+                if constexpr (kReload) {   // see phase 1
+                    const double2 *rec = reinterpret_cast<const double2 *>(p.mode) + 4 * k;
+                    const double2 a = __ldg(rec), b = __ldg(rec + 1), d = __ldg(rec + 3);
+                    ib_inf = a.y;
+                    inl_ = b.y;
+                    len = int(__double_as_longlong(d.y));
+                    iblast = (g0 + rows - 1 >= p.m - 1) ? 1.0 / mode_blast(p, k) : ib_inf;
+                } else {
+                    len = clen[u];
+                    ib_inf = cib_inf[u];
+                    inl_ = cinv[u];
+                    iblast = cibl[u];
+                }
                 if (k < p.kt) {
                     const double *tb = lts + k;
 #pragma unroll 4
@@ -515,7 +547,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 } else if (g0 < len && g0 + rows <= p.ecap) {
                     // transient rows: reference factors from the row-major tables,
                     // 8 rows of loads ahead of their sweep
-                    const double ib_m = cibl[u], inl = cinv[u], nio = -1.0 / off;
+                    const double ib_m = iblast, inl = inl_, nio = -1.0 / off;
                     const int mlast = p.m - 1;
 #pragma unroll 1
                     for (int r1 = rows; r1 > 0; r1 -= 8) {   // rows r1 - 1, r1 - 2, ... descending
@@ -546,7 +578,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 #pragma unroll 1
                     for (int rr = rows - 1; rr >= 0; --rr) {   // beyond the tables (rare)
                         double l, ib, bm1;
-                        factors_slow(p, k, g0 + rr, len, 0.0, cib_inf[u], cibl[u], mode_binf(p, k), &l, &ib, &bm1);
+                        factors_slow(p, k, g0 + rr, len, 0.0, ib_inf, iblast, mode_binf(p, k), &l, &ib, &bm1);
                         double *yp = yrow(rr) + k;
                         double y = *yp;
                         if (has_in) {
@@ -557,7 +589,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                         *yp = x;
                     }
                 } else {
-                    const double ib_m = cibl[u], inl = cinv[u];
+                    const double ib_m = iblast, inl = inl_;
                     const int mlast = p.m - 1;
 #pragma unroll 4
                     for (int rr = rows - 1; rr >= 0; --rr) {
