@@ -649,7 +649,8 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 trace(4, it, 1);
             }
             if (more && t == 0) tail = issue_pair(pl.job[segs[si2].job].out, g2, rows2, pl.job[segs[si2].job].p.m);
-            __syncthreads();   // idle pairs wait here, not on the mbarriers
+            // no CTA barrier here: the next item's sweep starts only after every
+            // pair's refill (issued after that pair's stores) has landed
             trace(3, it, 1);
         }
     }
