@@ -54,12 +54,14 @@ struct HostTimer {
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     bool on;
     explicit HostTimer(const char *n) : name(n) {
-        static const bool env = getenv("FD_HOST_TIMING") != nullptr;
-        on = env;
+        static const int env = getenv("FD_HOST_TIMING") ? atoi(getenv("FD_HOST_TIMING")) : 0;
+        on = env != 0;
+        nosync = env == 2;   // 2: host clock only, no stream synchronisation
     }
+    bool nosync = false;
     void mark(const char *what, cudaStream_t s = 0, bool sync = true) {
         if (!on) return;
-        if (sync) cudaStreamSynchronize(s);
+        if (sync && !nosync) cudaStreamSynchronize(s);
         const auto t = std::chrono::steady_clock::now();
         fprintf(stderr, "[fd host] %s %s %.3f ms\n", name, what,
                 std::chrono::duration<double, std::milli>(t - t0).count());
@@ -152,7 +154,8 @@ struct fd_schur_s {
     double mod_s, mod_n;
     std::vector<fd::Plan *> nb;
     std::vector<fd::Coupling> to_c, from_c;   // R_ci, R_ic per neighbour
-    std::vector<double *> nbf;                // neighbour work fields
+    std::vector<double *> nbf;                // neighbour work fields (solve outputs)
+    std::vector<double *> nbin;               // neighbour inputs: zero except the interface line
     double *tmp = nullptr, *tmp2 = nullptr;   // centre-sized work vectors
     // GMRES workspace
     double *V = nullptr;
@@ -242,12 +245,13 @@ static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream
     std::vector<SolveJob> jobs;
     for (size_t i = 0; i < nnb; ++i) {
         const Plan *q = op->nb[i];
-        FD_CUDA(cudaMemsetAsync(op->nbf[i], 0, sizeof(double) * q->m * q->n, s));
         const Coupling &c = op->from_c[i];
-        launch_scatter(c.len, c.from, c.to, c.c, p, op->nbf[i], 0, s);
-        jobs.push_back(job_of(q, op->nbf[i], op->nbf[i]));
+        launch_scatter(c.len, c.from, c.to, c.c, p, op->nbin[i], 0, s);   // R_ic p into a zero field
+        jobs.push_back(job_of(q, op->nbin[i], op->nbf[i]));
     }
     solve_batch(jobs, s);
+    for (size_t i = 0; i < nnb; ++i)   // back to all zeros for the next apply (no field-sized memset)
+        launch_zero_at(op->from_c[i].len, op->from_c[i].to, op->nbin[i], s);
     const Plan *cp = op->center;
     FD_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * cp->m * cp->n, s));
     for (size_t i = 0; i < nnb; ++i) {
@@ -614,6 +618,8 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, doub
             op->from_c.push_back(Coupling{len, up(from_c_from[i], len), up(fct.data(), len),
                                           from_c_coupling[i], nullptr});
             op->nbf.push_back((double *)dalloc(op, sizeof(double) * q->m * q->n));
+            op->nbin.push_back((double *)dalloc(op, sizeof(double) * q->m * q->n));
+            FD_CUDA(cudaMemset(op->nbin.back(), 0, sizeof(double) * q->m * q->n));
         }
         op->tmp = (double *)dalloc(op, sizeof(double) * Nc);
         op->tmp2 = (double *)dalloc(op, sizeof(double) * Nc);
@@ -696,6 +702,7 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     if (m < 1 || !(tol > 0) || max_restarts < 1) FD_FAIL(FD_ERR_VALIDATION, "bad GMRES config");
     cudaStream_t s = S(stream);
     HostTimer ht("ddm_solve");
+    ht.mark("entry", s, false);
     const size_t nnb = op->nb.size();
     const long long Nc = (long long)op->center->m * op->center->n;
     // pre-solves q_i = A_i^{-1} f_i into the caller's output fields (ddm.py:249-250)
@@ -729,12 +736,12 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     std::vector<SolveJob> jobs;
     for (size_t i = 0; i < nnb; ++i) {
         const Plan *q = op->nb[i];
-        FD_CUDA(cudaMemsetAsync(op->nbf[i], 0, sizeof(double) * q->m * q->n, s));
         const Coupling &c = op->from_c[i];
-        launch_scatter(c.len, c.from, c.to, c.c, p_center, op->nbf[i], 0, s);
-        jobs.push_back(job_of(q, op->nbf[i], op->nbf[i]));
+        launch_scatter(c.len, c.from, c.to, c.c, p_center, op->nbin[i], 0, s);
+        jobs.push_back(job_of(q, op->nbin[i], op->nbf[i]));
     }
     solve_batch(jobs, s);
+    for (size_t i = 0; i < nnb; ++i) launch_zero_at(op->from_c[i].len, op->from_c[i].to, op->nbin[i], s);
     for (size_t i = 0; i < nnb; ++i) {
         const Plan *q = op->nb[i];
         if (q->transposed)

@@ -61,6 +61,16 @@ __global__ void scatter_kernel(int len, const int64_t *__restrict__ from, const 
     }
 }
 
+__global__ void zero_at_kernel(int len, const int64_t *__restrict__ to, double *dst) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < len; t += gridDim.x * blockDim.x) dst[to[t]] = 0.0;
+}
+
+void launch_zero_at(int len, const int64_t *to, double *dst, cudaStream_t s) {
+    if (len <= 0) return;
+    zero_at_kernel<<<(len + 255) / 256, 256, 0, s>>>(len, to, dst);
+    FD_CUDA(cudaGetLastError());
+}
+
 void launch_scatter(int len, const int64_t *from, const int64_t *to, double c, const double *src,
                     double *dst, int accumulate, cudaStream_t s) {
     if (len <= 0) return;
