@@ -303,8 +303,13 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                         step(rr, l, ib);
                     }
                 } else {
+                    if (g0 + rb - 1 < mlast) {
 #pragma unroll 4
-                    for (; rr < rb; ++rr) step(rr, l_inf, (g0 + rr == mlast) ? ibm : ib_inf);
+                        for (; rr < rb; ++rr) step(rr, l_inf, ib_inf);
+                    } else {
+#pragma unroll 1
+                        for (; rr < rb; ++rr) step(rr, l_inf, (g0 + rr == mlast) ? ibm : ib_inf);
+                    }
                 }
                 const double cc = ccs[u];
                 ys[u] = y;
@@ -591,17 +596,28 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 } else {
                     const double ib_m = iblast, inl = inl_;
                     const int mlast = p.m - 1;
+                    if (has_in && g0 + rows - 1 < mlast) {   // interior rows, carry fix-up
 #pragma unroll 4
-                    for (int rr = rows - 1; rr >= 0; --rr) {
-                        double *yp = yrow(rr) + k;
-                        double y = *yp;
-                        if (has_in) {
-                            y = fma(Pc, yin, y);
+                        for (int rr = rows - 1; rr >= 0; --rr) {
+                            double *yp = yrow(rr) + k;
+                            const double y = fma(Pc, yin, *yp);
                             Pc *= inl;
+                            x = __dsub_rn(y, __dmul_rn(off, x)) * ib_inf;   // rectsolver.py:90
+                            *yp = x;
                         }
-                        const double ib = (g0 + rr == mlast) ? ib_m : ib_inf;
-                        x = __dsub_rn(y, __dmul_rn(off, x)) * ib;   // rectsolver.py:90
-                        *yp = x;
+                    } else {
+#pragma unroll 1
+                        for (int rr = rows - 1; rr >= 0; --rr) {
+                            double *yp = yrow(rr) + k;
+                            double y = *yp;
+                            if (has_in) {
+                                y = fma(Pc, yin, y);
+                                Pc *= inl;
+                            }
+                            const double ib = (g0 + rr == mlast) ? ib_m : ib_inf;
+                            x = __dsub_rn(y, __dmul_rn(off, x)) * ib;   // rectsolver.py:90
+                            *yp = x;
+                        }
                     }
                 }
                 xs[u] = x;
@@ -624,25 +640,22 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                        XA, rp > 1 ? XB : nullptr);
                 rsync<T>(pr);
                 trace(8 + pr, it, 1);
-                // epilogue out = alpha x + beta other over the pair's rows (adjacent in
-                // global memory), 8 shared-memory reads in flight per thread
+                // epilogue out = alpha x + beta other, row by row from the padded X
+                // layout; 8 independent loads/stores in flight per thread
                 const double al_ = J.alpha, be_ = J.beta;
-                double *o0 = J.out + size_t(g0 + 2 * pr) * n;
-                const double *q0p = J.other ? J.other + size_t(g0 + 2 * pr) * n : nullptr;
-                const int tot = rp * n;
-#pragma unroll 1
-                for (int q0 = t; q0 < tot; q0 += 8 * T) {
-                    double v[8], w8[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int q = q0 + u * T, h = q >= n;
-                        v[u] = (q < tot) ? XA[h * XR + xi(q - h * n)] : 0.0;
-                        w8[u] = (q < tot && q0p) ? __ldg(q0p + q) : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int q = q0 + u * T;
-                        if (q < tot && !(FD_DIAG && (pl.dbg & 1))) o0[q] = q0p ? fma(be_, w8[u], al_ * v[u]) : al_ * v[u];
+                for (int h = 0; h < rp; ++h) {
+                    const double *Xh = XA + h * XR;
+                    double *oh = J.out + size_t(g0 + 2 * pr + h) * n;
+                    const double *qh = J.other ? J.other + size_t(g0 + 2 * pr + h) * n : nullptr;
+                    if (qh) {
+#pragma unroll 8
+                        for (int q = t; q < n; q += T) oh[q] = fma(be_, __ldg(qh + q), al_ * Xh[xi(q)]);
+                    } else if (al_ == 1.0) {
+#pragma unroll 8
+                        for (int q = t; q < n; q += T) oh[q] = Xh[xi(q)];
+                    } else {
+#pragma unroll 8
+                        for (int q = t; q < n; q += T) oh[q] = al_ * Xh[xi(q)];
                     }
                 }
                 rsync<T>(pr);   // region free

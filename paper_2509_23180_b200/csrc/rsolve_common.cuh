@@ -66,8 +66,10 @@ struct RFft {
             }
             const double a = al[j], b = a - h2;
             const int i1 = j - 1, i2 = N - 1 - j;
+            // a single row is paired with itself (B = A): the two outputs separate
+            // exactly, the second is simply not stored
             v[r].x = fma(a, A[i1], b * A[i2]);
-            v[r].y = HB ? fma(a, B[i1], b * B[i2]) : 0.0;
+            v[r].y = fma(a, B[i1], b * B[i2]);
         }
     }
     __device__ static void first(double2 *buf, double2 (&v)[16], int t, int pr) {
