@@ -432,9 +432,9 @@ struct Fft2 {
 // (j, k); each thread walks its index by k + 1 per j.  MPT modes per thread
 // (n <= 128 MPT), G rows per group share every table load.
 constexpr int kDenseMax = 1024;
-template <int MPT_>
+template <int MPT_, int NT_ = 128>
 struct DenseDstT {
-    static constexpr int NT = 128;
+    static constexpr int NT = NT_;
     static constexpr int G = 8;
     static constexpr int MINB = 2;
     static constexpr int MPT = MPT_;

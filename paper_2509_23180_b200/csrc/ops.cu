@@ -294,7 +294,8 @@ __device__ __forceinline__ void arn_finish(ArnWork a, int nd, const double *bacc
 }
 
 __global__ void __launch_bounds__(kArnThreads) arnoldi_dots_kernel(long long N, int k, const double *__restrict__ V,
-                                                                    const double *__restrict__ w, ArnWork a, int ldg) {
+                                                                    const double *__restrict__ w, ArnWork a, int ldg,
+                                                                    int chunk) {
     __shared__ double sw[kArnChunk], sv[kArnChunk];
     __shared__ double bacc[2 * kMaxArnoldi + 2];
     __shared__ double wred[kArnWarps];
@@ -305,8 +306,8 @@ __global__ void __launch_bounds__(kArnThreads) arnoldi_dots_kernel(long long N, 
 #pragma unroll
     for (int q = 0; q < kArnJPW; ++q) as[q] = ac[q] = 0.0;
     double ww = 0.0;
-    for (long long c0 = (long long)blockIdx.x * kArnChunk; c0 < N; c0 += (long long)gridDim.x * kArnChunk) {
-        const int len = (int)min((long long)kArnChunk, N - c0);
+    for (long long c0 = (long long)blockIdx.x * chunk; c0 < N; c0 += (long long)gridDim.x * chunk) {
+        const int len = (int)min((long long)chunk, N - c0);
         __syncthreads();
         for (int t = threadIdx.x; t < len; t += kArnThreads) {
             const double wv = w[c0 + t];
@@ -406,15 +407,23 @@ __global__ void scale_sqrt_kernel(long long N, const double *__restrict__ x, con
         out[i] = x[i] / s;
 }
 
+// points per staged chunk: the full 2048 for large vectors, smaller for small
+// ones so that at least ~2 CTAs per SM take part (c0: N_c = 19881)
+static int arn_chunk(long long N) {
+    long long c = N / (148 * 2);
+    c = std::max<long long>(256, std::min<long long>(kArnChunk, (c + 31) / 32 * 32));
+    return (int)c;
+}
 static int arn_grid(long long N) {
-    long long g = (N + kArnChunk - 1) / kArnChunk;
+    const long long ch = arn_chunk(N);
+    long long g = (N + ch - 1) / ch;
     return (int)std::min<long long>(std::max<long long>(g, 1), 148LL * 4);
 }
 
 void launch_arnoldi_dots(long long N, int k, const double *V, const double *w, ArnWork a, int ldg,
                          cudaStream_t s) {
     if (k + 1 > kMaxArnoldi) throw Error{FD_ERR_VALIDATION, "arnoldi: restart length above 64"};
-    arnoldi_dots_kernel<<<arn_grid(N), kArnThreads, 0, s>>>(N, k, V, w, a, ldg);
+    arnoldi_dots_kernel<<<arn_grid(N), kArnThreads, 0, s>>>(N, k, V, w, a, ldg, arn_chunk(N));
     FD_CUDA(cudaGetLastError());
 }
 

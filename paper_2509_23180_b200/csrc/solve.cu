@@ -84,10 +84,10 @@ struct InvT<FftDst<LG>> {
 };
 
 // Dense transform of the G-row group in rowbuf (shared) into acc (registers).
-template <int M>
+template <int M, int NT_>
 __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const double *tab,
-                                           double (&acc)[DenseDstT<M>::G][M]) {
-    constexpr int NT = DenseDstT<M>::NT, G = DenseDstT<M>::G;
+                                           double (&acc)[DenseDstT<M, NT_>::G][M]) {
+    constexpr int NT = DenseDstT<M, NT_>::NT, G = DenseDstT<M, NT_>::G;
     const int N2 = 2 * (n + 1);
     int idx[M];
 #pragma unroll
@@ -115,28 +115,29 @@ __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const do
     }
 }
 
-template <int M>
+template <int M, int NT_>
 __device__ __forceinline__ double *dense_tab(double2 *smem) {
-    return reinterpret_cast<double *>(smem) + DenseDstT<M>::G * DenseDstT<M>::NMAX;
+    return reinterpret_cast<double *>(smem) + DenseDstT<M, NT_>::G * DenseDstT<M, NT_>::NMAX;
 }
 
-template <int M>
+template <int M, int NT_>
 __device__ __forceinline__ void stage_tab(double *tab, int n, const PlanDev &p) {
-    for (int q = threadIdx.x; q < 2 * (n + 1); q += DenseDstT<M>::NT) tab[q] = __ldg(p.dense + q);
+    for (int q = threadIdx.x; q < 2 * (n + 1); q += DenseDstT<M, NT_>::NT) tab[q] = __ldg(p.dense + q);
 }
 
-template <int M>
-struct FwdT<DenseDstT<M>> {
+template <int M, int NT_>
+struct FwdT<DenseDstT<M, NT_>> {
     __device__ static void run(const double *in, int rows, int n, double *rowbuf, double2 *smem,
                                const PlanDev &p) {
-        constexpr int NT = DenseDstT<M>::NT, G = DenseDstT<M>::G;
-        double *tab = dense_tab<M>(smem);
-        stage_tab<M>(tab, n, p);
+        constexpr int NT = DenseDstT<M, NT_>::NT, G = DenseDstT<M, NT_>::G;
+        double *tab = dense_tab<M, NT_>(smem);
+        stage_tab<M, NT_>(tab, n, p);
+#pragma unroll 8
         for (int idx = threadIdx.x; idx < G * n; idx += NT)
             rowbuf[idx] = idx < rows * n ? __ldg(in + idx) : 0.0;
         __syncthreads();
         double acc[G][M];
-        dense_rows<M>(rowbuf, n, tab, acc);
+        dense_rows<M, NT_>(rowbuf, n, tab, acc);
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < M; ++u) {
@@ -150,17 +151,17 @@ struct FwdT<DenseDstT<M>> {
     }
 };
 
-template <int M>
-struct InvT<DenseDstT<M>> {
+template <int M, int NT_>
+struct InvT<DenseDstT<M, NT_>> {
     __device__ static void run(double *rowbuf, int rows, int n, double *out, const double *other,
                                double alpha, double beta, double2 *smem, const PlanDev &p) {
-        constexpr int NT = DenseDstT<M>::NT, G = DenseDstT<M>::G;
-        double *tab = dense_tab<M>(smem);
-        stage_tab<M>(tab, n, p);
+        constexpr int NT = DenseDstT<M, NT_>::NT, G = DenseDstT<M, NT_>::G;
+        double *tab = dense_tab<M, NT_>(smem);
+        stage_tab<M, NT_>(tab, n, p);
         for (int idx = rows * n + threadIdx.x; idx < G * n; idx += NT) rowbuf[idx] = 0.0;
         __syncthreads();
         double acc[G][M];
-        dense_rows<M>(rowbuf, n, tab, acc);
+        dense_rows<M, NT_>(rowbuf, n, tab, acc);
 #pragma unroll
         for (int u = 0; u < M; ++u) {
             const int k = threadIdx.x + u * NT;
@@ -183,8 +184,8 @@ template <int LG>
 struct Cfg<FftDst<LG>> {
     static constexpr int MPT = ((1 << (LG - 1)) - 1 + FftDst<LG>::NT - 1) / FftDst<LG>::NT;
 };
-template <int M>
-struct Cfg<DenseDstT<M>> {
+template <int M, int NT_>
+struct Cfg<DenseDstT<M, NT_>> {
     static constexpr int MPT = M;
 };
 
@@ -216,22 +217,29 @@ __global__ void __launch_bounds__(P::NT, P::MINB) pass1_kernel(const __grid_cons
             ModeView mv;
             mv.load(p, k);
             double y = yh[u], w = pi[u], f = fs[u];
+            double lv[P::G], ibv[P::G];   // the group's factors, loaded ahead of the chain
+#pragma unroll
+            for (int rr = 0; rr < P::G; ++rr) {
+                const int i = g0 + rr;
+                const bool ex = rr < rows && i < mv.len;
+                const double *er = p.ex + 4 * size_t(mv.off + i);
+                lv[rr] = ex ? __ldg(er) : mv.l_inf;
+                ibv[rr] = (i == m - 1) ? mv.ib_last : (ex ? __ldg(er + 1) : mv.ib_inf);
+            }
 #pragma unroll
             for (int rr = 0; rr < P::G; ++rr) {
                 if (rr >= rows) break;
                 const int i = g0 + rr;
                 const double r = rowbuf[rr * n + k];
-                const bool ex = i < mv.len;
-                const double *er = p.ex + 4 * size_t(mv.off + i);
                 if (i == s) {
                     y = r;
                     w = 1.0;
                 } else {
-                    const double l = ex ? __ldg(er) : mv.l_inf;
+                    const double l = lv[rr];
                     y = __dsub_rn(r, __dmul_rn(l, y));   // rectsolver.py:86
                     w = -l * w;
                 }
-                const double ib = (i == m - 1) ? mv.ib_last : (ex ? __ldg(er + 1) : mv.ib_inf);
+                const double ib = ibv[rr];
                 f = fma(y, w * ib, f);
                 J.out[size_t(i) * n + k] = y;
             }
@@ -367,19 +375,27 @@ __global__ void __launch_bounds__(P::NT, P::MINB) pass2_kernel(const __grid_cons
             for (int rr = 0; rr < P::G; ++rr)
                 yv[rr] = rr < rows ? J.out[size_t(g0 + rr) * n + k] : 0.0;
             double x = xn[u], pcur = pc[u];
+            double Pv[P::G], bv[P::G];   // the group's factors, loaded ahead of the chain
+#pragma unroll
+            for (int rr = 0; rr < P::G; ++rr) {
+                const int i = g0 + rr;
+                const bool ex = rr < rows && i < mv.len;
+                const double *er = p.ex + 4 * size_t(mv.off + i);
+                Pv[rr] = ex ? __ldg(er + 3) : 0.0;
+                bv[rr] = (i == m - 1) ? mv.b_last : (ex ? __ldg(er + 2) : mv.b_inf);
+            }
 #pragma unroll
             for (int rr = P::G - 1; rr >= 0; --rr) {
                 if (rr >= rows) continue;
                 const int i = g0 + rr;
                 const bool ex = i < mv.len;
-                const double *er = p.ex + 4 * size_t(mv.off + i);
                 double y = yv[rr];
                 if (b > 0) {
-                    const double Pi = ex ? __ldg(er + 3) : pcur;
+                    const double Pi = ex ? Pv[rr] : pcur;
                     y = fma(Pi, yin[u], y);
                     pcur *= mv.inv_nl;
                 }
-                const double bi = (i == m - 1) ? mv.b_last : (ex ? __ldg(er + 2) : mv.b_inf);
+                const double bi = bv[rr];
                 x = __ddiv_rn(__dsub_rn(y, __dmul_rn(off, x)), bi);   // rectsolver.py:90
                 rowbuf[rr * n + k] = x;
             }
@@ -491,10 +507,11 @@ void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
     for (auto &j : jobs)
         if (j.p.n != n) FD_FAIL(FD_ERR_VALIDATION, "launch_solve: mixed transform lengths in one batch");
     if (transform_kind(n) == kDense) {
-        if (n <= 128) run_solve<DenseDstT<1>>(jobs, s);
-        else if (n <= 256) run_solve<DenseDstT<2>>(jobs, s);
-        else if (n <= 512) run_solve<DenseDstT<4>>(jobs, s);
-        else run_solve<DenseDstT<8>>(jobs, s);
+        if (n <= 128) run_solve<DenseDstT<1, 128>>(jobs, s);
+        else if (n <= 160) run_solve<DenseDstT<1, 160>>(jobs, s);
+        else if (n <= 256) run_solve<DenseDstT<1, 256>>(jobs, s);
+        else if (n <= 512) run_solve<DenseDstT<2, 256>>(jobs, s);
+        else run_solve<DenseDstT<4, 256>>(jobs, s);
         return;
     }
     if (jobs[0].ws && launch_persist(jobs, s, *jobs[0].ws)) return;
@@ -513,10 +530,11 @@ void launch_dst_rows(int rows, int n, const double *in, double *out, const doubl
                      const double *dense, cudaStream_t s) {
     if (rows <= 0) return;
     if (transform_kind(n) == kDense) {
-        if (n <= 128) run_dst<DenseDstT<1>>(rows, n, in, out, tw, dense, s);
-        else if (n <= 256) run_dst<DenseDstT<2>>(rows, n, in, out, tw, dense, s);
-        else if (n <= 512) run_dst<DenseDstT<4>>(rows, n, in, out, tw, dense, s);
-        else run_dst<DenseDstT<8>>(rows, n, in, out, tw, dense, s);
+        if (n <= 128) run_dst<DenseDstT<1, 128>>(rows, n, in, out, tw, dense, s);
+        else if (n <= 160) run_dst<DenseDstT<1, 160>>(rows, n, in, out, tw, dense, s);
+        else if (n <= 256) run_dst<DenseDstT<1, 256>>(rows, n, in, out, tw, dense, s);
+        else if (n <= 512) run_dst<DenseDstT<2, 256>>(rows, n, in, out, tw, dense, s);
+        else run_dst<DenseDstT<4, 256>>(rows, n, in, out, tw, dense, s);
         return;
     }
     switch (lg_of(n)) {
