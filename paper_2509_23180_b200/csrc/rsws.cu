@@ -21,10 +21,14 @@
 // -> sweep -> FFT + store (phase 3), handed over with one mbarrier per region
 // and stage.
 //
-// Measured on B200 at c1 (5 x 1023^2, apply time): lockstep 101 us; teams of
-// 256 + 256 threads 136 us (the FFT team alone needs 43 us for phase 1 -- half
-// the warps give half the FFT throughput -- and the 8-warp sweep 64 us);
-// 384 + 128 threads 367 us (8 modes per sweep thread spill).  The lockstep
+// Measured on B200 at c1 (5 x 1023^2, apply time): lockstep 101 us (89 us
+// after this round's register work); teams of 256 + 256 threads 136 us with
+// the long-transient factors read from L2 per row, 122 us with them staged per
+// region by TMA (this file's configuration): the FFT team finishes phase 1 at
+// 44 us, the sweep team at 60 us, and the kernel executes 50 M warp
+// instructions against the lockstep kernel's 34 M (per-pair bookkeeping, two
+// copies of the row loop); 384 + 128 threads 367 us (8 modes per sweep thread
+// spill).  The lockstep
 // kernel's components add up (load 11 + FFT 15 + sweep 13 us in phase 1) but
 // each runs on all 16 warps; with 16 warps per SM (128 registers per thread)
 // there is no spare team to overlap them with.
@@ -36,9 +40,9 @@ template <int NL>
 struct WS {
     static constexpr int N = 1 << NL;
     static constexpr int T = N / 16;       // FFT threads per pair team
-    static constexpr int NF = 384;         // FFT team (12 warps)
+    static constexpr int NF = 256;         // FFT team (8 warps)
     static constexpr int PF = NF / T;      // pair teams
-    static constexpr int NS = 128;         // sweep team (4 warps)
+    static constexpr int NS = 256;         // sweep team (8 warps)
     static constexpr int NT = NF + NS;
     static constexpr int R = 2 * (256 / T);   // shared-memory regions (row pairs in flight)
     static constexpr int MPT = (N - 1 + NS - 1) / NS;
