@@ -62,14 +62,18 @@ class GpuBackend:
     def index(self, idx):
         return self.torch.as_tensor(np.asarray(idx), device=self.dev)
 
+    # message buffers: device tensors for NCCL; host tensors when the process
+    # group is gloo (functional runs without NCCL)
+    host_comm = False
+
     def comm(self, x):
-        return x.contiguous()
+        return x.detach().cpu().contiguous() if self.host_comm else x.contiguous()
 
     def empty_comm(self, n):
-        return self.torch.empty(n, dtype=self.torch.float64, device=self.dev)
+        return self.torch.empty(n, dtype=self.torch.float64, device="cpu" if self.host_comm else self.dev)
 
     def from_comm(self, t):
-        return t
+        return t.to(self.dev) if self.host_comm else t
 
     def gmres(self, op, rhs, cfg):
         from .krylov import gmres
@@ -103,6 +107,8 @@ def dist_ddm_solve(comp, f, gmres_cfg=None, coupled_id=None, backend=None, group
     validate(comp).require()
     cfg = gmres_cfg or krylov.GmresConfig()
     be = backend or GpuBackend()
+    if isinstance(be, GpuBackend) and dist.is_initialized():
+        be.host_comm = dist.get_backend(group) == "gloo"
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     if coupled_id is None:
