@@ -248,6 +248,40 @@ static __device__ __noinline__ void factors_slow(const PlanDev &p, int k, int i,
 }
 
 
+// --- tensor memory (TMEM) as per-thread row storage ------------------------------
+// 512 columns x 128 lanes x 32 bit per SM.  A warp may only touch the 32 lanes
+// of its quarter (warp % 4); tcgen05.ld/st of shape 32x32b move N consecutive
+// 32-bit columns of the thread's own lane.  The solve uses it as private
+// storage for the phase-1 yhat values a thread needs again in phase 3.
+__device__ __forceinline__ void tmem_alloc512(uint32_t *dst) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc512(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// two doubles -> 4 columns of this thread's lane (warp-collective)
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, double a, double b) {
+    const unsigned long long ua = __double_as_longlong(a), ub = __double_as_longlong(b);
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+                 "r"(uint32_t(ua)), "r"(uint32_t(ua >> 32)), "r"(uint32_t(ub)), "r"(uint32_t(ub >> 32))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, double &a, double &b) {
+    uint32_t r0, r1, r2, r3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(taddr)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    a = __longlong_as_double((long long)(((unsigned long long)r1 << 32) | r0));
+    b = __longlong_as_double((long long)(((unsigned long long)r3 << 32) | r2));
+}
+
 // Phase 2 of the persistent solves: block carries (see rsolve.cu).  All NT
 // threads of the CTA; the first cap_bytes of shared memory are scratch.
 template <int NT>
