@@ -546,12 +546,10 @@ struct PersistA {
     static const void *fn() { return (const void *)persist_kernel<LG>; }
 };
 
-bool launch_persist_ws(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 bool launch_rsolve(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 bool launch_rsws(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
-    if (launch_persist_ws(jobs, s, ws)) return true;
     if (launch_rsws(jobs, s, ws)) return true;
     if (launch_rsolve(jobs, s, ws)) return true;
     const int n = jobs[0].p.n;
