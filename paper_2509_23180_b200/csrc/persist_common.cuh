@@ -1,5 +1,5 @@
-// Shared pieces of the persistent fused-solve kernels (persist.cu,
-// persist_ws.cu): job/segment descriptors, TMA bulk-copy + mbarrier helpers,
+// Shared pieces of the persistent fused-solve kernels (rsolve.cu, rsws.cu,
+// persist.cu): job/segment descriptors, TMA bulk-copy + mbarrier helpers,
 // per-mode factor access, and the host-side cooperative launcher.
 #pragma once
 #include <cooperative_groups.h>
