@@ -48,6 +48,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fvisibility=hidden",
               "-I", os.path.join(os.path.dirname(HERE), "include")] + ARCH
+    if os.environ.get("FD_DIAG_BUILD"):   # trace / component-skip diagnostics (tools/dbg_sweep.sh)
+        common += ["-DFD_DIAG=1"]
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
