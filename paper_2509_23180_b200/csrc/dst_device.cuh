@@ -435,7 +435,7 @@ constexpr int kDenseMax = 1024;
 template <int MPT_, int NT_ = 128>
 struct DenseDstT {
     static constexpr int NT = NT_;
-    static constexpr int G = 8;
+    static constexpr int G = NT_ <= 160 ? 4 : 8;   // small n: fewer rows per CTA, more CTAs
     static constexpr int MINB = 2;
     static constexpr int MPT = MPT_;
     static constexpr int NMAX = NT * MPT_;

@@ -433,7 +433,8 @@ int transform_kind(int n) {
 int rows_per_block(int n) {
     const int N = n + 1;
     if (transform_kind(n) == kFFT) return N >= 4096 ? 8 : 16;
-    return DenseDstT<1>::G;   // one group per carry block: more CTAs for the small dense solves
+    // one group per carry block: more CTAs for the small dense solves
+    return n <= 160 ? DenseDstT<1, 160>::G : DenseDstT<1, 256>::G;
 }
 
 template <class P>
