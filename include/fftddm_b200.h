@@ -69,9 +69,17 @@ int fd_plan_create(fd_plan *out, int m, int n, double dx, double dy, double kapp
 int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double kappa,
                         double mod_west, double mod_east, double mod_south, double mod_north,
                         int transform_axis, int device);
+/* General form: transform_pair 0 = DD (sine basis, DST-I), 1 = NN (shifted
+ * cosine basis, DCT-II/III; transforms.py:32-33,83-98,106-134).  A DD axis
+ * needs ghost-node ends; an NN axis's Neumann ends belong to its basis.  NN
+ * runs on the dense periodic-table transform (n <= 1024). */
+int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double kappa,
+                      double mod_west, double mod_east, double mod_south, double mod_north,
+                      int transform_axis, int transform_pair, int device);
 /* GPU transform available for length n: 1 = FFT (n+1 = 2^p, 256..4096),
- * 0 = dense (n <= 1024), -1 = none. */
+ * 0 = dense (n <= 1024), -1 = none.  DD pair; fd_transform_kind_pair for NN. */
 int fd_transform_kind(int n);
+int fd_transform_kind_pair(int n, int pair);
 int fd_plan_destroy(fd_plan plan);
 /* rows per carry block, explicit factor rows, transform kind (0 dense, 1 fft) */
 int fd_plan_info(fd_plan plan, int *block_rows, long long *explicit_rows, int *transform);

@@ -5,9 +5,9 @@ Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 `paper_2509_23180_b200` never imports it and has no CPU fallback.
 
 What it is: a numpy restatement of the reference `fftddm` hot path for the
-configurations the GPU path supports (DD transform axis along y, any
-per-end diagonal modification on the sweep axis), written from the
-reference's algorithm description.  Each function cites the reference
+configurations the GPU path supports (DD or NN transform axis, along y or --
+with the field transposed -- along x, any per-end diagonal modification on
+the sweep axis), written from the reference's algorithm description.  Each function cites the reference
 file:line it follows (paths relative to /root/reference/pkg/src/fftddm/).
 It uses the same numpy primitives as the reference (numpy's pocketfft for
 the DST-I, numpy BLAS for dots), so its timing stands in for the reference
@@ -38,6 +38,53 @@ def eigenvalues_dd(n, delta_t, delta_o, kappa=0.0):
     """lambda_j = -2(dt+do) + 2 dt cos(j pi/(n+1)) + kappa   (transforms.py:26-31,38)."""
     j = np.arange(1, n + 1, dtype=float)
     return -2.0 * (delta_t + delta_o) + 2.0 * delta_t * np.cos(j * np.pi / (n + 1)) + kappa
+
+
+def eigenvalues(bc, n, delta_t, delta_o, kappa=0.0):
+    """DD: cos(j pi/(n+1)); NN: cos((j-1) pi/n)   (transforms.py:26-38)."""
+    if bc == "DD":
+        return eigenvalues_dd(n, delta_t, delta_o, kappa)
+    if bc != "NN":
+        raise NotImplementedError("oracle covers the DD and NN pairs")
+    j = np.arange(1, n + 1, dtype=float)
+    return -2.0 * (delta_t + delta_o) + 2.0 * delta_t * np.cos((j - 1) * np.pi / n) + kappa
+
+
+def dct2(v):
+    """sum_k v_k cos(pi j (2k+1)/(2n)) through the even extension of length 2n
+    and one complex FFT, phase-shifted                  (transforms.py:83-89)."""
+    n = v.shape[-1]
+    ext = np.concatenate([v, v[..., ::-1]], axis=-1)
+    spec = np.fft.fft(ext, axis=-1)[..., :n]
+    return 0.5 * (np.exp(-0.5j * np.pi * np.arange(n) / n) * spec).real
+
+
+def dct3(a):
+    """sum_j a_j cos(pi j (2k+1)/(2n)) through one length-2n inverse FFT
+    (transforms.py:92-97)."""
+    n = a.shape[-1]
+    z = np.zeros(a.shape[:-1] + (2 * n,), dtype=complex)
+    z[..., :n] = a * np.exp(0.5j * np.pi * np.arange(n) / n)
+    return 2 * n * np.fft.ifft(z, axis=-1).real[..., :n]
+
+
+def nn_scale(n):
+    """sqrt(1/n) for the constant mode, sqrt(2/n) otherwise   (transforms.py:100-103)."""
+    s = np.full(n, math.sqrt(2.0 / n))
+    s[0] = math.sqrt(1.0 / n)
+    return s
+
+
+def apply_q(bc, v):
+    """Q v along the last axis (transforms.py:106-113)."""
+    v = np.asarray(v, dtype=float)
+    return apply_q_dd(v) if bc == "DD" else dct3(nn_scale(v.shape[-1]) * v)
+
+
+def apply_qt(bc, v):
+    """Q^T v along the last axis (transforms.py:129-136)."""
+    v = np.asarray(v, dtype=float)
+    return apply_q_dd(v) if bc == "DD" else nn_scale(v.shape[-1]) * dct2(v)
 
 
 def dst1(v):
@@ -103,31 +150,56 @@ class OraclePlan:
     beta: np.ndarray
     lower: np.ndarray
     off: float
+    axis: str = "y"
+    bc: str = "DD"
 
 
-def plan(sub):
-    """plan_rect, DD-transform-along-y branch (rectsolver.py:94-135,153-163)."""
-    if sub.axis_pair("y") != "DD" or sub.end_modifier("south") or sub.end_modifier("north"):
-        raise NotImplementedError("oracle covers the DD-along-y transform only")
-    if sub.axis_pair("x") == "PP":
+def transformable(sub, axis):
+    """Pure form: NN, or DD with ghost-node ends   (rectsolver.py:24-29)."""
+    pair = sub.axis_pair(axis)
+    if pair == "NN":
+        return True
+    lo, hi = ("west", "east") if axis == "x" else ("south", "north")
+    return pair == "DD" and sub.end_modifier(lo) == 0.0 and sub.end_modifier(hi) == 0.0
+
+
+def plan(sub, axis=None):
+    """plan_rect for DD/NN transform axes (rectsolver.py:94-135,153-163): axis y
+    when transformable, else x (the field is transposed, rectsolver.py:198-199);
+    `axis` forces the choice."""
+    if axis is None:
+        axis = "y" if transformable(sub, "y") else "x"
+    if not transformable(sub, axis):
+        raise NotImplementedError(f"axis {axis} is not transformable")
+    if axis == "y":
+        nt, ms, dt, ds, lo, hi = sub.n, sub.m, sub.delta_y, sub.delta_x, "west", "east"
+    else:
+        nt, ms, dt, ds, lo, hi = sub.m, sub.n, sub.delta_x, sub.delta_y, "south", "north"
+    bc = sub.axis_pair(axis)
+    if sub.axis_pair("x" if axis == "y" else "y") == "PP":
         raise NotImplementedError("oracle covers non-periodic sweep axes only")
-    lam = eigenvalues_dd(sub.n, sub.delta_y, sub.delta_x, sub.kappa)
-    diag = np.tile(lam, (sub.m, 1))
-    diag[0] += sub.end_modifier("west")
-    diag[-1] += sub.end_modifier("east")
-    tol = PIVOT_RTOL * max(np.abs(lam).max(), sub.delta_x)
-    beta, lower, bad = factor_tridiag(diag, sub.delta_x, tol)
+    lam = eigenvalues(bc, nt, dt, ds, sub.kappa)
+    diag = np.tile(lam, (ms, 1))
+    diag[0] += sub.end_modifier(lo)
+    diag[-1] += sub.end_modifier(hi)
+    tol = PIVOT_RTOL * max(np.abs(lam).max(), ds)
+    beta, lower, bad = factor_tridiag(diag, ds, tol)
     if np.any(bad):
         raise SingularOracleError(f"singular modes {np.nonzero(bad)[0].tolist()}")
-    return OraclePlan(sub=sub, beta=beta, lower=lower, off=sub.delta_x)
+    return OraclePlan(sub=sub, beta=beta, lower=lower, off=ds, axis=axis, bc=bc)
 
 
 def solve(pl: OraclePlan, f):
-    """Q^T along y -> per-mode tridiagonal along x -> Q   (rectsolver.py:183-213)."""
+    """Q^T along the transform axis -> per-mode tridiagonal -> Q   (rectsolver.py:183-213)."""
     grid = np.asarray(f, dtype=float).reshape(pl.sub.m, pl.sub.n)
-    fhat = apply_q_dd(grid)
+    if pl.axis == "x":
+        grid = grid.T
+    fhat = apply_qt(pl.bc, grid)
     phat = tridiag_solve(pl.beta, pl.lower, pl.off, fhat)
-    return apply_q_dd(phat).reshape(-1)
+    out = apply_q(pl.bc, phat)
+    if pl.axis == "x":
+        out = out.T
+    return np.ascontiguousarray(out).reshape(-1)
 
 
 def apply_operator(sub, v):

@@ -149,6 +149,33 @@ def build_cross_case(name: str, api=None, N: int | None = None):
     return comp, f, exact, meta
 
 
+def reference_cross(k_n: int, L: float = 1.0 / 7.0, kappa: float = 0.0, api=None):
+    """The reference package's own five-rectangle test cross (its bench.py
+    build_cross: side L, k_n nodes per L, h = L/k_n), restated on the geometry
+    API: a 2L x 4L centre with interfaces on all sides; west/east arms with
+    Neumann flanks (south/north) and a half-cell Dirichlet far end; south/north
+    arms with Neumann flanks (west/east) and a half-cell Dirichlet far end.  The
+    arms' transform axes are NN pairs (y for west/east, x for south/north)."""
+    api = api or default_api()
+    D, N, I = api.BoundaryKind.DIRICHLET, api.BoundaryKind.NEUMANN, api.BoundaryKind.INTERFACE
+    h, k = L / k_n, k_n
+
+    def rect(sid, origin, m, n, bc, half=()):
+        return api.RectSubdomain(id=sid, origin=origin, m=m, n=n, dx=h, dy=h, edge_bc=bc, kappa=kappa,
+                                 half_cell_dirichlet=frozenset(half))
+
+    c = rect(CENTER, (L, 2 * L), 2 * k, 4 * k, {"west": I, "east": I, "south": I, "north": I})
+    w = rect(WEST, (0.0, 2 * L), k, 4 * k, {"west": D, "east": I, "south": N, "north": N}, ("west",))
+    e = rect(EAST, (3 * L, 2 * L), 4 * k, 4 * k, {"west": I, "east": D, "south": N, "north": N}, ("east",))
+    s_ = rect(SOUTH, (L, 0.0), 2 * k, 2 * k, {"west": N, "east": N, "south": D, "north": I}, ("south",))
+    n_ = rect(NORTH, (L, 6 * L), 2 * k, k, {"west": N, "east": N, "south": I, "north": D}, ("north",))
+    ifaces = [api.make_interface(0, w, "east", c, "west"), api.make_interface(1, c, "east", e, "west"),
+              api.make_interface(2, s_, "north", c, "south"), api.make_interface(3, c, "north", n_, "south")]
+    comp = api.CompositeDomain(subdomains=[c, w, e, s_, n_], interfaces=ifaces)
+    api.validate(comp).require()
+    return comp
+
+
 def batch_rects(n: int = 1023, count: int = 5, kappa: float = 0.0, api=None):
     """c1: `count` independent all-Dirichlet n x n rectangles, h = 1/n."""
     api = api or default_api()

@@ -20,7 +20,7 @@
 namespace fd {
 
 Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
-                  int device);
+                  int device, int pair = kPairDD);
 void plan_destroy(Plan *p);
 void factor_tables_host(int m, int n, double dx, double dy, double kappa, double mod_w,
                         double mod_e, double *beta, double *lower);
@@ -179,8 +179,8 @@ static void *dalloc(fd_schur_s *op, size_t bytes) {
 
 static void solve_batch(const std::vector<SolveJob> &jobs, cudaStream_t s) {
     // group by transform length (one pipeline launch per length)
-    std::map<int, std::vector<SolveJob>> groups;
-    for (const auto &j : jobs) groups[j.p.n].push_back(j);
+    std::map<std::pair<int, int>, std::vector<SolveJob>> groups;   // by (transform length, pair)
+    for (const auto &j : jobs) groups[{j.p.n, j.p.tpair}].push_back(j);
     for (auto &g : groups) launch_solve(g.second, s);
 }
 
@@ -490,21 +490,26 @@ int fd_plan_create(fd_plan *out, int m, int n, double dx, double dy, double kapp
     FD_API_END
 }
 
-int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double kappa,
-                        double mod_west, double mod_east, double mod_south, double mod_north,
-                        int transform_axis, int device) {
+int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double kappa, double mod_west,
+                      double mod_east, double mod_south, double mod_north, int transform_axis,
+                      int transform_pair, int device) {
     FD_API_BEGIN
     if (!out) FD_FAIL(FD_ERR_VALIDATION, "null output handle");
     *out = nullptr;
+    if (transform_pair != kPairDD && transform_pair != kPairNN)
+        FD_FAIL(FD_ERR_UNSUPPORTED, "transform pair must be DD (0) or NN (1)");
+    // a DD transform axis must carry ghost-node ends (no half-cell modifier,
+    // rectsolver.py:24-29); an NN axis's Neumann ends are part of its basis
+    const bool dd = transform_pair == kPairDD;
     Plan *p = nullptr;
     if (transform_axis == 0) {
-        if (mod_south != 0.0 || mod_north != 0.0)
-            FD_FAIL(FD_ERR_UNSUPPORTED, "transform along y needs ghost-node ends on south/north");
-        p = plan_create(m, n, dx, dy, kappa, mod_west, mod_east, device);
+        if (dd && (mod_south != 0.0 || mod_north != 0.0))
+            FD_FAIL(FD_ERR_UNSUPPORTED, "DD transform along y needs ghost-node ends on south/north");
+        p = plan_create(m, n, dx, dy, kappa, mod_west, mod_east, device, transform_pair);
     } else if (transform_axis == 1) {
-        if (mod_west != 0.0 || mod_east != 0.0)
-            FD_FAIL(FD_ERR_UNSUPPORTED, "transform along x needs ghost-node ends on west/east");
-        p = plan_create(n, m, dy, dx, kappa, mod_south, mod_north, device);
+        if (dd && (mod_west != 0.0 || mod_east != 0.0))
+            FD_FAIL(FD_ERR_UNSUPPORTED, "DD transform along x needs ghost-node ends on west/east");
+        p = plan_create(n, m, dy, dx, kappa, mod_south, mod_north, device, transform_pair);
         p->transposed = true;
     } else {
         FD_FAIL(FD_ERR_VALIDATION, "transform_axis must be 0 (y) or 1 (x)");
@@ -514,6 +519,15 @@ int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double
     *out = new fd_plan_s{p};
     FD_API_END
 }
+
+int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double kappa,
+                        double mod_west, double mod_east, double mod_south, double mod_north,
+                        int transform_axis, int device) {
+    return fd_plan_create_ex(out, m, n, dx, dy, kappa, mod_west, mod_east, mod_south, mod_north,
+                             transform_axis, kPairDD, device);
+}
+
+int fd_transform_kind_pair(int n, int pair) { return transform_kind(n, pair); }
 
 int fd_transform_kind(int n) { return transform_kind(n); }
 

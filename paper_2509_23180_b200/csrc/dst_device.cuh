@@ -439,7 +439,8 @@ struct DenseDstT {
     static constexpr int MINB = 2;
     static constexpr int MPT = MPT_;
     static constexpr int NMAX = NT * MPT_;
-    static constexpr size_t SMEM = size_t(G) * NMAX * sizeof(double) + size_t(2) * (NMAX + 1) * sizeof(double);
+    // rows + the periodic basis table: 2(n+1) entries (DD sine) or 4n (NN cosine)
+    static constexpr size_t SMEM = size_t(G) * NMAX * sizeof(double) + size_t(4) * (NMAX + 1) * sizeof(double);
 };
 
 // ---------------------------------------------------------------------------

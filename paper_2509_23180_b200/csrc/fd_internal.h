@@ -60,7 +60,11 @@ struct PlanDev {
     const double *dense; // [n][n] sin table (dense transform) or nullptr
     const double2 *tw;   // FFT twiddles e^{-2 pi i t / L}, t < L = 2(n+1), or nullptr
     const double *ralpha;// [n+1] real-DST pre-weights (rsolve.cu), alpha_j = s/2 sin(pi j/N) + s/4
+    int tpair;           // transform-axis pair: kPairDD (sine basis) or kPairNN (shifted cosine)
 };
+
+// transform-axis BC pairs (reference transforms.BC_PAIRS, transforms.py:24)
+enum TransformPair { kPairDD = 0, kPairNN = 1 };
 
 // ---------------------------------------------------------------------------
 // Geometry of the real-symmetric persistent solve (rsolve.cu), shared with the
@@ -168,14 +172,14 @@ struct JobList {
 };
 
 // kernels / launchers (solve.cu)
-int rows_per_block(int n);
-int transform_kind(int n);
+int rows_per_block(int n, int pair = kPairDD);
+int transform_kind(int n, int pair = kPairDD);
 void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s);
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,
                      const double *dense, cudaStream_t s);
 const double2 *twiddles_for(int device, int n);
-const double *dense_table_for(int device, int n);
+const double *dense_table_for(int device, int n, int pair = kPairDD);
 
 // vector kernels (ops.cu)
 void launch_stencil(int m, int n, double delta_x, double delta_y, double kappa, double mw,

@@ -39,6 +39,13 @@ double eig_dd(int k, int n, double dt, double dor, double kappa) {
     double lam = -2.0 * (dt + dor) + (2.0 * dt) * cos(arg);
     return lam + kappa;
 }
+// NN: cos((j - 1) pi / n), j = 1..n   (transforms.py:32-33)
+double eig_nn(int k, int n, double dt, double dor, double kappa) {
+    const double jm1 = double(k);
+    const double arg = jm1 * M_PI / double(n);
+    double lam = -2.0 * (dt + dor) + (2.0 * dt) * cos(arg);
+    return lam + kappa;
+}
 
 // Run the reference recurrence for one mode until the bitwise fixed point.
 ModeFactors factor_mode(int m, double lam, double mod_w, double mod_e, double off, double tol,
@@ -161,13 +168,13 @@ static void parallel_for(int n, F fn) {
 }
 
 static HostTables build_tables(int m, int n, double dx, double dy, double kappa, double mod_w,
-                               double mod_e, int R, bool carry_tables) {
+                               double mod_e, int R, bool carry_tables, int pair = kPairDD) {
     const double delta_x = 1.0 / (dx * dx), delta_y = 1.0 / (dy * dy);
     const double off = delta_x;
     std::vector<double> lam(n);
     double amax = 0.0;
     for (int k = 0; k < n; ++k) {
-        lam[k] = eig_dd(k, n, delta_y, delta_x, kappa);
+        lam[k] = pair == kPairNN ? eig_nn(k, n, delta_y, delta_x, kappa) : eig_dd(k, n, delta_y, delta_x, kappa);
         amax = std::max(amax, fabs(lam[k]));
     }
     const double tol = 1e-13 * std::max(amax, off);   // rectsolver.py:135
@@ -335,18 +342,23 @@ const double2 *twiddles_for(int device, int n) {
     return (const double2 *)d;
 }
 
-const double *dense_table_for(int device, int n) {
-    if (transform_kind(n) != kDense) return nullptr;
+const double *dense_table_for(int device, int n, int pair) {
+    if (transform_kind(n, pair) != kDense) return nullptr;
     std::lock_guard<std::mutex> g(g_tab_mu);
-    auto key = std::make_pair(device, n);
+    auto key = std::make_pair(device, n + (pair << 24));
     auto it = g_dense.find(key);
     if (it != g_dense.end()) return (const double *)it->second;
-    // sin(pi q / (n+1)), q < 2(n+1): the dense DST-I reads S[j][k] at q = (j+1)(k+1) mod 2(n+1)
-    const long long P2 = 2LL * (n + 1);
-    std::vector<double> h(P2);
-    for (long long q = 0; q < P2; ++q) {
-        long double a = 3.141592653589793238462643383279502884L * (long double)q / (long double)(n + 1);
-        h[q] = (double)sinl(a);
+    const long double PI_L = 3.141592653589793238462643383279502884L;
+    std::vector<double> h;
+    if (pair == kPairNN) {
+        // cos(pi q / 2n), q < 4n: the dense DCT-II/III read their basis at q = o(2i+1) / i(2o+1) mod 4n
+        h.resize(4 * size_t(n));
+        for (long long q = 0; q < 4LL * n; ++q) h[q] = (double)cosl(PI_L * (long double)q / (2.0L * (long double)n));
+    } else {
+        // sin(pi q / (n+1)), q < 2(n+1): the dense DST-I reads S[j][k] at q = (j+1)(k+1) mod 2(n+1)
+        const long long P2 = 2LL * (n + 1);
+        h.resize(P2);
+        for (long long q = 0; q < P2; ++q) h[q] = (double)sinl(PI_L * (long double)q / (long double)(n + 1));
     }
     void *d = nullptr;
     FD_CUDA(cudaMalloc(&d, sizeof(double) * h.size()));
@@ -365,18 +377,18 @@ static T *upload(Plan *p, const std::vector<T> &h) {
 }
 
 static Plan *build_proto(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
-                         int device) {
+                         int device, int pair) {
     if (m < 1 || n < 1) FD_FAIL(FD_ERR_VALIDATION, "plan: empty grid");
     if (!(dx > 0) || !(dy > 0)) FD_FAIL(FD_ERR_VALIDATION, "plan: nonpositive spacing");
-    const int tk = transform_kind(n);
+    const int tk = transform_kind(n, pair);
     if (tk < 0) {
         std::ostringstream os;
         os << "plan: no GPU transform for n = " << n
            << " (supported: n+1 a power of two in [256, 4096], or n <= 1024)";
         FD_FAIL(FD_ERR_UNSUPPORTED, os.str());
     }
-    const int R = rows_per_block(n);
-    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R, tk == kDense);
+    const int R = rows_per_block(n, pair);
+    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R, tk == kDense, pair);
     if (!T.bad_modes.empty()) {
         std::ostringstream os;
         os << "operator singular in spectral modes (";
@@ -407,7 +419,8 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.off = p->delta_x;
         d.mod_w = mod_w;
         d.mod_e = mod_e;
-        d.scale = sqrt(2.0 / (n + 1));
+        d.tpair = pair;
+        d.scale = pair == kPairNN ? sqrt(2.0 / n) : sqrt(2.0 / (n + 1));
         d.ex_off = upload(p, T.off);
         d.ex_len = upload(p, T.len);
         d.ex = upload(p, T.ex);
@@ -469,9 +482,9 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.lt = T.kt ? upload(p, T.lt) : nullptr;
         d.blk = T.blk.empty() ? nullptr : upload(p, T.blk);
         d.ye = d.fs = nullptr;   // per-plan scratch (plan_create)
-        d.tw = twiddles_for(device, n);
+        d.tw = tk == kFFT ? twiddles_for(device, n) : nullptr;
         d.ralpha = d.tw ? reinterpret_cast<const double *>(d.tw + 2 * (n + 1)) : nullptr;
-        d.dense = dense_table_for(device, n);
+        d.dense = dense_table_for(device, n, pair);
     } catch (...) {
         cudaDeviceSynchronize();
         for (void *a : p->allocs) dfree(a);
@@ -495,10 +508,10 @@ static void free_tables(Plan *p) {
 // repeated solves on the same geometry reuse the last few builds (LRU).
 namespace {
 struct PlanKey {
-    int device, m, n;
+    int device, m, n, pair;
     double v[5];
     bool operator==(const PlanKey &o) const {
-        return device == o.device && m == o.m && n == o.n && memcmp(v, o.v, sizeof(v)) == 0;
+        return device == o.device && m == o.m && n == o.n && pair == o.pair && memcmp(v, o.v, sizeof(v)) == 0;
     }
 };
 constexpr size_t kPlanCache = 8;
@@ -507,8 +520,8 @@ auto *g_plan_lru = new std::list<std::pair<PlanKey, std::shared_ptr<Plan>>>();  
 }  // namespace
 
 Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
-                  int device) {
-    PlanKey key{device, m, n, {dx, dy, kappa, mod_w, mod_e}};
+                  int device, int pair) {
+    PlanKey key{device, m, n, pair, {dx, dy, kappa, mod_w, mod_e}};
     std::shared_ptr<Plan> proto;
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
@@ -520,7 +533,7 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
             }
     }
     if (!proto) {
-        proto = std::shared_ptr<Plan>(build_proto(m, n, dx, dy, kappa, mod_w, mod_e, device), free_tables);
+        proto = std::shared_ptr<Plan>(build_proto(m, n, dx, dy, kappa, mod_w, mod_e, device, pair), free_tables);
         std::lock_guard<std::mutex> g(g_plan_mu);
         g_plan_lru->emplace_front(key, proto);
         if (g_plan_lru->size() > kPlanCache) g_plan_lru->pop_back();

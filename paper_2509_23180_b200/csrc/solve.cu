@@ -83,35 +83,59 @@ struct InvT<FftDst<LG>> {
     }
 };
 
-// Dense transform of the G-row group in rowbuf (shared) into acc (registers).
+// Dense transform of the G-row group in rowbuf (shared) into acc (registers):
+// acc[g][o] = sum_i T(q_io) x_g[i], T a periodic table, q_io = idx0(o) + i step(o)
+// (mod the period).  DD (both directions): T = sin(pi q/(n+1)), q = (i+1)(o+1).
+// NN forward (Q^T, transforms.py:83-90,129-134): T = cos(pi q/2n), q = o(2i+1);
+// NN inverse (Q, transforms.py:92-98,106-109): q = i(2o+1), input 0 scaled by
+// 1/sqrt(2) (the basis' sqrt(1/n) vs sqrt(2/n)).
 template <int M, int NT_>
 __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const double *tab,
-                                           double (&acc)[DenseDstT<M, NT_>::G][M]) {
+                                           double (&acc)[DenseDstT<M, NT_>::G][M], int pair, bool inverse) {
     constexpr int NT = DenseDstT<M, NT_>::NT, G = DenseDstT<M, NT_>::G;
-    const int N2 = 2 * (n + 1);
-    int idx[M];
+    const bool nn = pair == kPairNN;
+    const int period = nn ? 4 * n : 2 * (n + 1);
+    int idx[M], step[M];
 #pragma unroll
     for (int u = 0; u < M; ++u) {
-        idx[u] = threadIdx.x + u * NT + 1;   // (j + 1)(k + 1) mod 2N at j = 0
+        const int o = threadIdx.x + u * NT;
+        if (!nn) {
+            idx[u] = o + 1;        // (i + 1)(o + 1) at i = 0
+            step[u] = o + 1;
+        } else if (!inverse) {
+            idx[u] = o;            // o (2i + 1) at i = 0
+            step[u] = 2 * o;
+        } else {
+            idx[u] = 0;            // i (2o + 1) at i = 0
+            step[u] = 2 * o + 1;
+        }
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g][u] = 0.0;
     }
 #pragma unroll 2
     for (int j = 0; j < n; ++j) {
         double x[G];
+        const double xs = (nn && inverse && j == 0) ? 0.70710678118654752440 : 1.0;
 #pragma unroll
-        for (int g = 0; g < G; ++g) x[g] = rowbuf[g * n + j];
+        for (int g = 0; g < G; ++g) x[g] = rowbuf[g * n + j] * xs;
 #pragma unroll
         for (int u = 0; u < M; ++u) {
-            const int k1 = threadIdx.x + u * NT + 1;
-            if (k1 <= n) {
+            const int o = threadIdx.x + u * NT;
+            if (o < n) {
                 const double sv = tab[idx[u]];
 #pragma unroll
                 for (int g = 0; g < G; ++g) acc[g][u] = fma(sv, x[g], acc[g][u]);
-                idx[u] += k1;
-                if (idx[u] >= N2) idx[u] -= N2;
+                idx[u] += step[u];
+                if (idx[u] >= period) idx[u] -= period;
             }
         }
+    }
+    if (nn && !inverse) {   // output 0 carries sqrt(1/n) instead of sqrt(2/n)
+#pragma unroll
+        for (int u = 0; u < M; ++u)
+            if (threadIdx.x + u * NT == 0)
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[g][u] *= 0.70710678118654752440;
     }
 }
 
@@ -122,7 +146,8 @@ __device__ __forceinline__ double *dense_tab(double2 *smem) {
 
 template <int M, int NT_>
 __device__ __forceinline__ void stage_tab(double *tab, int n, const PlanDev &p) {
-    for (int q = threadIdx.x; q < 2 * (n + 1); q += DenseDstT<M, NT_>::NT) tab[q] = __ldg(p.dense + q);
+    const int period = p.tpair == kPairNN ? 4 * n : 2 * (n + 1);
+    for (int q = threadIdx.x; q < period; q += DenseDstT<M, NT_>::NT) tab[q] = __ldg(p.dense + q);
 }
 
 template <int M, int NT_>
@@ -137,7 +162,7 @@ struct FwdT<DenseDstT<M, NT_>> {
             rowbuf[idx] = idx < rows * n ? __ldg(in + idx) : 0.0;
         __syncthreads();
         double acc[G][M];
-        dense_rows<M, NT_>(rowbuf, n, tab, acc);
+        dense_rows<M, NT_>(rowbuf, n, tab, acc, p.tpair, false);
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < M; ++u) {
@@ -161,7 +186,7 @@ struct InvT<DenseDstT<M, NT_>> {
         for (int idx = rows * n + threadIdx.x; idx < G * n; idx += NT) rowbuf[idx] = 0.0;
         __syncthreads();
         double acc[G][M];
-        dense_rows<M, NT_>(rowbuf, n, tab, acc);
+        dense_rows<M, NT_>(rowbuf, n, tab, acc, p.tpair, true);
 #pragma unroll
         for (int u = 0; u < M; ++u) {
             const int k = threadIdx.x + u * NT;
@@ -423,16 +448,16 @@ __global__ void __launch_bounds__(P::NT) dst_rows_kernel(int rows_total, int n, 
 
 // ---------------------------------------------------------------------------
 // host side
-int transform_kind(int n) {
+int transform_kind(int n, int pair) {
     const int N = n + 1;
-    if ((N & (N - 1)) == 0 && N >= 256 && N <= 4096) return kFFT;
-    if (n <= kDenseMax) return kDense;
+    if (pair == kPairDD && (N & (N - 1)) == 0 && N >= 256 && N <= 4096) return kFFT;
+    if (n <= kDenseMax) return kDense;   // any pair: periodic-table dense transform
     return -1;
 }
 
-int rows_per_block(int n) {
+int rows_per_block(int n, int pair) {
     const int N = n + 1;
-    if (transform_kind(n) == kFFT) return N >= 4096 ? 8 : 16;
+    if (transform_kind(n, pair) == kFFT) return N >= 4096 ? 8 : 16;
     // one group per carry block: more CTAs for the small dense solves
     return n <= 160 ? DenseDstT<1, 160>::G : DenseDstT<1, 256>::G;
 }
@@ -507,7 +532,9 @@ void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
     const int n = jobs[0].p.n;
     for (auto &j : jobs)
         if (j.p.n != n) FD_FAIL(FD_ERR_VALIDATION, "launch_solve: mixed transform lengths in one batch");
-    if (transform_kind(n) == kDense) {
+    for (auto &j : jobs)
+        if (j.p.tpair != jobs[0].p.tpair) FD_FAIL(FD_ERR_VALIDATION, "launch_solve: mixed transform pairs in one batch");
+    if (jobs[0].p.dense) {
         if (n <= 128) run_solve<DenseDstT<1, 128>>(jobs, s);
         else if (n <= 160) run_solve<DenseDstT<1, 160>>(jobs, s);
         else if (n <= 256) run_solve<DenseDstT<1, 256>>(jobs, s);

@@ -24,32 +24,47 @@ from .errors import SingularOperatorError, ValidationError
 from .geometry import BoundaryKind, GridField, RectSubdomain
 
 
+_PAIR_CODE = {"DD": 0, "NN": 1}
+
+
 def _gpu_axis(sub: RectSubdomain) -> str:
     """Transform axis of the GPU plan.  The reference transforms along y when
-    that axis is in pure DD form and along x otherwise (rectsolver.py:102-109);
-    the GPU follows it, except that a y length without a GPU transform (n + 1
-    above 4096, e.g. the c4 south/north arms, n = 16383) moves the transform to
-    a transformable x axis (the reference's own transform_axis = "x" branch):
+    that axis is in pure form -- an NN pair, or a DD pair with ghost-node ends
+    -- and along x otherwise (rectsolver.py:24-29,102-109); the GPU follows it,
+    except that a y length without a GPU transform (n + 1 above 4096 for DD,
+    e.g. the c4 south/north arms, n = 16383) moves the transform to a
+    transformable x axis (the reference's own transform_axis = "x" branch):
     the FFT stays within one SM's shared memory and the long axis becomes the
-    Thomas sweep.  Same operator, rounding-level differences only."""
-    def ok(axis):
-        lo, hi = ("south", "north") if axis == "y" else ("west", "east")
-        return sub.axis_pair(axis) == "DD" and not sub.end_modifier(lo) and not sub.end_modifier(hi)
+    Thomas sweep.  Same operator, rounding-level differences only.  Periodic
+    (PP) pairs are not on the GPU path."""
+    def pair_of(axis):
+        try:
+            return sub.axis_pair(axis)
+        except ValidationError:
+            return None
 
-    def has_kernel(length):
-        return _native.lib().fd_transform_kind(int(length)) >= 0
+    def ok(axis):
+        pair = pair_of(axis)
+        if pair == "NN":
+            return True
+        lo, hi = ("south", "north") if axis == "y" else ("west", "east")
+        return pair == "DD" and not sub.end_modifier(lo) and not sub.end_modifier(hi)
+
+    def has_kernel(axis):
+        length = sub.n if axis == "y" else sub.m
+        return _native.lib().fd_transform_kind_pair(int(length), _PAIR_CODE[pair_of(axis)]) >= 0
 
     y_ok, x_ok = ok("y"), ok("x")
-    if y_ok and (has_kernel(sub.n) or not (x_ok and has_kernel(sub.m))):
+    if y_ok and (has_kernel("y") or not (x_ok and has_kernel("x"))):
         axis = "y"
     elif x_ok:
         axis = "x"
     else:
         raise UnsupportedError(
-            f"subdomain {sub.id}: neither axis is a ghost-node Dirichlet/interface pair "
-            f"(got y {sub.axis_pair('y')}, x {sub.axis_pair('x')} with end modifiers)")
+            f"subdomain {sub.id}: neither axis is a transformable pair on the GPU path "
+            f"(got y {pair_of('y')}, x {pair_of('x')} with end modifiers)")
     sweep = "x" if axis == "y" else "y"
-    if sub.axis_pair(sweep) == "PP":
+    if pair_of(sweep) == "PP":
         raise UnsupportedError(f"subdomain {sub.id}: periodic sweep axis is not on the GPU path")
     return axis
 
@@ -60,10 +75,11 @@ class _Handle:
     def __init__(self, sub: RectSubdomain, axis: str):
         _native.require_cuda()
         h = _native.P()
-        _native.call("fd_plan_create_axis", ctypes_ref(h), sub.m, sub.n, float(sub.dx), float(sub.dy),
+        pair = _PAIR_CODE[sub.axis_pair(axis)]
+        _native.call("fd_plan_create_ex", ctypes_ref(h), sub.m, sub.n, float(sub.dx), float(sub.dy),
                      float(sub.kappa), float(sub.end_modifier("west")), float(sub.end_modifier("east")),
                      float(sub.end_modifier("south")), float(sub.end_modifier("north")),
-                     0 if axis == "y" else 1, _native.torch().cuda.current_device())
+                     0 if axis == "y" else 1, pair, _native.torch().cuda.current_device())
         self.ptr = h
 
     def __del__(self):
@@ -116,10 +132,10 @@ def plan_rect(subdomain: RectSubdomain, pin_mean: bool = False) -> RectPlan:
     _native.require_cuda()
     axis = _gpu_axis(sub)
     if axis == "y":
-        lam_plan = transforms.make_plan("DD", sub.n, sub.delta_y, sub.delta_x, sub.kappa)
+        lam_plan = transforms.make_plan(sub.axis_pair("y"), sub.n, sub.delta_y, sub.delta_x, sub.kappa)
         pair, off = sub.axis_pair("x"), sub.delta_x
     else:
-        lam_plan = transforms.make_plan("DD", sub.m, sub.delta_x, sub.delta_y, sub.kappa)
+        lam_plan = transforms.make_plan(sub.axis_pair("x"), sub.m, sub.delta_x, sub.delta_y, sub.kappa)
         pair, off = sub.axis_pair("y"), sub.delta_y
     handle = _Handle(sub, axis)
     return RectPlan(subdomain=sub, transform_axis=axis, y_plan=lam_plan,

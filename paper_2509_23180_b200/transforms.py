@@ -3,9 +3,10 @@
 `eigenvalues`/`make_plan` are host-side setup (O(n)).  `apply_Q`/`apply_Qt`
 for the Dirichlet-Dirichlet pair run the sm_100a DST-I kernel (Q = Q^T =
 sqrt(2/(n+1)) DST-I, transforms.py:112-113,135-136) on torch CUDA tensors;
-numpy input is copied to the device and the result back.  NN/PP transforms
-are outside the GPU path this round and raise
-UnsupportedError.
+numpy input is copied to the device and the result back.  The NN pair runs
+inside the rectangle solves (dense DCT-II/III, csrc/solve.cu); the standalone
+apply_Q/apply_Qt entry points cover DD, and PP is not on the GPU path
+(UnsupportedError).
 """
 
 from __future__ import annotations

@@ -2,7 +2,7 @@
 
 Run in the build container only (needs /root/reference):
 
-    python tests/golden/make_golden.py small c0 c1        # seconds
+    python tests/golden/make_golden.py small c0 c1 nn     # seconds
     python tests/golden/make_golden.py c2 c3              # minutes (c3 ~15 min, 16 GB)
 
 The reference package is imported from /root/reference/pkg/src; its inputs
@@ -170,10 +170,53 @@ def make_c1():
     print("c1.npz written")
 
 
+# NN-transform rectangles (m, n, dx, dy, kappa, bc WESN, half-cell edges): the
+# reference picks y when y is NN or ghost-node DD, else x (rectsolver.py:102-109)
+NN_RECT_CASES = [
+    (12, 16, 0.1, 0.1, 0.0, "DDNN", ()),              # NN along y, DD sweep
+    (20, 33, 0.05, 0.04, -3.0, "DDNN", ("west",)),    # + half-cell west end on the sweep
+    (9, 64, 1.0 / 64, 1.0 / 64, 2.5, "IDNN", ("east",)),
+    (16, 10, 0.1, 0.1, 0.0, "NNDD", ("south",)),      # y has a half-cell end -> NN along x
+    (40, 24, 1.0 / 40, 1.0 / 24, -10.0, "NNDD", ("north", "south")),
+    (130, 141, 1.0 / 141, 1.0 / 141, 0.0, "DDNN", ("east",)),
+]
+
+
+def make_nn():
+    """NN-transform rectangle solves and the reference's own test cross
+    (bench.build_cross: Neumann flanks, half-cell Dirichlet arm ends) solved
+    with its manufactured right-hand side, GMRES(50) to 1e-10."""
+    from fftddm import bench as rbench
+    out = {}
+    rng = np.random.default_rng(11)
+    for c, case in enumerate(NN_RECT_CASES):
+        sub = rect(*case)
+        pl = rectsolver.plan_rect(sub)
+        f = rng.standard_normal(sub.size)
+        out[f"nn_axis_{c}"] = np.array(pl.transform_axis)
+        out[f"nn_f_{c}"] = f
+        out[f"nn_p_{c}"] = rectsolver.solve_rect(pl, f).values
+    for k_n in (2, 4, 8, 16):
+        for kappa in (0.0, -3.0):
+            case = rbench.build_cross(k_n=k_n, kappa=kappa)
+            rhs = rbench.rhs_fields(case)
+            fields, rep = ddm.ddm_solve(case.composite, rhs, krylov.GmresConfig(m=50, tol=1e-10))
+            key = f"{k_n}_{int(-kappa)}"
+            out[f"x_iters_{key}"] = np.array(rep.iterations)
+            out[f"x_hist_{key}"] = np.asarray(rep.residual_history)
+            for sub in case.composite.subdomains:
+                out[f"x_f_{key}_{sub.id}"] = rhs[sub.id].values
+                out[f"x_p_{key}_{sub.id}"] = fields[sub.id].values
+    np.savez_compressed(os.path.join(HERE, "nn.npz"), **out)
+    print("nn.npz written")
+
+
 if __name__ == "__main__":
     for what in sys.argv[1:] or ["small", "c0", "c1"]:
         if what == "small":
             make_small()
+        elif what == "nn":
+            make_nn()
         elif what == "c1":
             make_c1()
         else:

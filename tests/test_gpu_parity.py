@@ -317,6 +317,52 @@ class TestTransposedAxis:
         assert (num / den) ** 0.5 == pytest.approx(float(g["rel_l2_exact"]), rel=1e-4)
 
 
+NN_RECT_CASES = [
+    (12, 16, 0.1, 0.1, 0.0, "DDNN", ()),
+    (20, 33, 0.05, 0.04, -3.0, "DDNN", ("west",)),
+    (9, 64, 1.0 / 64, 1.0 / 64, 2.5, "IDNN", ("east",)),
+    (16, 10, 0.1, 0.1, 0.0, "NNDD", ("south",)),
+    (40, 24, 1.0 / 40, 1.0 / 24, -10.0, "NNDD", ("north", "south")),
+    (130, 141, 1.0 / 141, 1.0 / 141, 0.0, "DDNN", ("east",)),
+]
+
+
+class TestNeumannTransform:
+    """NN (shifted-cosine) transform axes on the dense periodic-table path and
+    the reference's own test cross (Neumann flanks, half-cell arm ends),
+    against fixtures written by the reference."""
+
+    @pytest.mark.parametrize("c", range(len(NN_RECT_CASES)))
+    def test_rect_golden(self, c):
+        g = load_golden("nn")
+        sub = make(NN_RECT_CASES[c])
+        pl = rectsolver.plan_rect(sub)
+        assert pl.transform_axis == str(g[f"nn_axis_{c}"])
+        p = rectsolver.solve_rect(pl, g[f"nn_f_{c}"]).values
+        assert rel(p, g[f"nn_p_{c}"]) < 1e-12
+
+    @pytest.mark.parametrize("n", [1, 2, 7, 64, 141, 1000])
+    def test_against_oracle_and_residual(self, n, rng):
+        sub = make((33, n, 1.0 / 33, 1.0 / max(n, 2), -1.0, "DDNN", ("west",)))
+        f = rng.uniform(-1, 1, sub.size)
+        p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f).values
+        assert rel(p, O.solve(O.plan(sub), f)) < 1e-12
+        r = rectsolver.apply_rect_operator(sub, p) - f
+        assert np.linalg.norm(r) / np.linalg.norm(f) < 1e-11
+
+    @pytest.mark.parametrize("k_n,kappa", [(2, 0.0), (4, -3.0), (8, 0.0), (16, -3.0), (16, 0.0)])
+    def test_reference_cross(self, k_n, kappa):
+        g = load_golden("nn")
+        comp = configs.reference_cross(k_n, kappa=kappa)
+        key = f"{k_n}_{int(-kappa)}"
+        f = {s.id: g[f"x_f_{key}_{s.id}"] for s in comp.subdomains}
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+        assert rep.iterations == int(g[f"x_iters_{key}"])
+        num = sum(float(np.sum((fields[s.id].values - g[f"x_p_{key}_{s.id}"]) ** 2)) for s in comp.subdomains)
+        den = sum(float(np.sum(g[f"x_p_{key}_{s.id}"] ** 2)) for s in comp.subdomains)
+        assert (num / den) ** 0.5 < 1e-10
+
+
 class TestDistDriver:
     def test_native_backend_single_rank(self, golden_small):
         """dist_ddm_solve with the GPU backend and no process group (one rank owns

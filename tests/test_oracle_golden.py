@@ -92,3 +92,49 @@ class TestAgainstReferenceFixtures:
         for sid in range(5):
             assert rel(fields[sid], g[f"sol_{sid}"]) < 1e-13
         assert configs.rel_l2(fields, exact) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-9)
+
+
+NN_RECT_CASES = [
+    (12, 16, 0.1, 0.1, 0.0, "DDNN", ()),
+    (20, 33, 0.05, 0.04, -3.0, "DDNN", ("west",)),
+    (9, 64, 1.0 / 64, 1.0 / 64, 2.5, "IDNN", ("east",)),
+    (16, 10, 0.1, 0.1, 0.0, "NNDD", ("south",)),
+    (40, 24, 1.0 / 40, 1.0 / 24, -10.0, "NNDD", ("north", "south")),
+    (130, 141, 1.0 / 141, 1.0 / 141, 0.0, "DDNN", ("east",)),
+]
+
+
+@pytest.fixture(scope="module")
+def golden_nn():
+    return load_golden("nn")
+
+
+class TestNeumannTransformFixtures:
+    """NN (shifted-cosine) transform axes and the reference's own test cross,
+    against fixtures written by the reference (tests/golden/make_golden.py nn)."""
+
+    @pytest.mark.parametrize("c", range(len(NN_RECT_CASES)))
+    def test_rect(self, golden_nn, c):
+        from rects import make
+        sub = make(NN_RECT_CASES[c])
+        pl = O.plan(sub)
+        assert pl.axis == str(golden_nn[f"nn_axis_{c}"])
+        p = O.solve(pl, golden_nn[f"nn_f_{c}"])
+        ref = golden_nn[f"nn_p_{c}"]
+        assert rel(p, ref) < 1e-13
+
+    def test_nn_basis_orthonormal(self):
+        for n in (1, 2, 5, 16):
+            Q = O.apply_q("NN", np.eye(n))
+            np.testing.assert_allclose(Q @ Q.T, np.eye(n), atol=1e-13)
+            np.testing.assert_allclose(O.apply_qt("NN", O.apply_q("NN", np.eye(n))), np.eye(n), atol=1e-13)
+
+    @pytest.mark.parametrize("k_n,kappa", [(2, 0.0), (4, -3.0), (8, 0.0)])
+    def test_reference_cross(self, golden_nn, k_n, kappa):
+        comp = configs.reference_cross(k_n, kappa=kappa)
+        key = f"{k_n}_{int(-kappa)}"
+        f = {s.id: golden_nn[f"x_f_{key}_{s.id}"] for s in comp.subdomains}
+        fields, rep = O.ddm_solve(comp, f, m=50, tol=1e-10)
+        assert rep.iterations == int(golden_nn[f"x_iters_{key}"])
+        for s in comp.subdomains:
+            assert rel(fields[s.id], golden_nn[f"x_p_{key}_{s.id}"]) < 1e-12
