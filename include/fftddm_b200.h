@@ -119,6 +119,18 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south,
                     const double *to_c_coupling,
                     const int64_t *const *from_c_from, const int64_t *const *from_c_to,
                     const double *from_c_coupling);
+/* Interface-only (Steklov) neighbour applies -- SURVEY 8f row 2, an opt-in
+ * variant of SchurOperator.schur (ddm.py:108-123) with the same result up to
+ * rounding: neighbour i's interface line (length line_len, a DD pair with
+ * ghost-node ends along the line) sits at the first (end 0) or last (end 1)
+ * row of its sweep (sweep_len rows, end modifiers mod_lo/mod_hi); pos_in[j] /
+ * pos_out[j] are the line positions of entry j of its R_ic / R_ci maps.  Then
+ * R_ci A_i^{-1} R_ic = c_ci c_ic Q diag(1/beta_end) Q^T on the line, O(L log L)
+ * per apply.  Full solves stay in the pre-solves and the back-substitution. */
+int fd_schur_set_steklov(fd_schur op, int i, int line_len, int sweep_len, double delta_line,
+                         double delta_sweep, double kappa, double mod_lo, double mod_hi, int end,
+                         const int64_t *pos_in, const int64_t *pos_out);
+int fd_schur_use_steklov(fd_schur op, int enable);
 int fd_schur_destroy(fd_schur op);
 /* SchurOperator.schur / center_solve / preconditioned / unpreconditioned
  * (ddm.py:112-136); p, out are centre-sized device vectors, may not alias. */

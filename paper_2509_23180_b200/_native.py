@@ -27,7 +27,7 @@ EXPORTS = (
     "fd_factor_tables_host", "fd_rect_solve", "fd_rect_solve_batched", "fd_dst_rows",
     "fd_stencil_apply", "fd_schur_create", "fd_schur_destroy", "fd_schur_apply",
     "fd_center_solve", "fd_precond_apply", "fd_unprecond_apply", "fd_gmres_precond",
-    "fd_ddm_solve", "fd_arnoldi_step", "fd_basis_update", "fd_axpby", "fd_norm", "fd_dot",
+    "fd_ddm_solve", "fd_schur_set_steklov", "fd_schur_use_steklov", "fd_arnoldi_step", "fd_basis_update", "fd_axpby", "fd_norm", "fd_dot",
 )
 
 
@@ -70,6 +70,8 @@ def _declare(lib):
                                 ctypes.POINTER(P), ctypes.POINTER(P), DP,
                                 ctypes.POINTER(P), ctypes.POINTER(P), DP]),
         "fd_schur_destroy": (I, [P]),
+        "fd_schur_set_steklov": (I, [P, I, I, I, D, D, D, D, D, I, P, P]),
+        "fd_schur_use_steklov": (I, [P, I]),
         "fd_schur_apply": (I, [P, P, P, P]),
         "fd_center_solve": (I, [P, P, P, P]),
         "fd_precond_apply": (I, [P, P, P, P]),

@@ -165,6 +165,17 @@ struct fd_schur_s {
     // low-synchronisation Arnoldi: Gram rows, partials, results (device) + pinned mirror
     fd::ArnWork arn{};
     double *arn_out = nullptr, *arn_host = nullptr;
+    // interface-only (Steklov) neighbour applies: per arm the
+    // line positions of the R_ic / R_ci entries and the interface-end inverse
+    // pivots; line buffers [arms][L]
+    struct Steklov {
+        int L = 0;
+        int64_t *pos_in = nullptr, *pos_out = nullptr;   // device, per coupling entry
+        double *invpiv = nullptr;                        // device [L]
+    };
+    std::vector<Steklov> stk;
+    bool steklov = false;
+    double *lines = nullptr, *lines_hat = nullptr;
     std::vector<void *> allocs;
 };
 
@@ -239,8 +250,41 @@ static void solve_user(const std::vector<UJob> &uj, cudaStream_t s) {
     }
 }
 
+// Interface-only form of the same sum: for a DD line of length L adjacent to an
+// interface end of the sweep, R_ci A_i^{-1} R_ic restricted to that line is
+// c_ci c_ic Q diag(1 / beta_end) Q^T (Q the orthonormal DST-I of the line): the
+// neighbour's field is zero except on the line, so the forward elimination is
+// y = r on the line row and the back-substitution's interface value is
+// y / beta_end -- the arm's full solve yields exactly these values there.
+// O(L log L) per arm instead of a full arm solve.
+static void schur_apply_steklov(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
+    const size_t nnb = op->nb.size();
+    const int L = op->stk[0].L;
+    FD_CUDA(cudaMemsetAsync(op->lines, 0, sizeof(double) * nnb * L, s));
+    for (size_t i = 0; i < nnb; ++i) {
+        const Coupling &c = op->from_c[i];   // centre line -> the arm's interface line
+        launch_scatter(c.len, c.from, op->stk[i].pos_in, c.c, p, op->lines + i * L, 0, s);
+    }
+    launch_dst_rows((int)nnb, L, op->lines, op->lines_hat, twiddles_for(op->device, L),
+                    dense_table_for(op->device, L), s);
+    for (size_t i = 0; i < nnb; ++i)
+        launch_mul(L, op->lines_hat + i * L, op->stk[i].invpiv, op->lines_hat + i * L, s);
+    launch_dst_rows((int)nnb, L, op->lines_hat, op->lines, twiddles_for(op->device, L),
+                    dense_table_for(op->device, L), s);
+    const Plan *cp = op->center;
+    FD_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * cp->m * cp->n, s));
+    for (size_t i = 0; i < nnb; ++i) {
+        const Coupling &c = op->to_c[i];
+        launch_scatter(c.len, op->stk[i].pos_out, c.to, c.c, op->lines + i * L, out, 1, s);
+    }
+}
+
 // out = sum_i R_ci A_i^{-1} R_ic p   (ddm.py:108-123)
 static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
+    if (op->steklov) {
+        schur_apply_steklov(op, p, out, s);
+        return;
+    }
     const size_t nnb = op->nb.size();
     std::vector<SolveJob> jobs;
     for (size_t i = 0; i < nnb; ++i) {
@@ -648,6 +692,49 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, doub
         throw;
     }
     *out = op;
+    FD_API_END
+}
+
+int fd_schur_set_steklov(fd_schur op, int i, int line_len, int sweep_len, double delta_line,
+                         double delta_sweep, double kappa, double mod_lo, double mod_hi, int end,
+                         const int64_t *pos_in, const int64_t *pos_out) {
+    FD_API_BEGIN
+    if (!op || i < 0 || i >= (int)op->nb.size()) FD_FAIL(FD_ERR_VALIDATION, "steklov: bad neighbour index");
+    if (line_len < 1 || sweep_len < 1 || (end != 0 && end != 1)) FD_FAIL(FD_ERR_VALIDATION, "steklov: bad line");
+    if (transform_kind(line_len) < 0) FD_FAIL(FD_ERR_UNSUPPORTED, "steklov: no GPU transform for the line length");
+    FD_CUDA(cudaSetDevice(op->device));
+    if (op->stk.size() != op->nb.size()) op->stk.resize(op->nb.size());
+    auto &k = op->stk[i];
+    k.L = line_len;
+    const int len = op->from_c[i].len;
+    std::vector<double> inv(line_len);
+    steklov_pivots(line_len, sweep_len, delta_line, delta_sweep, kappa, mod_lo, mod_hi, end, inv.data());
+    k.invpiv = (double *)dalloc(op, sizeof(double) * line_len);
+    FD_CUDA(cudaMemcpy(k.invpiv, inv.data(), sizeof(double) * line_len, cudaMemcpyHostToDevice));
+    k.pos_in = (int64_t *)dalloc(op, sizeof(int64_t) * std::max(len, 1));
+    k.pos_out = (int64_t *)dalloc(op, sizeof(int64_t) * std::max(op->to_c[i].len, 1));
+    FD_CUDA(cudaMemcpy(k.pos_in, pos_in, sizeof(int64_t) * len, cudaMemcpyHostToDevice));
+    FD_CUDA(cudaMemcpy(k.pos_out, pos_out, sizeof(int64_t) * op->to_c[i].len, cudaMemcpyHostToDevice));
+    FD_API_END
+}
+
+int fd_schur_use_steklov(fd_schur op, int enable) {
+    FD_API_BEGIN
+    if (!op) FD_FAIL(FD_ERR_VALIDATION, "null operator");
+    if (!enable) {
+        op->steklov = false;
+    } else {
+        if (op->stk.size() != op->nb.size() || op->nb.empty())
+            FD_FAIL(FD_ERR_VALIDATION, "steklov: describe every neighbour first");
+        for (auto &k : op->stk)
+            if (!k.invpiv || k.L != op->stk[0].L)
+                FD_FAIL(FD_ERR_UNSUPPORTED, "steklov: every neighbour needs a described line of one length");
+        if (!op->lines) {
+            op->lines = (double *)dalloc(op, sizeof(double) * op->nb.size() * op->stk[0].L);
+            op->lines_hat = (double *)dalloc(op, sizeof(double) * op->nb.size() * op->stk[0].L);
+        }
+        op->steklov = true;
+    }
     FD_API_END
 }
 

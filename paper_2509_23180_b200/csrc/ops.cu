@@ -61,6 +61,17 @@ __global__ void scatter_kernel(int len, const int64_t *__restrict__ from, const 
     }
 }
 
+__global__ void mul_kernel(long long N, const double *__restrict__ x, const double *__restrict__ y, double *out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+        out[i] = x[i] * y[i];
+}
+
+void launch_mul(long long N, const double *x, const double *y, double *out, cudaStream_t s) {
+    if (N <= 0) return;
+    mul_kernel<<<(int)std::min<long long>((N + 255) / 256, 148LL * 16), 256, 0, s>>>(N, x, y, out);
+    FD_CUDA(cudaGetLastError());
+}
+
 __global__ void zero_at_kernel(int len, const int64_t *__restrict__ to, double *dst) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < len; t += gridDim.x * blockDim.x) dst[to[t]] = 0.0;
 }

@@ -581,6 +581,40 @@ void plan_destroy(Plan *p) {
     delete p;   // drops the shared tables reference
 }
 
+// Interface-end pivots of the per-mode sweep systems of a DD line of length L:
+// inv[k] = 1 / beta_end,k where beta_end is the last pivot of the reference's
+// forward recurrence (end = 1: the interface is the sweep's last row) or of the
+// same recurrence run from the far end (end = 0: first row), i.e. the corner
+// element of the inverse of tridiag(off, lambda_k + end modifiers, off).
+void steklov_pivots(int L, int M, double delta_line, double delta_sweep, double kappa, double mod_lo,
+                    double mod_hi, int end, double *inv) {
+    const double off = delta_sweep;
+    parallel_for(L, [&](int k0, int k1) {
+        for (int k = k0; k < k1; ++k) {
+            const double lam = eig_dd(k, L, delta_line, delta_sweep, kappa);
+            // walk from the far end towards the interface row
+            const double m_start = end ? mod_lo : mod_hi, m_end = end ? mod_hi : mod_lo;
+            double b = lam;
+            if (M == 1) {
+                b = lam + mod_lo;
+                b = b + mod_hi;
+            } else {
+                b = lam + m_start;
+                bool fixed = false;
+                for (int i = 1; i < M; ++i) {
+                    const double d = (i == M - 1) ? lam + m_end : lam;
+                    if (fixed && i < M - 1) continue;   // bitwise fixed point: rows until the last are equal
+                    const double l = off / b;
+                    const double nb = d - off * l;
+                    if (i < M - 1 && nb == b) fixed = true;
+                    b = nb;
+                }
+            }
+            inv[k] = 1.0 / b;
+        }
+    });
+}
+
 void factor_tables_host(int m, int n, double dx, double dy, double kappa, double mod_w,
                         double mod_e, double *beta, double *lower) {
     if (m < 1 || n < 1) FD_FAIL(FD_ERR_VALIDATION, "factor: empty grid");

@@ -84,6 +84,32 @@ class _Neighbor:
     plan: RectPlan
     to_center: CouplingMap      # R_ci
     from_center: CouplingMap    # R_ic
+    edge: str = ""              # the neighbour's edge on the interface
+
+
+def _steklov_line(sub, edge, to_center, from_center):
+    """Describe neighbour `sub`'s interface line for the interface-only apply
+    (SURVEY 8f row 2), or None when the line is not a ghost-node DD pair.
+    Returns (L, M, delta_line, delta_sweep, mod_lo, mod_hi, end, pos_in, pos_out)."""
+    if edge in ("west", "east"):
+        along, lo, hi, sweep_lo, sweep_hi = "y", "south", "north", "west", "east"
+        L, M, dl, ds = sub.n, sub.m, sub.delta_y, sub.delta_x
+        pos = lambda idx: np.asarray(idx) % sub.n   # noqa: E731
+    else:
+        along, lo, hi, sweep_lo, sweep_hi = "x", "west", "east", "south", "north"
+        L, M, dl, ds = sub.m, sub.n, sub.delta_x, sub.delta_y
+        pos = lambda idx: np.asarray(idx) // sub.n  # noqa: E731
+    try:
+        if sub.axis_pair(along) != "DD" or sub.end_modifier(lo) or sub.end_modifier(hi):
+            return None
+        if sub.axis_pair("x" if along == "y" else "y") == "PP":
+            return None
+    except ValidationError:
+        return None
+    end = 0 if edge in ("west", "south") else 1
+    return (L, M, dl, ds, float(sub.end_modifier(sweep_lo)), float(sub.end_modifier(sweep_hi)), end,
+            np.ascontiguousarray(pos(from_center.to_idx), dtype=np.int64),
+            np.ascontiguousarray(pos(to_center.from_idx), dtype=np.int64))
 
 
 class _SchurHandle:
@@ -122,6 +148,21 @@ class _SchurHandle:
                 _native.lib().fd_schur_destroy(self.ptr)
         except Exception:
             pass
+
+    def use_interface_only(self, neighbors, kappa) -> bool:
+        """Switch the neighbour applies to the interface-only (Steklov) form when
+        every neighbour's interface line qualifies; returns whether it did."""
+        lines = [_steklov_line(nb.plan.subdomain, nb.edge, nb.to_center, nb.from_center) for nb in neighbors]
+        if not lines or any(x is None for x in lines) or len({x[0] for x in lines}) != 1:
+            return False
+        for i, (L, M, dl, ds, mlo, mhi, end, pin, pout) in enumerate(lines):
+            st = _native.lib().fd_schur_set_steklov(self.ptr, i, L, M, float(dl), float(ds), float(kappa),
+                                                    mlo, mhi, end, pin.ctypes.data, pout.ctypes.data)
+            if st == _native.FD_ERR_UNSUPPORTED:
+                return False
+            _native.check(st)
+        _native.call("fd_schur_use_steklov", self.ptr, 1)
+        return True
 
 
 @dataclass(frozen=True)
@@ -199,24 +240,33 @@ def designate_center(comp: CompositeDomain) -> int:
 
 
 def build_schur_operator(comp: CompositeDomain, coupled_id: int | None = None,
-                         threads: int | None = None) -> SchurOperator:
-    """Plans for the centre and every neighbour + native operator (ref ddm.py:182-201)."""
+                         threads: int | None = None, interface_only: bool = False) -> SchurOperator:
+    """Plans for the centre and every neighbour + native operator (ref ddm.py:182-201).
+    interface_only=True selects the opt-in Steklov form of the neighbour applies
+    (same operator up to rounding) when every neighbour's
+    interface line is a ghost-node DD pair of one length."""
     if coupled_id is None:
         coupled_id = designate_center(comp)
     center = comp.subdomain(coupled_id)
     neighbors = []
     for iface in comp.interfaces_of(coupled_id):
         other = iface.other_side(coupled_id)[0]
+        edge = iface.side_a[1] if iface.side_a[0] == other else iface.side_b[1]
         neighbors.append(_Neighbor(plan=plan_rect(comp.subdomain(other)),
                                    to_center=make_coupling(comp, iface, other),
-                                   from_center=make_coupling(comp, iface, coupled_id)))
+                                   from_center=make_coupling(comp, iface, coupled_id), edge=edge))
     cplan = plan_rect(center)
     handle = _SchurHandle(cplan, neighbors)
+    if interface_only:
+        kappas = {comp.subdomain(nb.plan.subdomain.id).kappa for nb in neighbors}
+        if len(kappas) == 1:
+            handle.use_interface_only(neighbors, kappas.pop())
     return SchurOperator(coupled_id=coupled_id, center=center, center_plan=cplan,
                          neighbors=tuple(neighbors), handle=handle)
 
 
-def ddm_solve(comp: CompositeDomain, f, gmres_cfg=None, coupled_id: int | None = None):
+def ddm_solve(comp: CompositeDomain, f, gmres_cfg=None, coupled_id: int | None = None,
+              interface_only: bool = False):
     """Solve the composite system; returns ({id: GridField}, SolveReport)
     (ref ddm.py:210-270).  numpy right-hand sides give numpy solutions; torch
     CUDA right-hand sides stay on the device."""
@@ -237,7 +287,7 @@ def ddm_solve(comp: CompositeDomain, f, gmres_cfg=None, coupled_id: int | None =
         return {sub.id: GridField(sub.id, like_input(p.values, host))}, rep
     if cfg.preconditioner != "fft":
         return _ddm_solve_generic(comp, rhs, cfg, coupled_id, host)
-    op = build_schur_operator(comp, coupled_id=coupled_id)
+    op = build_schur_operator(comp, coupled_id=coupled_id, interface_only=interface_only)
     nbs = [nb.plan.subdomain for nb in op.neighbors]
     p_c = empty(op.size)
     p_nb = [empty(s.size) for s in nbs]

@@ -363,6 +363,43 @@ class TestNeumannTransform:
         assert (num / den) ** 0.5 < 1e-10
 
 
+class TestInterfaceOnlyVariant:
+    """Opt-in interface-only (Steklov) neighbour applies:
+    same operator up to rounding, so the same iterations and solution."""
+
+    @pytest.mark.parametrize("name,N", [("c0", 31), ("c0", 141), ("c3", 63), ("c4", 31)])
+    def test_matches_full_and_oracle(self, name, N):
+        comp, f, _, _ = configs.build_cross_case(name, N=N)
+        cfg = krylov.GmresConfig(m=50, tol=1e-10)
+        full, rep_f = ddm.ddm_solve(comp, f, cfg)
+        stk, rep_s = ddm.ddm_solve(comp, f, cfg, interface_only=True)
+        ofields, orep = O.ddm_solve(comp, f, m=50, tol=1e-10)
+        assert rep_s.iterations == rep_f.iterations == orep.iterations
+        num = sum(float(np.sum((stk[s].values - ofields[s]) ** 2)) for s in ofields)
+        den = sum(float(np.sum(ofields[s] ** 2)) for s in ofields)
+        assert (num / den) ** 0.5 < 1e-10
+
+    def test_schur_apply_matches(self, rng):
+        comp, f, _, _ = configs.build_cross_case("c3", N=255)
+        op_f = ddm.build_schur_operator(comp)
+        op_s = ddm.build_schur_operator(comp, interface_only=True)
+        p = dev(rng.uniform(-1, 1, op_f.size))
+        a, b = op_f.schur(p), op_s.schur(p)
+        assert (torch.linalg.norm(a - b) / torch.linalg.norm(a)).item() < 1e-13
+
+    @pytest.mark.slow
+    def test_c2_golden(self):
+        g = load_golden("c2")
+        comp, f, exact, _ = configs.build_cross_case("c2")
+        fd = {k: dev(v) for k, v in f.items()}
+        fields, rep = ddm.ddm_solve(comp, fd, krylov.GmresConfig(m=50, tol=1e-10), interface_only=True)
+        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        for sid in range(5):
+            v = fields[sid].values
+            idx = torch.as_tensor(g[f"idx_{sid}"], device="cuda")
+            assert rel(v[idx].cpu().numpy(), g[f"val_{sid}"]) < 1e-10
+
+
 class TestDistDriver:
     def test_native_backend_single_rank(self, golden_small):
         """dist_ddm_solve with the GPU backend and no process group (one rank owns

@@ -30,17 +30,18 @@ def main():
         fd = {k: torch.as_tensor(v, device="cuda") for k, v in f.items()}
         del f
         cfg = krylov.GmresConfig(m=50, tol=1e-10)
-        fields, rep = ddm.ddm_solve(comp, fd, cfg)   # warm-up (module load, tables)
+        kw = {"interface_only": True} if "--steklov" in sys.argv else {}
+        fields, rep = ddm.ddm_solve(comp, fd, cfg, **kw)   # warm-up (module load, tables)
         torch.cuda.synchronize()
         times = []
         for _ in range(reps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            fields, rep = ddm.ddm_solve(comp, fd, cfg)
+            fields, rep = ddm.ddm_solve(comp, fd, cfg, **kw)
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
         wall = float(np.median(times))
-        out = {"config": name, "points": meta["points"], "iterations": rep.iterations,
+        out = {"config": name + (" interface-only" if kw else ""), "points": meta["points"], "iterations": rep.iterations,
                "wall_s": wall, "mpts_per_s": meta["points"] / wall / 1e6,
                "gmres_wall_s": rep.wall_time, "all_s": [round(t, 4) for t in times], "us_per_iteration": rep.wall_time / max(rep.iterations, 1) * 1e6,
                "true_residual": rep.true_residual}
