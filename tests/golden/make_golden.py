@@ -207,6 +207,26 @@ def make_nn():
             for sub in case.composite.subdomains:
                 out[f"x_f_{key}_{sub.id}"] = rhs[sub.id].values
                 out[f"x_p_{key}_{sub.id}"] = fields[sub.id].values
+    # comparison preconditioners (krylov.py:179-186) and the fixed-point
+    # iteration (krylov.py:198-235) on the BASELINE cross geometry at N = 15
+    comp, f, _, _ = configs.build_cross_case("c0", api=API, N=15)
+    for pre in ("identity", "jacobi", "fft"):
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10, preconditioner=pre))
+        out[f"pre_iters_{pre}"] = np.array(rep.iterations)
+        for sid, fld in fields.items():
+            out[f"pre_p_{pre}_{sid}"] = fld.values
+    op = ddm.build_schur_operator(comp)
+    nbs = [nb for nb in op.neighbors]
+    fp = f[op.coupled_id].copy()
+    for nb in nbs:
+        q = rectsolver.solve_rect(nb.plan, f[nb.plan.subdomain.id]).values
+        fp = fp - nb.to_center.apply(q)
+    out["fp_rhs"] = fp
+    pc, rep = krylov.fixed_point(op, geometry.GridField(op.coupled_id, fp), max_iters=60, tol=1e-10)
+    out["fp_iters"] = np.array(rep.iterations)
+    out["fp_conv"] = np.array(rep.converged)
+    out["fp_hist"] = np.asarray(rep.residual_history)
+    out["fp_p"] = pc.values
     np.savez_compressed(os.path.join(HERE, "nn.npz"), **out)
     print("nn.npz written")
 

@@ -400,6 +400,31 @@ class TestInterfaceOnlyVariant:
             assert rel(v[idx].cpu().numpy(), g[f"val_{sid}"]) < 1e-10
 
 
+class TestComparisonStudies:
+    """identity / jacobi preconditioned GMRES (krylov.py:179-186) and the plain
+    fixed-point iteration (krylov.py:198-235) against reference runs."""
+
+    @pytest.mark.parametrize("pre", ["identity", "jacobi", "fft"])
+    def test_preconditioners(self, pre):
+        g = load_golden("nn")
+        comp, f, _, _ = configs.build_cross_case("c0", N=15)
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10, preconditioner=pre))
+        assert abs(rep.iterations - int(g[f"pre_iters_{pre}"])) <= 1
+        num = sum(float(np.sum((fields[s].values - g[f"pre_p_{pre}_{s}"]) ** 2)) for s in range(5))
+        den = sum(float(np.sum(g[f"pre_p_{pre}_{s}"] ** 2)) for s in range(5))
+        assert (num / den) ** 0.5 < 1e-9
+
+    def test_fixed_point(self):
+        from paper_2509_23180_b200.geometry import GridField
+        g = load_golden("nn")
+        comp, f, _, _ = configs.build_cross_case("c0", N=15)
+        op = ddm.build_schur_operator(comp)
+        pc, rep = krylov.fixed_point(op, GridField(op.coupled_id, g["fp_rhs"]), max_iters=60, tol=1e-10)
+        assert rep.iterations == int(g["fp_iters"]) and bool(rep.converged) == bool(g["fp_conv"])
+        np.testing.assert_allclose(rep.residual_history, g["fp_hist"], rtol=1e-9, atol=0)
+        assert rel(pc.values, g["fp_p"]) < 1e-10
+
+
 class TestDistDriver:
     def test_native_backend_single_rank(self, golden_small):
         """dist_ddm_solve with the GPU backend and no process group (one rank owns
