@@ -70,9 +70,11 @@ int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double
                         double mod_west, double mod_east, double mod_south, double mod_north,
                         int transform_axis, int device);
 /* General form: transform_pair 0 = DD (sine basis, DST-I), 1 = NN (shifted
- * cosine basis, DCT-II/III; transforms.py:32-33,83-98,106-134).  A DD axis
- * needs ghost-node ends; an NN axis's Neumann ends belong to its basis.  NN
- * runs on the dense periodic-table transform (n <= 1024). */
+ * cosine basis, DCT-II/III; transforms.py:32-33,83-98,106-134), 2 = PP (real
+ * Fourier basis, even n; transforms.py:34-35,114-126,139-148).  A DD axis
+ * needs ghost-node ends; NN/PP ends belong to the basis.  NN and PP run on
+ * the dense periodic-table transform (n <= 1024); the sweep axis must not be
+ * periodic. */
 int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double kappa,
                       double mod_west, double mod_east, double mod_south, double mod_north,
                       int transform_axis, int transform_pair, int device);
@@ -112,6 +114,11 @@ int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa,
  * to_center maps its line into the centre  (R_ci, ddm.py:85),
  * from_center maps the centre line into it (R_ic, ddm.py:86).
  * Index arrays are HOST int64 of length line_len[i]; they are copied. */
+/* Same with periodic axes (wrap-around neighbours instead of end modifiers,
+ * rectsolver.py:274-285). */
+int fd_stencil_apply_ex(int m, int n, double delta_x, double delta_y, double kappa,
+                        double mod_west, double mod_east, double mod_south, double mod_north,
+                        int periodic_x, int periodic_y, const double *v, double *out, void *stream);
 int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south,
                     double center_mod_north, int n_nb, const fd_plan *nb,
                     const int *line_len,

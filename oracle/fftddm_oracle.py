@@ -41,13 +41,18 @@ def eigenvalues_dd(n, delta_t, delta_o, kappa=0.0):
 
 
 def eigenvalues(bc, n, delta_t, delta_o, kappa=0.0):
-    """DD: cos(j pi/(n+1)); NN: cos((j-1) pi/n)   (transforms.py:26-38)."""
+    """DD: cos(j pi/(n+1)); NN: cos((j-1) pi/n); PP: cos(2 pi (j-1)/n)
+    (transforms.py:26-38)."""
     if bc == "DD":
         return eigenvalues_dd(n, delta_t, delta_o, kappa)
-    if bc != "NN":
-        raise NotImplementedError("oracle covers the DD and NN pairs")
     j = np.arange(1, n + 1, dtype=float)
-    return -2.0 * (delta_t + delta_o) + 2.0 * delta_t * np.cos((j - 1) * np.pi / n) + kappa
+    if bc == "NN":
+        c = np.cos((j - 1) * np.pi / n)
+    elif bc == "PP":
+        c = np.cos(2.0 * np.pi * (j - 1) / n)
+    else:
+        raise NotImplementedError(f"unknown pair {bc}")
+    return -2.0 * (delta_t + delta_o) + 2.0 * delta_t * c + kappa
 
 
 def dct2(v):
@@ -75,15 +80,49 @@ def nn_scale(n):
     return s
 
 
+def apply_q_pp(v):
+    """Real Fourier basis: cosine amplitudes to the real part, sine amplitudes
+    to the imaginary part of a half spectrum, one inverse FFT (transforms.py:114-126)."""
+    n = v.shape[-1]
+    spec = np.zeros(v.shape[:-1] + (n,), dtype=complex)
+    root = math.sqrt(1.0 / n)
+    spec[..., 0] = v[..., 0] * root
+    spec[..., n // 2] = v[..., n // 2] * root
+    if n > 2:
+        amp = math.sqrt(2.0 / n)
+        spec[..., 1:n // 2] = amp * v[..., 1:n // 2]
+        spec[..., n // 2 + 1:] = -1j * amp * v[..., n // 2 + 1:]
+    return n * np.fft.ifft(spec, axis=-1).real
+
+
+def apply_qt_pp(v):
+    """Q^T of the real Fourier basis through one FFT (transforms.py:139-148)."""
+    n = v.shape[-1]
+    spec = np.fft.fft(v, axis=-1)
+    out = np.empty_like(v)
+    root = math.sqrt(1.0 / n)
+    out[..., 0] = spec[..., 0].real * root
+    out[..., n // 2] = spec[..., n // 2].real * root
+    if n > 2:
+        amp = math.sqrt(2.0 / n)
+        out[..., 1:n // 2] = amp * spec[..., 1:n // 2].real
+        out[..., n // 2 + 1:] = -amp * spec[..., n // 2 + 1:].imag
+    return out
+
+
 def apply_q(bc, v):
-    """Q v along the last axis (transforms.py:106-113)."""
+    """Q v along the last axis (transforms.py:106-126)."""
     v = np.asarray(v, dtype=float)
+    if bc == "PP":
+        return apply_q_pp(v)
     return apply_q_dd(v) if bc == "DD" else dct3(nn_scale(v.shape[-1]) * v)
 
 
 def apply_qt(bc, v):
-    """Q^T v along the last axis (transforms.py:129-136)."""
+    """Q^T v along the last axis (transforms.py:129-148)."""
     v = np.asarray(v, dtype=float)
+    if bc == "PP":
+        return apply_qt_pp(v)
     return apply_q_dd(v) if bc == "DD" else nn_scale(v.shape[-1]) * dct2(v)
 
 
@@ -155,9 +194,9 @@ class OraclePlan:
 
 
 def transformable(sub, axis):
-    """Pure form: NN, or DD with ghost-node ends   (rectsolver.py:24-29)."""
+    """Pure form: NN or PP, or DD with ghost-node ends   (rectsolver.py:24-29)."""
     pair = sub.axis_pair(axis)
-    if pair == "NN":
+    if pair in ("NN", "PP"):
         return True
     lo, hi = ("west", "east") if axis == "x" else ("south", "north")
     return pair == "DD" and sub.end_modifier(lo) == 0.0 and sub.end_modifier(hi) == 0.0
@@ -203,18 +242,26 @@ def solve(pl: OraclePlan, f):
 
 
 def apply_operator(sub, v):
-    """5-point matvec with end modifiers, non-periodic axes (rectsolver.py:264-289)."""
+    """5-point matvec with end modifiers or periodic wrap (rectsolver.py:264-289)."""
     G = np.asarray(v, dtype=float).reshape(sub.m, sub.n)
     dx, dy = sub.delta_x, sub.delta_y
     out = (-2.0 * (dx + dy) + sub.kappa) * G
     out[:, 1:] += dy * G[:, :-1]
     out[:, :-1] += dy * G[:, 1:]
-    out[:, 0] += sub.end_modifier("south") * G[:, 0]
-    out[:, -1] += sub.end_modifier("north") * G[:, -1]
+    if sub.axis_pair("y") == "PP":
+        out[:, 0] += dy * G[:, -1]
+        out[:, -1] += dy * G[:, 0]
+    else:
+        out[:, 0] += sub.end_modifier("south") * G[:, 0]
+        out[:, -1] += sub.end_modifier("north") * G[:, -1]
     out[1:, :] += dx * G[:-1, :]
     out[:-1, :] += dx * G[1:, :]
-    out[0, :] += sub.end_modifier("west") * G[0, :]
-    out[-1, :] += sub.end_modifier("east") * G[-1, :]
+    if sub.axis_pair("x") == "PP":
+        out[0, :] += dx * G[-1, :]
+        out[-1, :] += dx * G[0, :]
+    else:
+        out[0, :] += sub.end_modifier("west") * G[0, :]
+        out[-1, :] += sub.end_modifier("east") * G[-1, :]
     return out.reshape(-1)
 
 

@@ -540,8 +540,8 @@ int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double k
     FD_API_BEGIN
     if (!out) FD_FAIL(FD_ERR_VALIDATION, "null output handle");
     *out = nullptr;
-    if (transform_pair != kPairDD && transform_pair != kPairNN)
-        FD_FAIL(FD_ERR_UNSUPPORTED, "transform pair must be DD (0) or NN (1)");
+    if (transform_pair != kPairDD && transform_pair != kPairNN && transform_pair != kPairPP)
+        FD_FAIL(FD_ERR_UNSUPPORTED, "transform pair must be DD (0), NN (1) or PP (2)");
     // a DD transform axis must carry ghost-node ends (no half-cell modifier,
     // rectsolver.py:24-29); an NN axis's Neumann ends are part of its basis
     const bool dd = transform_pair == kPairDD;
@@ -634,6 +634,16 @@ int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa,
     if (m < 1 || n < 1 || !v || !out) FD_FAIL(FD_ERR_VALIDATION, "bad stencil arguments");
     launch_stencil(m, n, delta_x, delta_y, kappa, mod_west, mod_east, mod_south, mod_north, v, out,
                    S(stream));
+    FD_API_END
+}
+
+int fd_stencil_apply_ex(int m, int n, double delta_x, double delta_y, double kappa, double mod_west,
+                        double mod_east, double mod_south, double mod_north, int periodic_x,
+                        int periodic_y, const double *v, double *out, void *stream) {
+    FD_API_BEGIN
+    if (m < 1 || n < 1 || !v || !out) FD_FAIL(FD_ERR_VALIDATION, "bad stencil arguments");
+    launch_stencil(m, n, delta_x, delta_y, kappa, mod_west, mod_east, mod_south, mod_north, v, out,
+                   S(stream), periodic_x, periodic_y);
     FD_API_END
 }
 

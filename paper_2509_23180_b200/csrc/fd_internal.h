@@ -60,11 +60,11 @@ struct PlanDev {
     const double *dense; // [n][n] sin table (dense transform) or nullptr
     const double2 *tw;   // FFT twiddles e^{-2 pi i t / L}, t < L = 2(n+1), or nullptr
     const double *ralpha;// [n+1] real-DST pre-weights (rsolve.cu), alpha_j = s/2 sin(pi j/N) + s/4
-    int tpair;           // transform-axis pair: kPairDD (sine basis) or kPairNN (shifted cosine)
+    int tpair;           // transform-axis pair: kPairDD (sine), kPairNN (shifted cosine), kPairPP (real Fourier)
 };
 
 // transform-axis BC pairs (reference transforms.BC_PAIRS, transforms.py:24)
-enum TransformPair { kPairDD = 0, kPairNN = 1 };
+enum TransformPair { kPairDD = 0, kPairNN = 1, kPairPP = 2 };
 
 // ---------------------------------------------------------------------------
 // Geometry of the real-symmetric persistent solve (rsolve.cu), shared with the
@@ -183,7 +183,8 @@ const double *dense_table_for(int device, int n, int pair = kPairDD);
 
 // vector kernels (ops.cu)
 void launch_stencil(int m, int n, double delta_x, double delta_y, double kappa, double mw,
-                    double me, double ms, double mn, const double *v, double *out, cudaStream_t s);
+                    double me, double ms, double mn, const double *v, double *out, cudaStream_t s,
+                    int ppx = 0, int ppy = 0);
 inline void launch_stencil(const Plan &p, double ms, double mn, const double *v, double *out,
                            cudaStream_t s) {
     launch_stencil(p.m, p.n, p.delta_x, p.delta_y, p.kappa, p.mod_w, p.mod_e, ms, mn, v, out, s);

@@ -17,7 +17,7 @@ namespace fd {
 // before it is added, exactly as numpy's `out[...] += d * G[...]`.
 __global__ void stencil_kernel(int m, int n, double c0, double dx, double dy, double mw, double me,
                                double ms, double mn, const double *__restrict__ v,
-                               double *__restrict__ out) {
+                               double *__restrict__ out, int ppx, int ppy) {
     const long long total = (long long)m * n;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -26,12 +26,22 @@ __global__ void stencil_kernel(int m, int n, double c0, double dx, double dy, do
         double a = __dmul_rn(c0, g);
         if (j > 0) a = __dadd_rn(a, __dmul_rn(dy, v[idx - 1]));
         if (j < n - 1) a = __dadd_rn(a, __dmul_rn(dy, v[idx + 1]));
-        if (j == 0) a = __dadd_rn(a, __dmul_rn(ms, g));
-        if (j == n - 1) a = __dadd_rn(a, __dmul_rn(mn, g));
+        if (ppy) {   // periodic y: wrap-around neighbours (rectsolver.py:274-276)
+            if (j == 0) a = __dadd_rn(a, __dmul_rn(dy, v[idx + n - 1]));
+            if (j == n - 1) a = __dadd_rn(a, __dmul_rn(dy, v[idx - (n - 1)]));
+        } else {
+            if (j == 0) a = __dadd_rn(a, __dmul_rn(ms, g));
+            if (j == n - 1) a = __dadd_rn(a, __dmul_rn(mn, g));
+        }
         if (i > 0) a = __dadd_rn(a, __dmul_rn(dx, v[idx - n]));
         if (i < m - 1) a = __dadd_rn(a, __dmul_rn(dx, v[idx + n]));
-        if (i == 0) a = __dadd_rn(a, __dmul_rn(mw, g));
-        if (i == m - 1) a = __dadd_rn(a, __dmul_rn(me, g));
+        if (ppx) {   // periodic x (rectsolver.py:283-285)
+            if (i == 0) a = __dadd_rn(a, __dmul_rn(dx, v[idx + (long long)(m - 1) * n]));
+            if (i == m - 1) a = __dadd_rn(a, __dmul_rn(dx, v[idx - (long long)(m - 1) * n]));
+        } else {
+            if (i == 0) a = __dadd_rn(a, __dmul_rn(mw, g));
+            if (i == m - 1) a = __dadd_rn(a, __dmul_rn(me, g));
+        }
         out[idx] = a;
     }
 }
@@ -43,11 +53,12 @@ static int grid_for(long long N, int threads) {
 }
 
 void launch_stencil(int m, int n, double delta_x, double delta_y, double kappa, double mw,
-                    double me, double ms, double mn, const double *v, double *out, cudaStream_t s) {
+                    double me, double ms, double mn, const double *v, double *out, cudaStream_t s,
+                    int ppx, int ppy) {
     const double c0 = -2.0 * (delta_x + delta_y) + kappa;   // rectsolver.py:270
     const long long N = (long long)m * n;
     stencil_kernel<<<grid_for(N, 256), 256, 0, s>>>(m, n, c0, delta_x, delta_y, mw, me, ms, mn, v,
-                                                    out);
+                                                    out, ppx, ppy);
     FD_CUDA(cudaGetLastError());
 }
 

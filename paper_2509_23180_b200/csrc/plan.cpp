@@ -39,6 +39,12 @@ double eig_dd(int k, int n, double dt, double dor, double kappa) {
     double lam = -2.0 * (dt + dor) + (2.0 * dt) * cos(arg);
     return lam + kappa;
 }
+// PP: cos(2 pi (j - 1) / n), j = 1..n   (transforms.py:34-35)
+double eig_pp(int k, int n, double dt, double dor, double kappa) {
+    const double arg = 2.0 * M_PI * double(k) / double(n);
+    double lam = -2.0 * (dt + dor) + (2.0 * dt) * cos(arg);
+    return lam + kappa;
+}
 // NN: cos((j - 1) pi / n), j = 1..n   (transforms.py:32-33)
 double eig_nn(int k, int n, double dt, double dor, double kappa) {
     const double jm1 = double(k);
@@ -174,7 +180,8 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
     std::vector<double> lam(n);
     double amax = 0.0;
     for (int k = 0; k < n; ++k) {
-        lam[k] = pair == kPairNN ? eig_nn(k, n, delta_y, delta_x, kappa) : eig_dd(k, n, delta_y, delta_x, kappa);
+        lam[k] = pair == kPairNN ? eig_nn(k, n, delta_y, delta_x, kappa)
+                 : pair == kPairPP ? eig_pp(k, n, delta_y, delta_x, kappa) : eig_dd(k, n, delta_y, delta_x, kappa);
         amax = std::max(amax, fabs(lam[k]));
     }
     const double tol = 1e-13 * std::max(amax, off);   // rectsolver.py:135
@@ -350,7 +357,14 @@ const double *dense_table_for(int device, int n, int pair) {
     if (it != g_dense.end()) return (const double *)it->second;
     const long double PI_L = 3.141592653589793238462643383279502884L;
     std::vector<double> h;
-    if (pair == kPairNN) {
+    if (pair == kPairPP) {
+        // cos(2 pi q / n), q < n, then sin(2 pi q / n), q < n: the real Fourier basis at q = o i mod n
+        h.resize(2 * size_t(n));
+        for (long long q = 0; q < n; ++q) {
+            h[q] = (double)cosl(2.0L * PI_L * (long double)q / (long double)n);
+            h[n + q] = (double)sinl(2.0L * PI_L * (long double)q / (long double)n);
+        }
+    } else if (pair == kPairNN) {
         // cos(pi q / 2n), q < 4n: the dense DCT-II/III read their basis at q = o(2i+1) / i(2o+1) mod 4n
         h.resize(4 * size_t(n));
         for (long long q = 0; q < 4LL * n; ++q) h[q] = (double)cosl(PI_L * (long double)q / (2.0L * (long double)n));
@@ -420,7 +434,7 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.mod_w = mod_w;
         d.mod_e = mod_e;
         d.tpair = pair;
-        d.scale = pair == kPairNN ? sqrt(2.0 / n) : sqrt(2.0 / (n + 1));
+        d.scale = (pair == kPairNN || pair == kPairPP) ? sqrt(2.0 / n) : sqrt(2.0 / (n + 1));
         d.ex_off = upload(p, T.off);
         d.ex_len = upload(p, T.len);
         d.ex = upload(p, T.ex);

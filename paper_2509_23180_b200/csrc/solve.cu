@@ -88,18 +88,27 @@ struct InvT<FftDst<LG>> {
 // (mod the period).  DD (both directions): T = sin(pi q/(n+1)), q = (i+1)(o+1).
 // NN forward (Q^T, transforms.py:83-90,129-134): T = cos(pi q/2n), q = o(2i+1);
 // NN inverse (Q, transforms.py:92-98,106-109): q = i(2o+1), input 0 scaled by
-// 1/sqrt(2) (the basis' sqrt(1/n) vs sqrt(2/n)).
+// 1/sqrt(2) (the basis' sqrt(1/n) vs sqrt(2/n)).  PP (real Fourier basis,
+// transforms.py:114-126,139-148): T = cos(2 pi q/n) for basis index <= n/2,
+// sin(2 pi q/n) above (table halves), q = o i mod n; basis 0 and n/2 carry
+// sqrt(1/n) (a 1/sqrt(2) on the output forward, on the input inverse).
 template <int M, int NT_>
 __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const double *tab,
                                            double (&acc)[DenseDstT<M, NT_>::G][M], int pair, bool inverse) {
     constexpr int NT = DenseDstT<M, NT_>::NT, G = DenseDstT<M, NT_>::G;
-    const bool nn = pair == kPairNN;
-    const int period = nn ? 4 * n : 2 * (n + 1);
-    int idx[M], step[M];
+    const bool nn = pair == kPairNN, pp = pair == kPairPP;
+    const int period = nn ? 4 * n : pp ? n : 2 * (n + 1);
+    const int half = n >> 1;
+    int idx[M], step[M], toff[M];
 #pragma unroll
     for (int u = 0; u < M; ++u) {
         const int o = threadIdx.x + u * NT;
-        if (!nn) {
+        toff[u] = 0;
+        if (pp) {
+            idx[u] = 0;            // o i mod n at i = 0
+            step[u] = o;
+            if (!inverse && o > half) toff[u] = n;   // sine half of the table
+        } else if (!nn) {
             idx[u] = o + 1;        // (i + 1)(o + 1) at i = 0
             step[u] = o + 1;
         } else if (!inverse) {
@@ -115,14 +124,15 @@ __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const do
 #pragma unroll 2
     for (int j = 0; j < n; ++j) {
         double x[G];
-        const double xs = (nn && inverse && j == 0) ? 0.70710678118654752440 : 1.0;
+        const double xs = ((nn || pp) && inverse && (j == 0 || (pp && j == half))) ? 0.70710678118654752440 : 1.0;
+        const int joff = (pp && inverse && j > half) ? n : 0;   // inverse: the input's basis picks the half
 #pragma unroll
         for (int g = 0; g < G; ++g) x[g] = rowbuf[g * n + j] * xs;
 #pragma unroll
         for (int u = 0; u < M; ++u) {
             const int o = threadIdx.x + u * NT;
             if (o < n) {
-                const double sv = tab[idx[u]];
+                const double sv = tab[idx[u] + toff[u] + joff];
 #pragma unroll
                 for (int g = 0; g < G; ++g) acc[g][u] = fma(sv, x[g], acc[g][u]);
                 idx[u] += step[u];
@@ -130,10 +140,10 @@ __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const do
             }
         }
     }
-    if (nn && !inverse) {   // output 0 carries sqrt(1/n) instead of sqrt(2/n)
+    if ((nn || pp) && !inverse) {   // output 0 (and n/2 for PP) carries sqrt(1/n) instead of sqrt(2/n)
 #pragma unroll
         for (int u = 0; u < M; ++u)
-            if (threadIdx.x + u * NT == 0)
+            if (threadIdx.x + u * NT == 0 || (pp && threadIdx.x + u * NT == half))
 #pragma unroll
                 for (int g = 0; g < G; ++g) acc[g][u] *= 0.70710678118654752440;
     }
@@ -146,7 +156,7 @@ __device__ __forceinline__ double *dense_tab(double2 *smem) {
 
 template <int M, int NT_>
 __device__ __forceinline__ void stage_tab(double *tab, int n, const PlanDev &p) {
-    const int period = p.tpair == kPairNN ? 4 * n : 2 * (n + 1);
+    const int period = p.tpair == kPairNN ? 4 * n : p.tpair == kPairPP ? 2 * n : 2 * (n + 1);
     for (int q = threadIdx.x; q < period; q += DenseDstT<M, NT_>::NT) tab[q] = __ldg(p.dense + q);
 }
 
@@ -451,6 +461,7 @@ __global__ void __launch_bounds__(P::NT) dst_rows_kernel(int rows_total, int n, 
 int transform_kind(int n, int pair) {
     const int N = n + 1;
     if (pair == kPairDD && (N & (N - 1)) == 0 && N >= 256 && N <= 4096) return kFFT;
+    if (pair == kPairPP && (n & 1)) return -1;   // periodic transforms need an even length
     if (n <= kDenseMax) return kDense;   // any pair: periodic-table dense transform
     return -1;
 }

@@ -248,6 +248,9 @@ def build_schur_operator(comp: CompositeDomain, coupled_id: int | None = None,
     if coupled_id is None:
         coupled_id = designate_center(comp)
     center = comp.subdomain(coupled_id)
+    if "PP" in (center.axis_pair("x"), center.axis_pair("y")):
+        from ._native import UnsupportedError
+        raise UnsupportedError("a periodic coupled subdomain is not on the GPU path")
     neighbors = []
     for iface in comp.interfaces_of(coupled_id):
         other = iface.other_side(coupled_id)[0]

@@ -24,7 +24,7 @@ from .errors import SingularOperatorError, ValidationError
 from .geometry import BoundaryKind, GridField, RectSubdomain
 
 
-_PAIR_CODE = {"DD": 0, "NN": 1}
+_PAIR_CODE = {"DD": 0, "NN": 1, "PP": 2}
 
 
 def _gpu_axis(sub: RectSubdomain) -> str:
@@ -35,8 +35,8 @@ def _gpu_axis(sub: RectSubdomain) -> str:
     e.g. the c4 south/north arms, n = 16383) moves the transform to a
     transformable x axis (the reference's own transform_axis = "x" branch):
     the FFT stays within one SM's shared memory and the long axis becomes the
-    Thomas sweep.  Same operator, rounding-level differences only.  Periodic
-    (PP) pairs are not on the GPU path."""
+    Thomas sweep.  Same operator, rounding-level differences only.  A periodic
+    sweep axis (cyclic Thomas) is not on the GPU path."""
     def pair_of(axis):
         try:
             return sub.axis_pair(axis)
@@ -45,7 +45,7 @@ def _gpu_axis(sub: RectSubdomain) -> str:
 
     def ok(axis):
         pair = pair_of(axis)
-        if pair == "NN":
+        if pair in ("NN", "PP"):
             return True
         lo, hi = ("south", "north") if axis == "y" else ("west", "east")
         return pair == "DD" and not sub.end_modifier(lo) and not sub.end_modifier(hi)
@@ -173,14 +173,13 @@ def solve_rect_batched(plans, fields, out=None):
 
 
 def apply_rect_operator(sub: RectSubdomain, values):
-    """5-point matvec with end modifiers (ref rectsolver.py:264-289), non-periodic."""
-    if sub.axis_pair("x") == "PP" or sub.axis_pair("y") == "PP":
-        raise UnsupportedError("periodic stencils are not on the GPU path")
+    """5-point matvec with end modifiers or periodic wrap (ref rectsolver.py:264-289)."""
     v, host = to_device(values, sub.size)
     out = empty(sub.size)
-    _native.call("fd_stencil_apply", sub.m, sub.n, float(sub.delta_x), float(sub.delta_y),
+    ppx, ppy = int(sub.axis_pair("x") == "PP"), int(sub.axis_pair("y") == "PP")
+    _native.call("fd_stencil_apply_ex", sub.m, sub.n, float(sub.delta_x), float(sub.delta_y),
                  float(sub.kappa), float(sub.end_modifier("west")), float(sub.end_modifier("east")),
-                 float(sub.end_modifier("south")), float(sub.end_modifier("north")),
+                 float(sub.end_modifier("south")), float(sub.end_modifier("north")), ppx, ppy,
                  _native.dptr(v), _native.dptr(out), _native.stream_ptr())
     return like_input(out, host)
 

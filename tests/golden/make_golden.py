@@ -45,7 +45,7 @@ def sample_idx(size, sid):
 
 
 def rect(m, n, dx, dy, kappa, bc, half=()):
-    kinds = {"D": B.DIRICHLET, "N": B.NEUMANN, "I": B.INTERFACE}
+    kinds = {"D": B.DIRICHLET, "N": B.NEUMANN, "I": B.INTERFACE, "P": B.PERIODIC}
     edge_bc = {e: kinds[c] for e, c in zip(("west", "east", "south", "north"), bc)}
     return geometry.RectSubdomain(id=0, origin=(0.0, 0.0), m=m, n=n, dx=dx, dy=dy,
                                   edge_bc=edge_bc, kappa=kappa,
@@ -179,6 +179,11 @@ NN_RECT_CASES = [
     (16, 10, 0.1, 0.1, 0.0, "NNDD", ("south",)),      # y has a half-cell end -> NN along x
     (40, 24, 1.0 / 40, 1.0 / 24, -10.0, "NNDD", ("north", "south")),
     (130, 141, 1.0 / 141, 1.0 / 141, 0.0, "DDNN", ("east",)),
+    # PP (real Fourier) transform axes
+    (12, 16, 0.1, 0.1, 0.0, "DDPP", ()),
+    (33, 64, 0.03, 1.0 / 64, -2.0, "NNPP", ("west",)),
+    (18, 10, 0.1, 0.1, -1.0, "PPDD", ("south",)),
+    (64, 256, 1.0 / 64, 1.0 / 256, 0.0, "IDPP", ("east",)),
 ]
 
 

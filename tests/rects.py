@@ -19,7 +19,8 @@ RECT_CASES = [
     (40, 1023, 1.0 / 1023, 1.0 / 1023, -10.0, "DDDD", ()),
 ]
 
-_K = {"D": BoundaryKind.DIRICHLET, "N": BoundaryKind.NEUMANN, "I": BoundaryKind.INTERFACE}
+_K = {"D": BoundaryKind.DIRICHLET, "N": BoundaryKind.NEUMANN, "I": BoundaryKind.INTERFACE,
+      "P": BoundaryKind.PERIODIC}
 
 
 def make(case, sid=0):

@@ -324,11 +324,16 @@ NN_RECT_CASES = [
     (16, 10, 0.1, 0.1, 0.0, "NNDD", ("south",)),
     (40, 24, 1.0 / 40, 1.0 / 24, -10.0, "NNDD", ("north", "south")),
     (130, 141, 1.0 / 141, 1.0 / 141, 0.0, "DDNN", ("east",)),
+    (12, 16, 0.1, 0.1, 0.0, "DDPP", ()),
+    (33, 64, 0.03, 1.0 / 64, -2.0, "NNPP", ("west",)),
+    (18, 10, 0.1, 0.1, -1.0, "PPDD", ("south",)),
+    (64, 256, 1.0 / 64, 1.0 / 256, 0.0, "IDPP", ("east",)),
 ]
 
 
 class TestNeumannTransform:
-    """NN (shifted-cosine) transform axes on the dense periodic-table path and
+    """NN (shifted-cosine) and PP (real Fourier) transform axes on the dense
+    periodic-table path and
     the reference's own test cross (Neumann flanks, half-cell arm ends),
     against fixtures written by the reference."""
 
@@ -340,6 +345,18 @@ class TestNeumannTransform:
         assert pl.transform_axis == str(g[f"nn_axis_{c}"])
         p = rectsolver.solve_rect(pl, g[f"nn_f_{c}"]).values
         assert rel(p, g[f"nn_p_{c}"]) < 1e-12
+
+    @pytest.mark.parametrize("n", [2, 8, 64, 142, 1000])
+    def test_periodic_against_oracle_and_residual(self, n, rng):
+        """PP transform axis (even n), half-cell sweep end; A p = f with the
+        periodic wrap stencil (rectsolver.py:274-276)."""
+        sub = make((21, n, 1.0 / 21, 1.0 / max(n, 2), -0.5, "DDPP", ("east",)))
+        f = rng.uniform(-1, 1, sub.size)
+        p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f).values
+        assert rel(p, O.solve(O.plan(sub), f)) < 1e-12
+        r = rectsolver.apply_rect_operator(sub, p) - f
+        assert np.linalg.norm(r) / np.linalg.norm(f) < 1e-11
+        np.testing.assert_array_equal(rectsolver.apply_rect_operator(sub, f), O.apply_operator(sub, f))
 
     @pytest.mark.parametrize("n", [1, 2, 7, 64, 141, 1000])
     def test_against_oracle_and_residual(self, n, rng):

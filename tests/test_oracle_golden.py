@@ -101,6 +101,10 @@ NN_RECT_CASES = [
     (16, 10, 0.1, 0.1, 0.0, "NNDD", ("south",)),
     (40, 24, 1.0 / 40, 1.0 / 24, -10.0, "NNDD", ("north", "south")),
     (130, 141, 1.0 / 141, 1.0 / 141, 0.0, "DDNN", ("east",)),
+    (12, 16, 0.1, 0.1, 0.0, "DDPP", ()),
+    (33, 64, 0.03, 1.0 / 64, -2.0, "NNPP", ("west",)),
+    (18, 10, 0.1, 0.1, -1.0, "PPDD", ("south",)),
+    (64, 256, 1.0 / 64, 1.0 / 256, 0.0, "IDPP", ("east",)),
 ]
 
 
