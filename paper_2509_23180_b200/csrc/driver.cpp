@@ -80,21 +80,47 @@ struct Scratch {
     double *hval;      // pinned host mirror
     int cap;
 };
+// Pinned host mirrors for the per-iteration scalar read-backs: page-locked
+// allocations cost milliseconds, so released blocks are kept for reuse (one
+// size class; the few blocks a process needs are never returned to the OS).
+static std::mutex g_pin_mu;
+static std::vector<void *> *g_pin_free = new std::vector<void *>();   // never destroyed
+constexpr size_t kPinBytes = 8192;
+static void *pinned_get(size_t bytes) {
+    if (bytes > kPinBytes) throw Error{FD_ERR_VALIDATION, "pinned mirror too large"};
+    {
+        std::lock_guard<std::mutex> g(g_pin_mu);
+        if (!g_pin_free->empty()) {
+            void *p = g_pin_free->back();
+            g_pin_free->pop_back();
+            return p;
+        }
+    }
+    void *p = nullptr;
+    FD_CUDA(cudaMallocHost(&p, kPinBytes));
+    return p;
+}
+static void pinned_put(void *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    g_pin_free->push_back(p);
+}
+
 static Scratch make_scratch(int cap) {
     Scratch s{};
-    FD_CUDA(cudaMalloc(&s.red.partials, sizeof(double) * kRedBlocks));
-    FD_CUDA(cudaMalloc(&s.red.counter, sizeof(unsigned int)));
+    s.red.partials = (double *)dmalloc(sizeof(double) * kRedBlocks);
+    s.red.counter = (unsigned int *)dmalloc(sizeof(unsigned int));
     FD_CUDA(cudaMemset(s.red.counter, 0, sizeof(unsigned int)));
-    FD_CUDA(cudaMalloc(&s.dval, sizeof(double) * cap));
-    FD_CUDA(cudaMallocHost(&s.hval, sizeof(double) * cap));
+    s.dval = (double *)dmalloc(sizeof(double) * cap);
+    s.hval = (double *)pinned_get(sizeof(double) * cap);
     s.cap = cap;
     return s;
 }
-static void free_scratch(Scratch &s) {
-    cudaFree(s.red.partials);
-    cudaFree(s.red.counter);
-    cudaFree(s.dval);
-    cudaFreeHost(s.hval);
+static void free_scratch(Scratch &s) {   // callers synchronise the device first
+    dfree(s.red.partials);
+    dfree(s.red.counter);
+    dfree(s.dval);
+    pinned_put(s.hval);
 }
 static std::mutex g_scr_mu;
 static std::map<int, Scratch> g_scratch;
@@ -332,7 +358,7 @@ static void ensure_arnoldi(fd_schur_s *op) {
     FD_CUDA(cudaMemset(op->arn.counter, 0, sizeof(unsigned int)));
     op->arn.G = (double *)dalloc(op, sizeof(double) * kMaxArnoldi * kMaxArnoldi);
     op->arn_out = (double *)dalloc(op, sizeof(double) * (2 * kMaxArnoldi + 4));
-    FD_CUDA(cudaMallocHost(&op->arn_host, sizeof(double) * (2 * kMaxArnoldi + 4)));
+    op->arn_host = (double *)pinned_get(sizeof(double) * (2 * kMaxArnoldi + 4));
 }
 
 // Arnoldi step on the operator's basis with the low-synchronisation MGS of
@@ -757,7 +783,7 @@ int fd_schur_destroy(fd_schur op) {
         for (void *a : op->allocs) dfree(a);
         if (op->V) dfree(op->V);
         if (op->sc.cap) free_scratch(op->sc);
-        if (op->arn_host) cudaFreeHost(op->arn_host);
+        pinned_put(op->arn_host);
         delete op;
         ht.mark("done", 0, false);
     }
