@@ -106,6 +106,11 @@ int fd_dst_rows(int rows, int n, const double *in, double *out, int device, void
 /* --- rectsolver.apply_rect_operator (rectsolver.py:264-289), non-periodic:
  * out = 5-point stencil of v on an m x n grid, delta = 1/h^2, end modifiers
  * mod_* on the four boundary-adjacent lines (geometry.py:118-128). */
+/* apply_Q (inverse = 1) / apply_Qt (inverse = 0) of any pair along rows of
+ * length n (transforms.py:106-148): DD on the FFT or dense path, NN and PP on
+ * the dense periodic-table path (n <= 1024, PP even n). */
+int fd_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out, int device,
+                      void *stream);
 int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa,
                      double mod_west, double mod_east, double mod_south, double mod_north,
                      const double *v, double *out, void *stream);

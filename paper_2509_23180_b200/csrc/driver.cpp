@@ -653,6 +653,21 @@ int fd_dst_rows(int rows, int n, const double *in, double *out, int device, void
     FD_API_END
 }
 
+int fd_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out, int device,
+                      void *stream) {
+    FD_API_BEGIN
+    if (rows < 0 || n < 1 || !in || !out) FD_FAIL(FD_ERR_VALIDATION, "bad transform arguments");
+    if (pair != kPairDD && pair != kPairNN && pair != kPairPP) FD_FAIL(FD_ERR_UNSUPPORTED, "unknown transform pair");
+    const int tk = transform_kind(n, pair);
+    if (tk < 0) FD_FAIL(FD_ERR_UNSUPPORTED, "no GPU transform for this length and pair");
+    FD_CUDA(cudaSetDevice(device));
+    if (tk == kFFT)   // DD: Q = Q^T
+        launch_dst_rows(rows, n, in, out, twiddles_for(device, n), nullptr, S(stream));
+    else
+        launch_transform_rows(rows, n, pair, inverse, in, out, dense_table_for(device, n, pair), S(stream));
+    FD_API_END
+}
+
 int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa, double mod_west,
                      double mod_east, double mod_south, double mod_north, const double *v,
                      double *out, void *stream) {

@@ -176,6 +176,8 @@ int rows_per_block(int n, int pair = kPairDD);
 int transform_kind(int n, int pair = kPairDD);
 void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s);
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
+void launch_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out,
+                           const double *dense, cudaStream_t s);
 void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,
                      const double *dense, cudaStream_t s);
 const double2 *twiddles_for(int device, int n);

@@ -456,6 +456,24 @@ __global__ void __launch_bounds__(P::NT) dst_rows_kernel(int rows_total, int n, 
     InvT<P>::run(rowbuf, rows, n, out + size_t(g0) * n, nullptr, 1.0, 0.0, smem, p);
 }
 
+// dense basis transform of rows (any pair): forward = Q^T, inverse = Q
+template <class P>
+__global__ void __launch_bounds__(P::NT) dense_rows_kernel(int rows_total, int n, const double *in,
+                                                           double *out, PlanDev p, int inverse) {
+    extern __shared__ __align__(16) double2 smem[];
+    double *rowbuf = reinterpret_cast<double *>(smem);
+    const int g0 = blockIdx.x * P::G;
+    const int rows = min(P::G, rows_total - g0);
+    if (inverse) {
+        for (int idx = threadIdx.x; idx < rows * n; idx += P::NT) rowbuf[idx] = in[size_t(g0) * n + idx];
+        __syncthreads();
+        InvT<P>::run(rowbuf, rows, n, out + size_t(g0) * n, nullptr, 1.0, 0.0, smem, p);
+    } else {
+        FwdT<P>::run(in + size_t(g0) * n, rows, n, rowbuf, smem, p);
+        for (int idx = threadIdx.x; idx < rows * n; idx += P::NT) out[size_t(g0) * n + idx] = rowbuf[idx];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 int transform_kind(int n, int pair) {
@@ -563,6 +581,31 @@ void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
         default:
             FD_FAIL(FD_ERR_UNSUPPORTED, "no transform for this length");
     }
+}
+
+template <class P>
+static void run_dense_rows(int rows, int n, int pair, int inverse, const double *in, double *out,
+                           const double *dense, cudaStream_t s) {
+    PlanDev p{};
+    p.n = n;
+    p.tpair = pair;
+    p.scale = (pair == kPairNN || pair == kPairPP) ? sqrt(2.0 / n) : sqrt(2.0 / (n + 1));
+    p.dense = dense;
+    setup_smem<P>((const void *)dense_rows_kernel<P>);
+    const int grid = (rows + P::G - 1) / P::G;
+    dense_rows_kernel<P><<<grid, P::NT, P::SMEM, s>>>(rows, n, in, out, p, inverse);
+    FD_CUDA(cudaGetLastError());
+}
+
+void launch_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out,
+                           const double *dense, cudaStream_t s) {
+    if (rows <= 0) return;
+    if (!dense) FD_FAIL(FD_ERR_UNSUPPORTED, "no dense table for this transform");
+    if (n <= 128) run_dense_rows<DenseDstT<1, 128>>(rows, n, pair, inverse, in, out, dense, s);
+    else if (n <= 160) run_dense_rows<DenseDstT<1, 160>>(rows, n, pair, inverse, in, out, dense, s);
+    else if (n <= 256) run_dense_rows<DenseDstT<1, 256>>(rows, n, pair, inverse, in, out, dense, s);
+    else if (n <= 512) run_dense_rows<DenseDstT<2, 256>>(rows, n, pair, inverse, in, out, dense, s);
+    else run_dense_rows<DenseDstT<4, 256>>(rows, n, pair, inverse, in, out, dense, s);
 }
 
 void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,

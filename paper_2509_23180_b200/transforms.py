@@ -3,10 +3,9 @@
 `eigenvalues`/`make_plan` are host-side setup (O(n)).  `apply_Q`/`apply_Qt`
 for the Dirichlet-Dirichlet pair run the sm_100a DST-I kernel (Q = Q^T =
 sqrt(2/(n+1)) DST-I, transforms.py:112-113,135-136) on torch CUDA tensors;
-numpy input is copied to the device and the result back.  The NN pair runs
-inside the rectangle solves (dense DCT-II/III, csrc/solve.cu); the standalone
-apply_Q/apply_Qt entry points cover DD, and PP is not on the GPU path
-(UnsupportedError).
+numpy input is copied to the device and the result back.  NN (DCT-II/III)
+and PP (real Fourier) run on the dense periodic-table transform (n <= 1024,
+PP even n); other lengths raise UnsupportedError.
 """
 
 from __future__ import annotations
@@ -58,9 +57,10 @@ def make_plan(bc: str, n: int, delta_t: float, delta_o: float, kappa: float = 0.
     return SpectralPlan(bc, n, delta_t, delta_o, kappa, lam)
 
 
-def _apply(plan: SpectralPlan, v):
-    if plan.bc != "DD":
-        raise UnsupportedError(f"{plan.bc} transforms are not on the GPU path")
+_PAIR = {"DD": 0, "NN": 1, "PP": 2}
+
+
+def _apply(plan: SpectralPlan, v, inverse: bool):
     require_cuda()
     t = _native.torch()
     host = not is_torch(v)
@@ -70,17 +70,17 @@ def _apply(plan: SpectralPlan, v):
     shape = x.shape
     rows = x.reshape(-1, plan.n).to(device="cuda", dtype=t.float64).contiguous()
     out = t.empty_like(rows)
-    _native.call("fd_dst_rows", rows.shape[0], plan.n, _native.dptr(rows), _native.dptr(out),
-                 t.cuda.current_device(), _native.stream_ptr())
+    _native.call("fd_transform_rows", rows.shape[0], plan.n, _PAIR[plan.bc], int(inverse),
+                 _native.dptr(rows), _native.dptr(out), t.cuda.current_device(), _native.stream_ptr())
     out = out.reshape(shape)
     return out.cpu().numpy() if host else out
 
 
 def apply_Q(plan: SpectralPlan, v):
-    """Q @ v along the last axis (ref transforms.py:106-113)."""
-    return _apply(plan, v)
+    """Q @ v along the last axis (ref transforms.py:106-126)."""
+    return _apply(plan, v, True)
 
 
 def apply_Qt(plan: SpectralPlan, v):
-    """Q^T @ v along the last axis; Q is symmetric for DD (ref transforms.py:129-136)."""
-    return _apply(plan, v)
+    """Q^T @ v along the last axis; Q is symmetric for DD (ref transforms.py:129-148)."""
+    return _apply(plan, v, False)

@@ -442,6 +442,22 @@ class TestComparisonStudies:
         assert rel(pc.values, g["fp_p"]) < 1e-10
 
 
+class TestTransformPairs:
+    """apply_Q / apply_Qt for every pair (transforms.py:106-148) against the
+    oracle's restatement of the reference's FFT formulations."""
+
+    @pytest.mark.parametrize("bc,n", [("DD", 7), ("DD", 1023), ("NN", 1), ("NN", 16), ("NN", 141), ("NN", 1000),
+                                      ("PP", 2), ("PP", 16), ("PP", 142), ("PP", 1024)])
+    def test_q_and_qt(self, bc, n, rng):
+        pl = transforms.make_plan(bc, n, 1.0, 1.0)
+        x = rng.standard_normal((5, n))
+        q = transforms.apply_Q(pl, x)
+        qt = transforms.apply_Qt(pl, x)
+        assert rel(q, O.apply_q(bc, x)) < 1e-13
+        assert rel(qt, O.apply_qt(bc, x)) < 1e-13
+        assert rel(transforms.apply_Qt(pl, q), x) < 1e-13   # orthonormal
+
+
 class TestDistDriver:
     def test_native_backend_single_rank(self, golden_small):
         """dist_ddm_solve with the GPU backend and no process group (one rank owns
