@@ -111,6 +111,15 @@ int fd_dst_rows(int rows, int n, const double *in, double *out, int device, void
  * the dense periodic-table path (n <= 1024, PP even n). */
 int fd_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out, int device,
                       void *stream);
+/* Device-side problem assembly: f = lap p + kappa p at the
+ * cell-centred nodes (origin + (i - 1/2) h, geometry.py:82-86) of an m x n
+ * rectangle, minus lift_e * delta * p(ghost) on the line next to each edge
+ * with a nonzero lift factor (1 ghost-node, 2 half-cell Dirichlet;
+ * rectsolver.py:292-313); exact (optional) = p.  solution 0: sin(pi x)
+ * sin(pi y) + e^(x+y)/e^2, 1: sin(pi x) sin(pi y). */
+int fd_assemble_rhs(int m, int n, double x0, double y0, double dx, double dy, double kappa, int solution,
+                    double lift_west, double lift_east, double lift_south, double lift_north, double *f,
+                    double *exact, void *stream);
 int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa,
                      double mod_west, double mod_east, double mod_south, double mod_north,
                      const double *v, double *out, void *stream);

@@ -25,7 +25,7 @@ EXPORTS = (
     "fd_transform_kind", "fd_transform_kind_pair",
     "fd_plan_destroy", "fd_plan_info",
     "fd_factor_tables_host", "fd_rect_solve", "fd_rect_solve_batched", "fd_dst_rows",
-    "fd_transform_rows", "fd_stencil_apply", "fd_stencil_apply_ex", "fd_schur_create", "fd_schur_destroy", "fd_schur_apply",
+    "fd_transform_rows", "fd_assemble_rhs", "fd_stencil_apply", "fd_stencil_apply_ex", "fd_schur_create", "fd_schur_destroy", "fd_schur_apply",
     "fd_center_solve", "fd_precond_apply", "fd_unprecond_apply", "fd_gmres_precond",
     "fd_ddm_solve", "fd_schur_set_steklov", "fd_schur_use_steklov", "fd_arnoldi_step", "fd_basis_update", "fd_axpby", "fd_norm", "fd_dot",
 )
@@ -66,6 +66,7 @@ def _declare(lib):
         "fd_rect_solve_batched": (I, [I, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), P]),
         "fd_dst_rows": (I, [I, I, P, P, I, P]),
         "fd_transform_rows": (I, [I, I, I, I, P, P, I, P]),
+        "fd_assemble_rhs": (I, [I, I, D, D, D, D, D, I, D, D, D, D, P, P, P]),
         "fd_stencil_apply": (I, [I, I, D, D, D, D, D, D, D, P, P, P]),
         "fd_stencil_apply_ex": (I, [I, I, D, D, D, D, D, D, D, I, I, P, P, P]),
         "fd_schur_create": (I, [ctypes.POINTER(P), P, D, D, I, ctypes.POINTER(P), ctypes.POINTER(I),

@@ -118,6 +118,47 @@ def manufactured_rhs(comp, solution: str, api=None):
     return f, exact
 
 
+_SOLUTION_CODE = {"sin_exp": 0, "sin": 1}
+
+
+def manufactured_rhs_device(comp, solution: str):
+    """manufactured_rhs assembled on the device (C ABI fd_assemble_rhs, SURVEY
+    8f row 3): the same recipe -- f = lap p + kappa p at the nodes, each
+    Dirichlet edge lifted with p at its ghost points -- without the host
+    arrays or their upload.  Returns ({id: f}, {id: exact}) as CUDA tensors."""
+    import torch
+
+    from . import _native
+    from .geometry import BoundaryKind
+    _native.require_cuda()
+    f, exact = {}, {}
+    for sub in comp.subdomains:
+        lift = []
+        for edge in ("west", "east", "south", "north"):
+            if sub.edge_bc[edge] is BoundaryKind.DIRICHLET:
+                lift.append(2.0 if edge in sub.half_cell_dirichlet else 1.0)
+            else:
+                lift.append(0.0)
+        fi = torch.empty(sub.size, dtype=torch.float64, device="cuda")
+        ei = torch.empty(sub.size, dtype=torch.float64, device="cuda")
+        _native.call("fd_assemble_rhs", sub.m, sub.n, float(sub.origin[0]), float(sub.origin[1]),
+                     float(sub.dx), float(sub.dy), float(sub.kappa), _SOLUTION_CODE[solution], *lift,
+                     _native.dptr(fi), _native.dptr(ei), _native.stream_ptr())
+        f[sub.id], exact[sub.id] = fi, ei
+    return f, exact
+
+
+def rel_l2_device(fields: dict, exact: dict) -> float:
+    """rel_l2 with both sides on the device."""
+    num = den = 0.0
+    for sid, ex in exact.items():
+        v = fields[sid]
+        v = v.values if hasattr(v, "values") else v
+        num += float(((v - ex) ** 2).sum())
+        den += float((ex ** 2).sum())
+    return math.sqrt(num / den)
+
+
 def random_rhs(comp, seed: int = 0):
     """i.i.d. uniform[-1, 1] per subdomain, drawn in id order from one generator."""
     rng = np.random.default_rng(seed)
@@ -125,14 +166,15 @@ def random_rhs(comp, seed: int = 0):
             for sub in sorted(comp.subdomains, key=lambda s: s.id)}
 
 
-def build_cross_case(name: str, api=None, N: int | None = None):
+def build_cross_case(name: str, api=None, N: int | None = None, device: bool = False):
     """(composite, rhs dict, exact dict or None, meta) for c0, c2, c3, c4 or a
-    reduced-N variant of their geometry (`N` overrides the size)."""
+    reduced-N variant of their geometry (`N` overrides the size).  device=True
+    assembles the manufactured right-hand sides (c0, c2, c4) on the GPU."""
     api = api or default_api()
     if name in ("c0", "c2"):
         N = N or (141 if name == "c0" else 2047)
         comp = cross_composite(N, kappa=0.0, api=api)
-        f, exact = manufactured_rhs(comp, "sin_exp", api)
+        f, exact = manufactured_rhs_device(comp, "sin_exp") if device else manufactured_rhs(comp, "sin_exp", api)
     elif name == "c3":
         N = N or 4095
         comp = cross_composite(N, kappa=-100.0, api=api)
@@ -141,7 +183,7 @@ def build_cross_case(name: str, api=None, N: int | None = None):
         N = N or 4095
         arm = 4 * N + 3          # 16383 at N = 4095: same h, n stays 2^p - 1
         comp = cross_composite(N, arm=arm, kappa=0.0, api=api)
-        f, exact = manufactured_rhs(comp, "sin", api)
+        f, exact = manufactured_rhs_device(comp, "sin") if device else manufactured_rhs(comp, "sin", api)
     else:
         raise ValueError(f"unknown cross config {name!r}")
     meta = {"name": name, "N": N, "points": sum(s.size for s in comp.subdomains),

@@ -668,6 +668,16 @@ int fd_transform_rows(int rows, int n, int pair, int inverse, const double *in, 
     FD_API_END
 }
 
+int fd_assemble_rhs(int m, int n, double x0, double y0, double dx, double dy, double kappa, int solution,
+                    double lift_west, double lift_east, double lift_south, double lift_north, double *f,
+                    double *exact, void *stream) {
+    FD_API_BEGIN
+    if (m < 1 || n < 1 || !f || (solution != 0 && solution != 1)) FD_FAIL(FD_ERR_VALIDATION, "bad assembly arguments");
+    const double lift[4] = {lift_west, lift_east, lift_south, lift_north};
+    launch_assemble(m, n, x0, y0, dx, dy, kappa, solution, lift, f, exact, S(stream));
+    FD_API_END
+}
+
 int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa, double mod_west,
                      double mod_east, double mod_south, double mod_north, const double *v,
                      double *out, void *stream) {

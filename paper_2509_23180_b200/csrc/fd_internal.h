@@ -193,6 +193,8 @@ inline void launch_stencil(const Plan &p, double ms, double mn, const double *v,
 }
 void launch_scatter(int len, const int64_t *from, const int64_t *to, double c, const double *src,
                     double *dst, int accumulate, cudaStream_t s);
+void launch_assemble(int m, int n, double x0, double y0, double dx, double dy, double kappa, int sol,
+                     const double lift[4], double *f, double *exact, cudaStream_t s);
 void launch_mul(long long N, const double *x, const double *y, double *out, cudaStream_t s);   // out = x * y
 void steklov_pivots(int L, int M, double delta_line, double delta_sweep, double kappa, double mod_lo,
                     double mod_hi, int end, double *inv);

@@ -501,3 +501,50 @@ void launch_transpose(int R, int C, const double *in, double *out, double alpha,
 }
 
 }  // namespace fd
+
+namespace fd {
+
+// ---------------------------------------------------------------------------
+// Device-side problem assembly: the manufactured right-hand
+// side f = lap p + kappa p at the cell-centred nodes of one rectangle, each
+// Dirichlet edge lifted with p at its ghost points (rectsolver.lift_dirichlet,
+// rectsolver.py:292-313: rhs -= factor * delta * g on the adjacent line, in
+// edge order west, east, south, north), and optionally p itself.  Solutions:
+// 0 = sin(pi x) sin(pi y) + e^(x+y)/e^2, 1 = sin(pi x) sin(pi y).
+__device__ __forceinline__ double mf_p(int sol, double x, double y) {
+    const double s = sin(M_PI * x) * sin(M_PI * y);
+    return sol == 0 ? s + exp(x + y) / (M_E * M_E) : s;
+}
+__device__ __forceinline__ double mf_lap(int sol, double x, double y) {
+    const double s = -2.0 * (M_PI * M_PI) * sin(M_PI * x) * sin(M_PI * y);
+    return sol == 0 ? s + 2.0 * exp(x + y) / (M_E * M_E) : s;
+}
+
+__global__ void assemble_kernel(int m, int n, double x0, double y0, double dx, double dy, double kappa,
+                                int sol, double lw, double le, double ls, double ln, double delta_x,
+                                double delta_y, double *__restrict__ f, double *__restrict__ exact) {
+    const long long total = (long long)m * n;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx / n), j = (int)(idx - (long long)i * n);
+        const double x = x0 + (double(i + 1) - 0.5) * dx, y = y0 + (double(j + 1) - 0.5) * dy;
+        const double p = mf_p(sol, x, y);
+        double v = mf_lap(sol, x, y) + kappa * p;
+        if (lw != 0.0 && i == 0) v = v - lw * delta_x * mf_p(sol, x - dx, y);
+        if (le != 0.0 && i == m - 1) v = v - le * delta_x * mf_p(sol, x + dx, y);
+        if (ls != 0.0 && j == 0) v = v - ls * delta_y * mf_p(sol, x, y - dy);
+        if (ln != 0.0 && j == n - 1) v = v - ln * delta_y * mf_p(sol, x, y + dy);
+        f[idx] = v;
+        if (exact) exact[idx] = p;
+    }
+}
+
+void launch_assemble(int m, int n, double x0, double y0, double dx, double dy, double kappa, int sol,
+                     const double lift[4], double *f, double *exact, cudaStream_t s) {
+    const long long N = (long long)m * n;
+    assemble_kernel<<<grid_for(N, 256), 256, 0, s>>>(m, n, x0, y0, dx, dy, kappa, sol, lift[0], lift[1], lift[2],
+                                                     lift[3], 1.0 / (dx * dx), 1.0 / (dy * dy), f, exact);
+    FD_CUDA(cudaGetLastError());
+}
+
+}  // namespace fd
