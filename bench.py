@@ -233,6 +233,25 @@ def full_solve(dev, name="c2", reps=3):
                                       "value": meta["points"] / s_wall, "rel_l2_vs_exact": s_err,
                                       "what": "ddm_solve(interface_only=True): Steklov neighbour applies "
                                               "(SURVEY 8f row 2), full solves in pre-solve/back-substitution"}}
+    # the largest BASELINE cross (c4, 285M points), problem assembled on the
+    # device inside the timed region, both operator forms
+    c4 = {}
+    for variant, kw in (("default", {}), ("interface_only", {"interface_only": True})):
+        ts = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            comp4, f4, ex4, meta4 = configs.build_cross_case("c4", device=True)
+            fields4, rep4 = ddm.ddm_solve(comp4, f4, cfg, **kw)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        c4[variant] = {"iterations": rep4.iterations, "wall_s": min(ts), "value": meta4["points"] / min(ts),
+                       "rel_l2_vs_exact": configs.rel_l2_device(fields4, ex4)}
+        del fields4, f4, ex4
+    out["c4_device_assembled"] = dict(c4, points=meta4["points"],
+                                      timing="assembly + ddm_solve, best of 2 (the first call of each builds plan tables)",
+                                      reference={"iterations": 67, "wall_s": 1373.4, "rel_l2_vs_exact": 4.933e-8,
+                                                 "where": "reference fftddm on the build container's CPU (SURVEY 6)"})
     gpath = os.path.join(ROOT, "tests", "golden", f"{name}.npz")
     if os.path.exists(gpath):
         g = np.load(gpath)
