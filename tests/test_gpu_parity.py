@@ -478,6 +478,50 @@ class TestDeviceAssembly:
         assert configs.rel_l2_device(fields, exd) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-4)
 
 
+class TestEdgeCases:
+    """Error paths and degenerate inputs the reference tests."""
+
+    def test_zero_rhs(self):
+        comp, f, _, _ = configs.build_cross_case("c0", N=15)
+        zero = {k: np.zeros_like(v) for k, v in f.items()}
+        fields, rep = ddm.ddm_solve(comp, zero, krylov.GmresConfig(m=50, tol=1e-10))
+        assert rep.converged and rep.iterations == 0
+        assert all(np.all(fields[s].values == 0.0) for s in fields)
+
+    def test_singular_all_neumann(self):
+        from paper_2509_23180_b200.errors import SingularOperatorError
+        sub = make((8, 8, 0.125, 0.125, 0.0, "NNNN", ()))
+        with pytest.raises(SingularOperatorError):
+            rectsolver.plan_rect(sub)
+
+    def test_wrong_length(self):
+        sub = make((8, 7, 0.125, 0.125, 0.0, "DDDD", ()))
+        pl = rectsolver.plan_rect(sub)
+        with pytest.raises((ValueError, Exception)):
+            rectsolver.solve_rect(pl, np.zeros(55))
+
+    def test_default_restart_length(self):
+        """GmresConfig() defaults to m = 80 (krylov.py:32-49): above the
+        low-synchronisation Arnoldi's 64 vectors, the classic MGS kernels run."""
+        comp, f, _, _ = configs.build_cross_case("c0", N=31)
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig())
+        ofields, orep = O.ddm_solve(comp, f, m=80, tol=1e-10)
+        assert rep.iterations == orep.iterations
+        num = sum(float(np.sum((fields[s].values - ofields[s]) ** 2)) for s in ofields)
+        den = sum(float(np.sum(ofields[s] ** 2)) for s in ofields)
+        assert (num / den) ** 0.5 < 1e-10
+
+    @pytest.mark.parametrize("m,n", [(1, 1), (1, 7), (7, 1), (2, 2), (3, 1100), (1100, 3)])
+    def test_thin_rectangles(self, m, n, rng):
+        h = 1.0 / max(m, n)
+        sub = make((m, n, h, h, -1.0, "DDDD", ()))
+        pl = rectsolver.plan_rect(sub)
+        f = rng.uniform(-1, 1, sub.size)
+        p = rectsolver.solve_rect(pl, f).values
+        r = rectsolver.apply_rect_operator(sub, p) - f
+        assert np.linalg.norm(r) / np.linalg.norm(f) < 1e-12
+
+
 class TestDistDriver:
     def test_native_backend_single_rank(self, golden_small):
         """dist_ddm_solve with the GPU backend and no process group (one rank owns
