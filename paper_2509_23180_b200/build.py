@@ -50,7 +50,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
               "-I", os.path.join(os.path.dirname(HERE), "include")] + ARCH
     if os.environ.get("FD_DIAG_BUILD"):   # trace / component-skip diagnostics (tools/dbg_sweep.sh)
         common += ["-DFD_DIAG=1"]
-    objs = []
+    jobs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [nvcc(), "-c", src, "-o", obj] + common
@@ -60,8 +60,15 @@ def build(verbose: bool = False, force: bool = False) -> str:
             cmd += ["-x", "c++"]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        jobs.append((cmd, obj))
+    # translation units compile independently: run them on the host's cores
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+        for r in ex.map(lambda j: subprocess.run(j[0], capture_output=not verbose, text=True), jobs):
+            if r.returncode != 0:
+                sys.stderr.write((r.stdout or "") + (r.stderr or ""))
+                raise subprocess.CalledProcessError(r.returncode, r.args)
+    objs = [o for _, o in jobs]
     tmp = LIB + ".tmp"
     cmd = [nvcc(), "-shared", "-o", tmp] + objs + ARCH + ["-Xcompiler", "-fPIC"]
     subprocess.run(cmd, check=True)
