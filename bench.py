@@ -380,7 +380,12 @@ def run_gpu(args, world, rank, local):
     io_bytes = sum(r.nbytes for r in rhs)
 
 
-    solve = None if args.no_solve else full_solve(dev)
+    solve = None
+    if not args.no_solve:
+        try:
+            solve = full_solve(dev)
+        except Exception as exc:   # the apply line must still print
+            solve = {"error": f"{type(exc).__name__}: {exc}"}
 
     # kernels of ours per batched apply: one persistent cooperative launch on the
     # FFT path (n + 1 = 2^p), pass1 + carry + pass2 on the dense path
