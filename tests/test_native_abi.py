@@ -125,3 +125,33 @@ def test_gpu_axis_unsupported(lib):
     from paper_2509_23180_b200.rectsolver import _gpu_axis
     with pytest.raises(UnsupportedError):
         _gpu_axis(make((12, 9, 1.0, 1.0, 0.0, "DDDD", ("west", "south"))))
+
+
+def test_interface_line_descriptors():
+    """Interface-only variant: line geometry of each arm of the BASELINE cross
+    (host logic, no GPU): the line runs along the interface, the sweep across
+    it, and the interface row is the sweep's first or last row."""
+    from paper_2509_23180_b200 import configs, ddm
+    comp = configs.cross_composite(15, arm=40, kappa=-2.0)
+    centre = comp.subdomain(0)
+    seen = {}
+    for iface in comp.interfaces_of(0):
+        other = iface.other_side(0)[0]
+        sub = comp.subdomain(other)
+        edge = iface.side_a[1] if iface.side_a[0] == other else iface.side_b[1]
+        to_c = ddm.make_coupling(comp, iface, other)
+        from_c = ddm.make_coupling(comp, iface, 0)
+        L, M, dl, ds, mlo, mhi, end, pin, pout = ddm._steklov_line(sub, edge, to_c, from_c)
+        assert L == 15 and M == 40 and end == (1 if edge in ("east", "north") else 0)
+        assert sorted(pin.tolist()) == list(range(15)) and sorted(pout.tolist()) == list(range(15))
+        assert mlo == 0.0 and mhi == 0.0 and dl == pytest.approx(15.0 ** 2) and ds == pytest.approx(15.0 ** 2)
+        seen[edge] = True
+    assert sorted(seen) == ["east", "north", "south", "west"]
+    # a half-cell end on the line's own axis disqualifies the line
+    ref = configs.reference_cross(4)
+    for iface in ref.interfaces_of(0):
+        other = iface.other_side(0)[0]
+        sub = ref.subdomain(other)
+        edge = iface.side_a[1] if iface.side_a[0] == other else iface.side_b[1]
+        assert ddm._steklov_line(sub, edge, ddm.make_coupling(ref, iface, other),
+                                 ddm.make_coupling(ref, iface, 0)) is None   # NN flanks along the line
