@@ -201,6 +201,12 @@ struct fd_schur_s {
     };
     std::vector<Steklov> stk;
     bool steklov = false;
+    // small problems: the preconditioned apply (a dozen short launches) replayed
+    // as one CUDA graph on a fixed input buffer (0 untried, 2 warmed, 1 ready, -1 off)
+    int graph_state = 0;
+    cudaGraphExec_t pgraph = nullptr;
+    cudaStream_t gstream = nullptr;
+    double *gin = nullptr;
     double *lines = nullptr, *lines_hat = nullptr;
     std::vector<void *> allocs;
 };
@@ -343,6 +349,56 @@ static void precond_apply(fd_schur_s *op, const double *p, double *out, cudaStre
     center_solve(op, op->tmp, out, -1.0, 1.0, p, s);
 }
 
+static void drop_graph(fd_schur_s *op) {
+    if (op->pgraph) cudaGraphExecDestroy(op->pgraph);
+    op->pgraph = nullptr;
+    op->graph_state = 0;
+}
+
+// precond_apply(op, p, op->w) for the GMRES loop.  Problems with only dense
+// (three-kernel) solves and at most 2^18 centre points are launch-bound: after
+// one warm-up apply the sequence is captured once into a graph that reads a
+// fixed input copy, and every later apply is one copy + one graph launch.
+static void precond_apply_loop(fd_schur_s *op, const double *p, cudaStream_t s) {
+    const long long N = (long long)op->center->m * op->center->n;
+    if (op->graph_state == 0) {
+        bool ok = N <= (1LL << 18) && op->center->transform == kDense;
+        for (const Plan *q : op->nb) ok = ok && (op->steklov || q->transform == kDense);
+        op->graph_state = ok ? 2 : -1;
+        precond_apply(op, p, op->w, s);
+        return;
+    }
+    if (op->graph_state == 2) {
+        op->graph_state = -1;   // unless the capture below succeeds
+        try {
+            if (!op->gin) op->gin = (double *)dalloc(op, sizeof(double) * N);
+            if (!op->gstream) FD_CUDA(cudaStreamCreateWithFlags(&op->gstream, cudaStreamNonBlocking));
+            FD_CUDA(cudaStreamBeginCapture(op->gstream, cudaStreamCaptureModeThreadLocal));
+            cudaGraph_t g = nullptr;
+            try {
+                precond_apply(op, op->gin, op->w, op->gstream);
+            } catch (...) {
+                cudaStreamEndCapture(op->gstream, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            FD_CUDA(cudaStreamEndCapture(op->gstream, &g));
+            const cudaError_t e = cudaGraphInstantiate(&op->pgraph, g, 0);
+            cudaGraphDestroy(g);
+            if (e == cudaSuccess) op->graph_state = 1;
+        } catch (...) {
+            op->pgraph = nullptr;
+        }
+        cudaGetLastError();   // a refused capture leaves no sticky error
+    }
+    if (op->graph_state == 1) {
+        FD_CUDA(cudaMemcpyAsync(op->gin, p, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+        FD_CUDA(cudaGraphLaunch(op->pgraph, s));
+    } else {
+        precond_apply(op, p, op->w, s);
+    }
+}
+
 // (A_c - S) p   (ddm.py:128-131)
 static void unprecond_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
     launch_stencil(*op->center, op->mod_s, op->mod_n, p, op->tmp2, s);
@@ -449,7 +505,7 @@ static int gmres_precond(fd_schur_s *op, const double *rhs, double *x, int x_is_
         int k_used = 0;
         bool breakdown = false;
         for (int k = 0; k < m; ++k) {
-            precond_apply(op, op->V + (long long)k * N, w, s);
+            precond_apply_loop(op, op->V + (long long)k * N, s);   // -> w
             double w_norm = 0.0;
             if (lowsync)
                 arnoldi_step_ls(op, N, k, hcol.data(), &w_norm, s);
@@ -796,6 +852,7 @@ int fd_schur_use_steklov(fd_schur op, int enable) {
         }
         op->steklov = true;
     }
+    drop_graph(op);   // the captured apply no longer matches
     FD_API_END
 }
 
@@ -805,6 +862,8 @@ int fd_schur_destroy(fd_schur op) {
         HostTimer ht("schur_destroy");
         cudaSetDevice(op->device);
         cudaDeviceSynchronize();
+        drop_graph(op);
+        if (op->gstream) cudaStreamDestroy(op->gstream);
         for (void *a : op->allocs) dfree(a);
         if (op->V) dfree(op->V);
         if (op->sc.cap) free_scratch(op->sc);
