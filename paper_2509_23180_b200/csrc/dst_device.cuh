@@ -432,15 +432,20 @@ struct Fft2 {
 // (j, k); each thread walks its index by k + 1 per j.  MPT modes per thread
 // (n <= 128 MPT), G rows per group share every table load.
 constexpr int kDenseMax = 1024;
-template <int MPT_, int NT_ = 128>
+template <int MPT_, int NT_ = 128, int S_ = 1>
 struct DenseDstT {
-    static constexpr int NT = NT_;
+    // NT_ mode columns x S_ threads each: the S_ threads of a mode split the
+    // transform's input sum (small n: more threads, shorter dependent loops)
+    static constexpr int S = S_;
+    static constexpr int NMODE = NT_;
+    static constexpr int NT = NT_ * S_;
     static constexpr int G = NT_ <= 160 ? 4 : 8;   // small n: fewer rows per CTA, more CTAs
-    static constexpr int MINB = 2;
+    static constexpr int MINB = S_ > 1 ? 1 : 2;
     static constexpr int MPT = MPT_;
-    static constexpr int NMAX = NT * MPT_;
-    // rows + the periodic basis table: 2(n+1) entries (DD sine) or 4n (NN cosine)
+    static constexpr int NMAX = NT_ * MPT_;
+    // rows + the periodic basis table: 2(n+1) entries (DD sine), 4n (NN cosine) or 2n (PP)
     static constexpr size_t SMEM = size_t(G) * NMAX * sizeof(double) + size_t(4) * (NMAX + 1) * sizeof(double);
+    static_assert(S_ == 1 || MPT_ == 1, "split transforms own one mode per thread group");
 };
 
 // ---------------------------------------------------------------------------

@@ -92,37 +92,43 @@ struct InvT<FftDst<LG>> {
 // transforms.py:114-126,139-148): T = cos(2 pi q/n) for basis index <= n/2,
 // sin(2 pi q/n) above (table halves), q = o i mod n; basis 0 and n/2 carry
 // sqrt(1/n) (a 1/sqrt(2) on the output forward, on the input inverse).
-template <int M, int NT_>
+template <int M, int NT_, int S_>
 __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const double *tab,
-                                           double (&acc)[DenseDstT<M, NT_>::G][M], int pair, bool inverse) {
-    constexpr int NT = DenseDstT<M, NT_>::NT, G = DenseDstT<M, NT_>::G;
+                                           double (&acc)[DenseDstT<M, NT_, S_>::G][M], int pair, bool inverse) {
+    using D = DenseDstT<M, NT_, S_>;
+    constexpr int G = D::G, S = D::S, NM = D::NMODE;
     const bool nn = pair == kPairNN, pp = pair == kPairPP;
     const int period = nn ? 4 * n : pp ? n : 2 * (n + 1);
     const int half = n >> 1;
+    const int q = threadIdx.x % S;                     // this thread's share of the input sum
+    const int chunk = (n + S - 1) / S, jb = min(n, q * chunk), je = min(n, jb + chunk);
     int idx[M], step[M], toff[M];
 #pragma unroll
     for (int u = 0; u < M; ++u) {
-        const int o = threadIdx.x + u * NT;
+        const int o = threadIdx.x / S + u * NM;
         toff[u] = 0;
+        long long i0;
         if (pp) {
-            idx[u] = 0;            // o i mod n at i = 0
+            i0 = (long long)o * jb;            // o i mod n
             step[u] = o;
             if (!inverse && o > half) toff[u] = n;   // sine half of the table
         } else if (!nn) {
-            idx[u] = o + 1;        // (i + 1)(o + 1) at i = 0
+            i0 = (long long)(jb + 1) * (o + 1);  // (i + 1)(o + 1)
             step[u] = o + 1;
         } else if (!inverse) {
-            idx[u] = o;            // o (2i + 1) at i = 0
+            i0 = (long long)o * (2 * jb + 1);  // o (2i + 1)
             step[u] = 2 * o;
         } else {
-            idx[u] = 0;            // i (2o + 1) at i = 0
+            i0 = (long long)jb * (2 * o + 1);  // i (2o + 1)
             step[u] = 2 * o + 1;
         }
+        idx[u] = int(i0 % period);
+        if (step[u] >= period) step[u] -= period;
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g][u] = 0.0;
     }
 #pragma unroll 2
-    for (int j = 0; j < n; ++j) {
+    for (int j = jb; j < je; ++j) {
         double x[G];
         const double xs = ((nn || pp) && inverse && (j == 0 || (pp && j == half))) ? 0.70710678118654752440 : 1.0;
         const int joff = (pp && inverse && j > half) ? n : 0;   // inverse: the input's basis picks the half
@@ -130,7 +136,7 @@ __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const do
         for (int g = 0; g < G; ++g) x[g] = rowbuf[g * n + j] * xs;
 #pragma unroll
         for (int u = 0; u < M; ++u) {
-            const int o = threadIdx.x + u * NT;
+            const int o = threadIdx.x / S + u * NM;
             if (o < n) {
                 const double sv = tab[idx[u] + toff[u] + joff];
 #pragma unroll
@@ -140,44 +146,55 @@ __device__ __forceinline__ void dense_rows(const double *rowbuf, int n, const do
             }
         }
     }
+    if constexpr (S > 1) {   // combine the S partial sums (adjacent lanes)
+#pragma unroll
+        for (int off = 1; off < S; off <<= 1)
+#pragma unroll
+            for (int u = 0; u < M; ++u)
+#pragma unroll
+                for (int g = 0; g < G; ++g) acc[g][u] += __shfl_xor_sync(0xffffffffu, acc[g][u], off);
+    }
     if ((nn || pp) && !inverse) {   // output 0 (and n/2 for PP) carries sqrt(1/n) instead of sqrt(2/n)
 #pragma unroll
-        for (int u = 0; u < M; ++u)
-            if (threadIdx.x + u * NT == 0 || (pp && threadIdx.x + u * NT == half))
+        for (int u = 0; u < M; ++u) {
+            const int o = threadIdx.x / S + u * NM;
+            if (o == 0 || (pp && o == half))
 #pragma unroll
                 for (int g = 0; g < G; ++g) acc[g][u] *= 0.70710678118654752440;
+        }
     }
 }
 
-template <int M, int NT_>
+template <int M, int NT_, int S_>
 __device__ __forceinline__ double *dense_tab(double2 *smem) {
-    return reinterpret_cast<double *>(smem) + DenseDstT<M, NT_>::G * DenseDstT<M, NT_>::NMAX;
+    return reinterpret_cast<double *>(smem) + DenseDstT<M, NT_, S_>::G * DenseDstT<M, NT_, S_>::NMAX;
 }
 
-template <int M, int NT_>
+template <int M, int NT_, int S_>
 __device__ __forceinline__ void stage_tab(double *tab, int n, const PlanDev &p) {
     const int period = p.tpair == kPairNN ? 4 * n : p.tpair == kPairPP ? 2 * n : 2 * (n + 1);
-    for (int q = threadIdx.x; q < period; q += DenseDstT<M, NT_>::NT) tab[q] = __ldg(p.dense + q);
+    for (int q = threadIdx.x; q < period; q += DenseDstT<M, NT_, S_>::NT) tab[q] = __ldg(p.dense + q);
 }
 
-template <int M, int NT_>
-struct FwdT<DenseDstT<M, NT_>> {
+template <int M, int NT_, int S_>
+struct FwdT<DenseDstT<M, NT_, S_>> {
     __device__ static void run(const double *in, int rows, int n, double *rowbuf, double2 *smem,
                                const PlanDev &p) {
-        constexpr int NT = DenseDstT<M, NT_>::NT, G = DenseDstT<M, NT_>::G;
-        double *tab = dense_tab<M, NT_>(smem);
-        stage_tab<M, NT_>(tab, n, p);
+        constexpr int NT = DenseDstT<M, NT_, S_>::NT, G = DenseDstT<M, NT_, S_>::G;
+        double *tab = dense_tab<M, NT_, S_>(smem);
+        stage_tab<M, NT_, S_>(tab, n, p);
 #pragma unroll 8
         for (int idx = threadIdx.x; idx < G * n; idx += NT)
             rowbuf[idx] = idx < rows * n ? __ldg(in + idx) : 0.0;
         __syncthreads();
         double acc[G][M];
-        dense_rows<M, NT_>(rowbuf, n, tab, acc, p.tpair, false);
+        dense_rows<M, NT_, S_>(rowbuf, n, tab, acc, p.tpair, false);
         __syncthreads();
+        constexpr int S = DenseDstT<M, NT_, S_>::S, NM = DenseDstT<M, NT_, S_>::NMODE;
 #pragma unroll
         for (int u = 0; u < M; ++u) {
-            const int k = threadIdx.x + u * NT;
-            if (k < n)
+            const int k = threadIdx.x / S + u * NM;
+            if (k < n && threadIdx.x % S == 0)
 #pragma unroll
                 for (int g = 0; g < G; ++g)
                     if (g < rows) rowbuf[g * n + k] = p.scale * acc[g][u];
@@ -186,21 +203,22 @@ struct FwdT<DenseDstT<M, NT_>> {
     }
 };
 
-template <int M, int NT_>
-struct InvT<DenseDstT<M, NT_>> {
+template <int M, int NT_, int S_>
+struct InvT<DenseDstT<M, NT_, S_>> {
     __device__ static void run(double *rowbuf, int rows, int n, double *out, const double *other,
                                double alpha, double beta, double2 *smem, const PlanDev &p) {
-        constexpr int NT = DenseDstT<M, NT_>::NT, G = DenseDstT<M, NT_>::G;
-        double *tab = dense_tab<M, NT_>(smem);
-        stage_tab<M, NT_>(tab, n, p);
+        constexpr int NT = DenseDstT<M, NT_, S_>::NT, G = DenseDstT<M, NT_, S_>::G;
+        double *tab = dense_tab<M, NT_, S_>(smem);
+        stage_tab<M, NT_, S_>(tab, n, p);
         for (int idx = rows * n + threadIdx.x; idx < G * n; idx += NT) rowbuf[idx] = 0.0;
         __syncthreads();
         double acc[G][M];
-        dense_rows<M, NT_>(rowbuf, n, tab, acc, p.tpair, true);
+        dense_rows<M, NT_, S_>(rowbuf, n, tab, acc, p.tpair, true);
+        constexpr int S = DenseDstT<M, NT_, S_>::S, NM = DenseDstT<M, NT_, S_>::NMODE;
 #pragma unroll
         for (int u = 0; u < M; ++u) {
-            const int k = threadIdx.x + u * NT;
-            if (k < n)
+            const int k = threadIdx.x / S + u * NM;
+            if (k < n && threadIdx.x % S == 0)
 #pragma unroll
                 for (int g = 0; g < G; ++g)
                     if (g < rows) {
@@ -219,8 +237,8 @@ template <int LG>
 struct Cfg<FftDst<LG>> {
     static constexpr int MPT = ((1 << (LG - 1)) - 1 + FftDst<LG>::NT - 1) / FftDst<LG>::NT;
 };
-template <int M, int NT_>
-struct Cfg<DenseDstT<M, NT_>> {
+template <int M, int NT_, int S_>
+struct Cfg<DenseDstT<M, NT_, S_>> {
     static constexpr int MPT = M;
 };
 
@@ -488,7 +506,7 @@ int rows_per_block(int n, int pair) {
     const int N = n + 1;
     if (transform_kind(n, pair) == kFFT) return N >= 4096 ? 8 : 16;
     // one group per carry block: more CTAs for the small dense solves
-    return n <= 160 ? DenseDstT<1, 160>::G : DenseDstT<1, 256>::G;
+    return n <= 160 ? DenseDstT<1, 160, 4>::G : DenseDstT<1, 256>::G;
 }
 
 template <class P>
@@ -564,8 +582,8 @@ void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
     for (auto &j : jobs)
         if (j.p.tpair != jobs[0].p.tpair) FD_FAIL(FD_ERR_VALIDATION, "launch_solve: mixed transform pairs in one batch");
     if (jobs[0].p.dense) {
-        if (n <= 128) run_solve<DenseDstT<1, 128>>(jobs, s);
-        else if (n <= 160) run_solve<DenseDstT<1, 160>>(jobs, s);
+        if (n <= 128) run_solve<DenseDstT<1, 128, 4>>(jobs, s);
+        else if (n <= 160) run_solve<DenseDstT<1, 160, 4>>(jobs, s);
         else if (n <= 256) run_solve<DenseDstT<1, 256>>(jobs, s);
         else if (n <= 512) run_solve<DenseDstT<2, 256>>(jobs, s);
         else run_solve<DenseDstT<4, 256>>(jobs, s);
