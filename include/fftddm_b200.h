@@ -73,11 +73,35 @@ int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double
  * cosine basis, DCT-II/III; transforms.py:32-33,83-98,106-134), 2 = PP (real
  * Fourier basis, even n; transforms.py:34-35,114-126,139-148).  A DD axis
  * needs ghost-node ends; NN/PP ends belong to the basis.  NN and PP run on
- * the dense periodic-table transform (n <= 1024); the sweep axis must not be
- * periodic. */
+ * the dense periodic-table transform (n <= 1024); a periodic sweep axis
+ * needs fd_plan_create_sweep. */
 int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double kappa,
                       double mod_west, double mod_east, double mod_south, double mod_north,
                       int transform_axis, int transform_pair, int device);
+/* Full plan_rect (rectsolver.py:94-180): as fd_plan_create_ex plus
+ *  - sweep_cyclic: the sweep axis is periodic (PP, even count).  The per-mode
+ *    system is solved as the reference does -- Thomas on the rank-one modified
+ *    matrix, then the Sherman-Morrison correction (rectsolver.py:136-153,
+ *    202-205); with two rows the wrap doubles the coupling.  End modifiers of
+ *    the sweep axis are ignored.
+ *  - pin_mean: singular spectral modes (all-Neumann / periodic, kappa = 0) do
+ *    not fail the plan; they are solved in the minimum-norm sense
+ *    (rectsolver.py:157-175,206-207).  The caller lists them with
+ *    fd_plan_singular_modes and attaches each mode's sweep-matrix
+ *    pseudo-inverse with fd_plan_set_pinv before the first solve (a solve
+ *    before that returns FD_ERR_SINGULAR).
+ * Periodic-sweep and pin_mean plans run the dense-transform solve (n <= 1024). */
+int fd_plan_create_sweep(fd_plan *out, int m, int n, double dx, double dy, double kappa,
+                         double mod_west, double mod_east, double mod_south, double mod_north,
+                         int transform_axis, int transform_pair, int sweep_cyclic, int pin_mean,
+                         int device);
+/* singular spectral modes of a pin_mean plan (indices along the transform
+ * axis, ascending); *count receives the total, at most cap are written. */
+int fd_plan_singular_modes(fd_plan plan, int *modes, int cap, int *count);
+/* attach the pseudo-inverses of the singular modes' sweep matrices, host
+ * memory, count x ms x ms row-major (ms = sweep length: m for a y transform,
+ * n for an x transform), in fd_plan_singular_modes order. */
+int fd_plan_set_pinv(fd_plan plan, int count, const double *pinv);
 /* GPU transform available for length n: 1 = FFT (n+1 = 2^p, 256..4096),
  * 0 = dense (n <= 1024), -1 = none.  DD pair; fd_transform_kind_pair for NN. */
 int fd_transform_kind(int n);

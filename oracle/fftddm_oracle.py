@@ -191,6 +191,12 @@ class OraclePlan:
     off: float
     axis: str = "y"
     bc: str = "DD"
+    cyclic: bool = False
+    sm_q: np.ndarray = None
+    sm_denom: np.ndarray = None
+    sm_gamma: np.ndarray = None
+    singular: tuple = ()
+    singular_dense: tuple = ()
 
 
 def transformable(sub, axis):
@@ -202,10 +208,12 @@ def transformable(sub, axis):
     return pair == "DD" and sub.end_modifier(lo) == 0.0 and sub.end_modifier(hi) == 0.0
 
 
-def plan(sub, axis=None):
-    """plan_rect for DD/NN transform axes (rectsolver.py:94-135,153-163): axis y
-    when transformable, else x (the field is transposed, rectsolver.py:198-199);
-    `axis` forces the choice."""
+def plan(sub, axis=None, pin_mean=False):
+    """plan_rect (rectsolver.py:94-180): axis y when transformable, else x (the
+    field is transposed, rectsolver.py:198-199); `axis` forces the choice.  A
+    periodic sweep axis factors the rank-one modified system and keeps the
+    Sherman-Morrison correction solves (rectsolver.py:136-153); pin_mean keeps
+    the dense matrices of singular modes (rectsolver.py:157-175)."""
     if axis is None:
         axis = "y" if transformable(sub, "y") else "x"
     if not transformable(sub, axis):
@@ -215,26 +223,67 @@ def plan(sub, axis=None):
     else:
         nt, ms, dt, ds, lo, hi = sub.m, sub.n, sub.delta_x, sub.delta_y, "south", "north"
     bc = sub.axis_pair(axis)
-    if sub.axis_pair("x" if axis == "y" else "y") == "PP":
-        raise NotImplementedError("oracle covers non-periodic sweep axes only")
+    cyclic = sub.axis_pair("x" if axis == "y" else "y") == "PP"
     lam = eigenvalues(bc, nt, dt, ds, sub.kappa)
     diag = np.tile(lam, (ms, 1))
-    diag[0] += sub.end_modifier(lo)
-    diag[-1] += sub.end_modifier(hi)
+    if cyclic:
+        if ms % 2:
+            raise SingularOracleError("periodic sweep axis needs an even count")
+    else:
+        diag[0] += sub.end_modifier(lo)
+        diag[-1] += sub.end_modifier(hi)
     tol = PIVOT_RTOL * max(np.abs(lam).max(), ds)
-    beta, lower, bad = factor_tridiag(diag, ds, tol)
+    q = den = gam = None
+    if cyclic and ms > 2:
+        gam = np.where(np.abs(diag[0]) > tol, -diag[0], ds)
+        bd = diag.copy()
+        bd[0] -= gam
+        bd[-1] -= ds * ds / gam
+        beta, lower, bad = factor_tridiag(bd, ds, tol)
+        u = np.zeros((ms, nt))
+        u[0] = gam
+        u[-1] = ds
+        q = tridiag_solve(beta, lower, ds, u)
+        den = 1.0 + q[0] + (ds / gam) * q[-1]
+        bad = bad | (np.abs(den) < 1e-12)
+    elif cyclic:
+        beta, lower, bad = factor_tridiag(diag, 2.0 * ds, tol)
+    else:
+        beta, lower, bad = factor_tridiag(diag, ds, tol)
+    singular, mats = (), ()
     if np.any(bad):
-        raise SingularOracleError(f"singular modes {np.nonzero(bad)[0].tolist()}")
-    return OraclePlan(sub=sub, beta=beta, lower=lower, off=ds, axis=axis, bc=bc)
+        if not pin_mean:
+            raise SingularOracleError(f"singular modes {np.nonzero(bad)[0].tolist()}")
+        singular = tuple(int(k) for k in np.nonzero(bad)[0])
+        ms_list = []
+        for k in singular:
+            M = np.diag(diag[:, k])
+            i = np.arange(ms - 1)
+            M[i, i + 1] += ds
+            M[i + 1, i] += ds
+            if cyclic:
+                M[0, ms - 1] += ds
+                M[ms - 1, 0] += ds
+            ms_list.append(M)
+        mats = tuple(ms_list)
+    return OraclePlan(sub=sub, beta=beta, lower=lower, off=ds, axis=axis, bc=bc, cyclic=cyclic,
+                      sm_q=q, sm_denom=den, sm_gamma=gam, singular=singular, singular_dense=mats)
 
 
 def solve(pl: OraclePlan, f):
-    """Q^T along the transform axis -> per-mode tridiagonal -> Q   (rectsolver.py:183-213)."""
+    """Q^T along the transform axis -> per-mode tridiagonal (+ periodic
+    correction, + minimum-norm singular modes) -> Q   (rectsolver.py:183-213)."""
     grid = np.asarray(f, dtype=float).reshape(pl.sub.m, pl.sub.n)
     if pl.axis == "x":
         grid = grid.T
     fhat = apply_qt(pl.bc, grid)
-    phat = tridiag_solve(pl.beta, pl.lower, pl.off, fhat)
+    off = 2.0 * pl.off if (pl.cyclic and fhat.shape[0] == 2) else pl.off
+    phat = tridiag_solve(pl.beta, pl.lower, off, fhat)
+    if pl.sm_q is not None:
+        vy = phat[0] + (pl.off / pl.sm_gamma) * phat[-1]
+        phat = phat - pl.sm_q * (vy / pl.sm_denom)
+    for k, M in zip(pl.singular, pl.singular_dense):
+        phat[:, k] = np.linalg.lstsq(M, fhat[:, k], rcond=None)[0]
     out = apply_q(pl.bc, phat)
     if pl.axis == "x":
         out = out.T

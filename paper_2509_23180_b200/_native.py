@@ -21,7 +21,8 @@ FD_OK, FD_ERR_VALIDATION, FD_ERR_SINGULAR, FD_ERR_NOT_CONVERGED, FD_ERR_CUDA, FD
 
 # every symbol the header declares (checked by tests/test_native_abi.py)
 EXPORTS = (
-    "fd_last_error", "fd_version", "fd_plan_create", "fd_plan_create_axis", "fd_plan_create_ex",
+    "fd_last_error", "fd_version", "fd_plan_create", "fd_plan_create_axis", "fd_plan_create_ex", "fd_plan_create_sweep",
+    "fd_plan_singular_modes", "fd_plan_set_pinv",
     "fd_transform_kind", "fd_transform_kind_pair",
     "fd_plan_destroy", "fd_plan_info",
     "fd_factor_tables_host", "fd_rect_solve", "fd_rect_solve_batched", "fd_dst_rows",
@@ -58,6 +59,9 @@ def _declare(lib):
         "fd_plan_create_axis": (I, [ctypes.POINTER(P), I, I, D, D, D, D, D, D, D, I, I]),
         "fd_transform_kind": (I, [I]),
         "fd_plan_create_ex": (I, [ctypes.POINTER(P), I, I, D, D, D, D, D, D, D, I, I, I]),
+        "fd_plan_create_sweep": (I, [ctypes.POINTER(P), I, I, D, D, D, D, D, D, D, I, I, I, I, I]),
+        "fd_plan_singular_modes": (I, [P, ctypes.POINTER(I), I, ctypes.POINTER(I)]),
+        "fd_plan_set_pinv": (I, [P, I, ctypes.POINTER(D)]),
         "fd_transform_kind_pair": (I, [I, I]),
         "fd_plan_destroy": (I, [P]),
         "fd_plan_info": (I, [P, ctypes.POINTER(I), ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(I)]),

@@ -14,13 +14,14 @@
 #include <mutex>
 #include <set>
 #include <sstream>
+#include <tuple>
 
 #include "fd_internal.h"
 
 namespace fd {
 
 Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
-                  int device, int pair = kPairDD);
+                  int device, int pair = kPairDD, int flags = 0);
 void plan_destroy(Plan *p);
 void factor_tables_host(int m, int n, double dx, double dy, double kappa, double mod_w,
                         double mod_e, double *beta, double *lower);
@@ -222,8 +223,10 @@ static void *dalloc(fd_schur_s *op, size_t bytes) {
 
 static void solve_batch(const std::vector<SolveJob> &jobs, cudaStream_t s) {
     // group by transform length (one pipeline launch per length)
-    std::map<std::pair<int, int>, std::vector<SolveJob>> groups;   // by (transform length, pair)
-    for (const auto &j : jobs) groups[{j.p.n, j.p.tpair}].push_back(j);
+    // by (transform length, pair, dense path): a periodic-sweep or pin_mean plan
+    // of an FFT length runs the dense three-kernel solve
+    std::map<std::tuple<int, int, bool>, std::vector<SolveJob>> groups;
+    for (const auto &j : jobs) groups[{j.p.n, j.p.tpair, j.p.dense != nullptr}].push_back(j);
     for (auto &g : groups) launch_solve(g.second, s);
 }
 
@@ -616,9 +619,10 @@ int fd_plan_create(fd_plan *out, int m, int n, double dx, double dy, double kapp
     FD_API_END
 }
 
-int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double kappa, double mod_west,
-                      double mod_east, double mod_south, double mod_north, int transform_axis,
-                      int transform_pair, int device) {
+int fd_plan_create_sweep(fd_plan *out, int m, int n, double dx, double dy, double kappa,
+                         double mod_west, double mod_east, double mod_south, double mod_north,
+                         int transform_axis, int transform_pair, int sweep_cyclic, int pin_mean,
+                         int device) {
     FD_API_BEGIN
     if (!out) FD_FAIL(FD_ERR_VALIDATION, "null output handle");
     *out = nullptr;
@@ -627,15 +631,19 @@ int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double k
     // a DD transform axis must carry ghost-node ends (no half-cell modifier,
     // rectsolver.py:24-29); an NN axis's Neumann ends are part of its basis
     const bool dd = transform_pair == kPairDD;
+    const int flags = (sweep_cyclic ? kPlanCyclic : 0) | (pin_mean ? kPlanPinMean : 0);
     Plan *p = nullptr;
     if (transform_axis == 0) {
         if (dd && (mod_south != 0.0 || mod_north != 0.0))
             FD_FAIL(FD_ERR_UNSUPPORTED, "DD transform along y needs ghost-node ends on south/north");
-        p = plan_create(m, n, dx, dy, kappa, mod_west, mod_east, device, transform_pair);
+        // a periodic sweep axis has no end modifiers (rectsolver.py:127-134)
+        p = plan_create(m, n, dx, dy, kappa, sweep_cyclic ? 0.0 : mod_west, sweep_cyclic ? 0.0 : mod_east,
+                        device, transform_pair, flags);
     } else if (transform_axis == 1) {
         if (dd && (mod_west != 0.0 || mod_east != 0.0))
             FD_FAIL(FD_ERR_UNSUPPORTED, "DD transform along x needs ghost-node ends on west/east");
-        p = plan_create(n, m, dy, dx, kappa, mod_south, mod_north, device, transform_pair);
+        p = plan_create(n, m, dy, dx, kappa, sweep_cyclic ? 0.0 : mod_south, sweep_cyclic ? 0.0 : mod_north,
+                        device, transform_pair, flags);
         p->transposed = true;
     } else {
         FD_FAIL(FD_ERR_VALIDATION, "transform_axis must be 0 (y) or 1 (x)");
@@ -643,6 +651,44 @@ int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double k
     p->um = m;
     p->un = n;
     *out = new fd_plan_s{p};
+    FD_API_END
+}
+
+int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double kappa, double mod_west,
+                      double mod_east, double mod_south, double mod_north, int transform_axis,
+                      int transform_pair, int device) {
+    return fd_plan_create_sweep(out, m, n, dx, dy, kappa, mod_west, mod_east, mod_south, mod_north,
+                                transform_axis, transform_pair, 0, 0, device);
+}
+
+int fd_plan_singular_modes(fd_plan plan, int *modes, int cap, int *count) {
+    FD_API_BEGIN
+    if (!plan || !count) FD_FAIL(FD_ERR_VALIDATION, "null argument");
+    const auto &sm = plan->p->sing_modes;
+    *count = (int)sm.size();
+    for (int i = 0; i < (int)sm.size() && i < cap && modes; ++i) modes[i] = sm[i];
+    FD_API_END
+}
+
+int fd_plan_set_pinv(fd_plan plan, int count, const double *pinv) {
+    FD_API_BEGIN
+    if (!plan || (count && !pinv)) FD_FAIL(FD_ERR_VALIDATION, "null argument");
+    Plan *p = plan->p;
+    if (!(p->flags & kPlanPinMean)) FD_FAIL(FD_ERR_VALIDATION, "plan was not created with pin_mean");
+    if (count != p->dev.nsing) FD_FAIL(FD_ERR_VALIDATION, "pseudo-inverse count != singular modes");
+    if (!count) return FD_OK;
+    const int m = p->dev.m;
+    std::vector<double> t(size_t(count) * m * m);   // transposed per mode: [j][i]
+    for (int c = 0; c < count; ++c)
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < m; ++j)
+                t[(size_t(c) * m + j) * m + i] = pinv[(size_t(c) * m + i) * m + j];
+    FD_CUDA(cudaSetDevice(p->device));
+    double *d = static_cast<double *>(dmalloc(sizeof(double) * t.size()));
+    p->allocs.push_back(d);
+    FD_CUDA(cudaMemcpy(d, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
+    p->dev.pinv = d;
+    p->pinv_ready = true;
     FD_API_END
 }
 

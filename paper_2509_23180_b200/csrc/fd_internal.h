@@ -61,7 +61,20 @@ struct PlanDev {
     const double2 *tw;   // FFT twiddles e^{-2 pi i t / L}, t < L = 2(n+1), or nullptr
     const double *ralpha;// [n+1] real-DST pre-weights (rsolve.cu), alpha_j = s/2 sin(pi j/N) + s/4
     int tpair;           // transform-axis pair: kPairDD (sine), kPairNN (shifted cosine), kPairPP (real Fourier)
+    // periodic sweep axis (rectsolver.py:136-153,202-205): the factors above are
+    // those of the rank-one modified system; phat -= q_k (vy_k / denom_k)
+    int cyclic;
+    const double *smq;   // [m][n] correction solves q_k
+    const double *cyc;   // [n][2]: delta/gamma_k, denom_k
+    // pin_mean singular modes (rectsolver.py:157-175,206-207): phat_k = M_k^+ fhat_k
+    int nsing;
+    const int *sidx;     // [n]: index of mode k among the singular modes, -1 otherwise
+    const double *pinv;  // [nsing][m][m] pseudo-inverses (caller-attached)
+    double *sf, *sph;    // [nsing][m] per-plan scratch: fhat columns, M^+ fhat
 };
+
+// plan flags (fd_plan_create_sweep)
+constexpr int kPlanCyclic = 1, kPlanPinMean = 2;
 
 // transform-axis BC pairs (reference transforms.BC_PAIRS, transforms.py:24)
 enum TransformPair { kPairDD = 0, kPairNN = 1, kPairPP = 2 };
@@ -141,6 +154,9 @@ struct Plan {
     std::vector<void *> allocs;
     Workspace ws;
     std::shared_ptr<Plan> shared;   // immutable device tables shared by identical plans (plan.cpp)
+    int flags = 0;                  // kPlanCyclic | kPlanPinMean
+    std::vector<int> sing_modes;    // singular spectral modes (pin_mean plans)
+    bool pinv_ready = false;
     // transform along x (reference transform_axis == "x"): the tables above are
     // those of the transposed rectangle (m, n) = (user n, user m); user-layout
     // fields are transposed into tws around the solve
@@ -181,7 +197,7 @@ void launch_transform_rows(int rows, int n, int pair, int inverse, const double 
 void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,
                      const double *dense, cudaStream_t s);
 const double2 *twiddles_for(int device, int n);
-const double *dense_table_for(int device, int n, int pair = kPairDD);
+const double *dense_table_for(int device, int n, int pair = kPairDD, bool force = false);
 
 // vector kernels (ops.cu)
 void launch_stencil(int m, int n, double delta_x, double delta_y, double kappa, double mw,

@@ -154,6 +154,10 @@ struct HostTables {
     std::vector<std::vector<double>> fl, fb;   // per mode: explicit l_i, beta_i (i < len)
     int kt = 0, ktp = 0;
     long long explicit_rows = 0;
+    // periodic sweep axis: Sherman-Morrison correction (rectsolver.py:136-153)
+    double soff = 0.0;         // sweep coupling used by the factors (2 delta when m == 2)
+    std::vector<double> smq;   // [m][n] q_k
+    std::vector<double> cyc;   // [n][2] delta/gamma_k, denom_k
 };
 
 // parallel loop over [0, n) in contiguous chunks on the host's cores
@@ -174,9 +178,11 @@ static void parallel_for(int n, F fn) {
 }
 
 static HostTables build_tables(int m, int n, double dx, double dy, double kappa, double mod_w,
-                               double mod_e, int R, bool carry_tables, int pair = kPairDD) {
+                               double mod_e, int R, bool carry_tables, int pair = kPairDD,
+                               bool cyclic = false) {
     const double delta_x = 1.0 / (dx * dx), delta_y = 1.0 / (dy * dy);
-    const double off = delta_x;
+    // periodic sweep with two rows: the wrap doubles the coupling (rectsolver.py:152-153)
+    const double off = (cyclic && m == 2) ? 2.0 * delta_x : delta_x;
     std::vector<double> lam(n);
     double amax = 0.0;
     for (int k = 0; k < n; ++k) {
@@ -188,6 +194,18 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
     const int nb = (m + R - 1) / R;
     HostTables T;
     T.lam = lam;
+    T.soff = off;
+    // per-mode end modifiers: the sweep-axis ends, or (periodic sweep, m > 2) the
+    // rank-one split of the wrap-around entries, gamma_k = -diag_0 unless that is
+    // below the pivot tolerance (rectsolver.py:139-144)
+    const bool sm = cyclic && m > 2;
+    std::vector<double> mwk(n, cyclic ? 0.0 : mod_w), mek(n, cyclic ? 0.0 : mod_e), gam(sm ? n : 0);
+    if (sm)
+        for (int k = 0; k < n; ++k) {
+            gam[k] = fabs(lam[k]) > tol ? -lam[k] : delta_x;
+            mwk[k] = -gam[k];
+            mek[k] = -(delta_x * delta_x / gam[k]);
+        }
     T.off.resize(n);
     T.len.resize(n);
     T.cv.resize(4 * size_t(n));
@@ -205,7 +223,7 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
     std::vector<BlkS> bs(n);
     parallel_for(n, [&](int k0, int k1) {
         for (int k = k0; k < k1; ++k) {
-            mf[k] = factor_mode(m, lam[k], mod_w, mod_e, off, tol, R);
+            mf[k] = factor_mode(m, lam[k], mwk[k], mek[k], off, tol, R);
             if (!carry_tables) continue;
             const ModeFactors &f = mf[k];
             const int len = (int)f.l.size();
@@ -231,6 +249,32 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
             }
         }
     });
+    if (sm) {   // q_k = A_k^-1 u, u = (gamma_k, 0, ..., 0, delta)   (rectsolver.py:145-150)
+        T.smq.assign(size_t(m) * n, 0.0);
+        T.cyc.assign(2 * size_t(n), 0.0);
+        parallel_for(n, [&](int k0, int k1) {
+            std::vector<double> y(m);
+            for (int k = k0; k < k1; ++k) {
+                ModeFactors &f = mf[k];
+                const int len = (int)f.l.size();
+                auto gl = [&](int i) { return i < len ? f.l[i] : f.l_inf; };
+                auto gb = [&](int i) { return i == m - 1 ? f.b_last : (i < len ? f.b[i] : f.b_inf); };
+                y[0] = gam[k];
+                for (int i = 1; i < m; ++i) y[i] = (i == m - 1 ? delta_x : 0.0) - gl(i) * y[i - 1];
+                double x = y[m - 1] / gb(m - 1);
+                T.smq[size_t(m - 1) * n + k] = x;
+                for (int i = m - 2; i >= 0; --i) {
+                    x = (y[i] - delta_x * x) / gb(i);
+                    T.smq[size_t(i) * n + k] = x;
+                }
+                const double r = delta_x / gam[k];
+                const double den = 1.0 + T.smq[k] + r * T.smq[size_t(m - 1) * n + k];
+                T.cyc[2 * k] = r;
+                T.cyc[2 * k + 1] = den;
+                if (fabs(den) < 1e-12) f.bad = true;   // rectsolver.py:151
+            }
+        });
+    }
     size_t total = 0;
     for (int k = 0; k < n; ++k) {
         const ModeFactors &f = mf[k];
@@ -349,8 +393,8 @@ const double2 *twiddles_for(int device, int n) {
     return (const double2 *)d;
 }
 
-const double *dense_table_for(int device, int n, int pair) {
-    if (transform_kind(n, pair) != kDense) return nullptr;
+const double *dense_table_for(int device, int n, int pair, bool force) {
+    if (transform_kind(n, pair) != kDense && !(force && n <= 1024)) return nullptr;
     std::lock_guard<std::mutex> g(g_tab_mu);
     auto key = std::make_pair(device, n + (pair << 24));
     auto it = g_dense.find(key);
@@ -391,19 +435,24 @@ static T *upload(Plan *p, const std::vector<T> &h) {
 }
 
 static Plan *build_proto(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
-                         int device, int pair) {
+                         int device, int pair, int flags) {
     if (m < 1 || n < 1) FD_FAIL(FD_ERR_VALIDATION, "plan: empty grid");
     if (!(dx > 0) || !(dy > 0)) FD_FAIL(FD_ERR_VALIDATION, "plan: nonpositive spacing");
-    const int tk = transform_kind(n, pair);
+    const bool cyclic = flags & kPlanCyclic, pin = flags & kPlanPinMean;
+    if (cyclic && (m % 2)) FD_FAIL(FD_ERR_VALIDATION, "plan: periodic sweep axis needs an even count");
+    int tk = transform_kind(n, pair);
+    // the correction and pseudo-inverse terms live in the three-kernel dense solve
+    const bool forced = tk == kFFT && (cyclic || pin);
+    if (forced) tk = n <= 1024 ? kDense : -1;   // dense transform limit (dst_device.cuh kDenseMax)
     if (tk < 0) {
         std::ostringstream os;
         os << "plan: no GPU transform for n = " << n
            << " (supported: n+1 a power of two in [256, 4096], or n <= 1024)";
         FD_FAIL(FD_ERR_UNSUPPORTED, os.str());
     }
-    const int R = rows_per_block(n, pair);
-    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R, tk == kDense, pair);
-    if (!T.bad_modes.empty()) {
+    const int R = forced ? 8 : rows_per_block(n, pair);   // forced: the dense path's rows per group
+    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R, tk == kDense, pair, cyclic);
+    if (!T.bad_modes.empty() && !pin) {
         std::ostringstream os;
         os << "operator singular in spectral modes (";
         for (size_t i = 0; i < T.bad_modes.size() && i < 16; ++i) os << (i ? ", " : "") << T.bad_modes[i];
@@ -430,7 +479,7 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.n = n;
         d.R = R;
         d.nb = (m + R - 1) / R;
-        d.off = p->delta_x;
+        d.off = T.soff;
         d.mod_w = mod_w;
         d.mod_e = mod_e;
         d.tpair = pair;
@@ -498,7 +547,18 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.ye = d.fs = nullptr;   // per-plan scratch (plan_create)
         d.tw = tk == kFFT ? twiddles_for(device, n) : nullptr;
         d.ralpha = d.tw ? reinterpret_cast<const double *>(d.tw + 2 * (n + 1)) : nullptr;
-        d.dense = dense_table_for(device, n, pair);
+        d.dense = dense_table_for(device, n, pair, forced);
+        p->flags = flags;
+        d.cyclic = !T.smq.empty();
+        d.smq = d.cyclic ? upload(p, T.smq) : nullptr;
+        d.cyc = d.cyclic ? upload(p, T.cyc) : nullptr;
+        p->sing_modes = T.bad_modes;
+        d.nsing = (int)T.bad_modes.size();
+        if (d.nsing) {
+            std::vector<int> sidx(n, -1);
+            for (int i = 0; i < d.nsing; ++i) sidx[T.bad_modes[i]] = i;
+            d.sidx = upload(p, sidx);
+        }
     } catch (...) {
         cudaDeviceSynchronize();
         for (void *a : p->allocs) dfree(a);
@@ -522,10 +582,11 @@ static void free_tables(Plan *p) {
 // repeated solves on the same geometry reuse the last few builds (LRU).
 namespace {
 struct PlanKey {
-    int device, m, n, pair;
+    int device, m, n, pair, flags;
     double v[5];
     bool operator==(const PlanKey &o) const {
-        return device == o.device && m == o.m && n == o.n && pair == o.pair && memcmp(v, o.v, sizeof(v)) == 0;
+        return device == o.device && m == o.m && n == o.n && pair == o.pair && flags == o.flags &&
+               memcmp(v, o.v, sizeof(v)) == 0;
     }
 };
 constexpr size_t kPlanCache = 8;
@@ -534,8 +595,8 @@ auto *g_plan_lru = new std::list<std::pair<PlanKey, std::shared_ptr<Plan>>>();  
 }  // namespace
 
 Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w, double mod_e,
-                  int device, int pair) {
-    PlanKey key{device, m, n, pair, {dx, dy, kappa, mod_w, mod_e}};
+                  int device, int pair, int flags) {
+    PlanKey key{device, m, n, pair, flags, {dx, dy, kappa, mod_w, mod_e}};
     std::shared_ptr<Plan> proto;
     {
         std::lock_guard<std::mutex> g(g_plan_mu);
@@ -547,7 +608,7 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
             }
     }
     if (!proto) {
-        proto = std::shared_ptr<Plan>(build_proto(m, n, dx, dy, kappa, mod_w, mod_e, device, pair), free_tables);
+        proto = std::shared_ptr<Plan>(build_proto(m, n, dx, dy, kappa, mod_w, mod_e, device, pair, flags), free_tables);
         std::lock_guard<std::mutex> g(g_plan_mu);
         g_plan_lru->emplace_front(key, proto);
         if (g_plan_lru->size() > kPlanCache) g_plan_lru->pop_back();
@@ -569,8 +630,19 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
     p->dev = proto->dev;
     p->tprof = proto->tprof;
     p->shared = proto;
+    p->flags = proto->flags;
+    p->sing_modes = proto->sing_modes;
+    p->dev.pinv = nullptr;   // pseudo-inverses are attached per plan (fd_plan_set_pinv)
+    p->dev.sf = p->dev.sph = nullptr;
     if (p->transform == kDense) {   // pass-1/carry scratch of the three-kernel solve
         try {
+            if (p->dev.nsing) {
+                const size_t sb = sizeof(double) * size_t(p->dev.nsing) * m;
+                p->dev.sf = static_cast<double *>(dmalloc(sb));
+                p->allocs.push_back(p->dev.sf);
+                p->dev.sph = static_cast<double *>(dmalloc(sb));
+                p->allocs.push_back(p->dev.sph);
+            }
             const size_t bytes = sizeof(double) * size_t(p->dev.nb) * n;
             p->dev.ye = static_cast<double *>(dmalloc(bytes));
             p->allocs.push_back(p->dev.ye);

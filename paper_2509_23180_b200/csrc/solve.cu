@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) pass1_kernel(const __grid_cons
             if (k >= n) continue;
             ModeView mv;
             mv.load(p, k);
+            const int si = p.nsing ? __ldg(p.sidx + k) : -1;
             double y = yh[u], w = pi[u], f = fs[u];
             double lv[P::G], ibv[P::G];   // the group's factors, loaded ahead of the chain
 #pragma unroll
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(P::NT, P::MINB) pass1_kernel(const __grid_cons
                 if (rr >= rows) break;
                 const int i = g0 + rr;
                 const double r = rowbuf[rr * n + k];
+                if (si >= 0) p.sf[size_t(si) * m + i] = r;   // fhat column of a pinned mode
                 if (i == s) {
                     y = r;
                     w = 1.0;
@@ -389,6 +391,19 @@ __global__ void __launch_bounds__(kCarryThreads) carry_kernel(const __grid_const
 }
 
 // ---------------------------------------------------------------------------
+// pinned (singular) modes: sph = M_k^+ fhat_k, pinv stored transposed [j][i]
+__global__ void __launch_bounds__(256) pinv_kernel(int m, int nsing, const double *pinvT,
+                                                   const double *sf, double *sph) {
+    const int i = blockIdx.x * 256 + threadIdx.x, si = blockIdx.y;
+    if (i >= m) return;
+    const double *P = pinvT + size_t(si) * m * m;
+    const double *f = sf + size_t(si) * m;
+    double acc = 0.0;
+    for (int j = 0; j < m; ++j) acc = fma(__ldg(P + size_t(j) * m + i), f[j], acc);
+    sph[size_t(si) * m + i] = acc;
+}
+
+// ---------------------------------------------------------------------------
 // pass 2: carry fix-up + back-substitution (rows descending) + inverse DST
 template <class P>
 __global__ void __launch_bounds__(P::NT, P::MINB) pass2_kernel(const __grid_constant__ JobList jl) {
@@ -402,15 +417,23 @@ __global__ void __launch_bounds__(P::NT, P::MINB) pass2_kernel(const __grid_cons
     const int s = b * p.R, e = min(m, s + p.R) - 1;
     const double off = p.off;
     double *rowbuf = reinterpret_cast<double *>(smem);
-    double yin[MPT], xn[MPT], pc[MPT];
+    double yin[MPT], xn[MPT], pc[MPT], cc[MPT];
 #pragma unroll
     for (int u = 0; u < MPT; ++u) {
         const int k = threadIdx.x + u * P::NT;
-        yin[u] = xn[u] = pc[u] = 0.0;
+        yin[u] = xn[u] = pc[u] = cc[u] = 0.0;
         if (k < n) {
             if (b > 0) yin[u] = p.ye[size_t(b - 1) * n + k];
             if (b < p.nb - 1) xn[u] = p.fs[size_t(b + 1) * n + k];
             pc[u] = __ldg(p.blk + (size_t(b) * 3 + 0) * n + k);   // P at row e
+            if (p.cyclic) {
+                // Sherman-Morrison factor from the carried ends: x_0 = X_0,
+                // x_{m-1} = Y_{m-1} / beta_{m-1}   (rectsolver.py:203-205)
+                const double x0 = p.fs[k];
+                const double xl = __ddiv_rn(p.ye[size_t(p.nb - 1) * n + k], __ldg(p.last + 2 * k));
+                const double vy = __dadd_rn(x0, __dmul_rn(__ldg(p.cyc + 2 * k), xl));
+                cc[u] = __ddiv_rn(vy, __ldg(p.cyc + 2 * k + 1));
+            }
         }
     }
     const int glast = s + ((e - s) / P::G) * P::G;
@@ -450,7 +473,13 @@ __global__ void __launch_bounds__(P::NT, P::MINB) pass2_kernel(const __grid_cons
                 }
                 const double bi = bv[rr];
                 x = __ddiv_rn(__dsub_rn(y, __dmul_rn(off, x)), bi);   // rectsolver.py:90
-                rowbuf[rr * n + k] = x;
+                double xo = x;
+                if (p.cyclic) xo = __dsub_rn(x, __dmul_rn(__ldg(p.smq + size_t(i) * n + k), cc[u]));
+                if (p.nsing) {
+                    const int si = __ldg(p.sidx + k);
+                    if (si >= 0) xo = p.sph[size_t(si) * m + i];   // rectsolver.py:206-207
+                }
+                rowbuf[rr * n + k] = xo;
             }
             xn[u] = x;
             pc[u] = pcur;
@@ -543,6 +572,13 @@ static void run_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
         FD_CUDA(cudaGetLastError());
         carry_kernel<<<totc, kCarryThreads, 0, s>>>(jc);
         FD_CUDA(cudaGetLastError());
+        for (int j = 0; j < jl.count; ++j) {
+            const PlanDev &p = jl.job[j].p;
+            if (!p.nsing) continue;
+            if (!p.pinv) FD_FAIL(FD_ERR_SINGULAR, "plan is singular (pin_mean plan without pseudo-inverses)");
+            pinv_kernel<<<dim3((p.m + 255) / 256, p.nsing), 256, 0, s>>>(p.m, p.nsing, p.pinv, p.sf, p.sph);
+            FD_CUDA(cudaGetLastError());
+        }
         pass2_kernel<P><<<tot, P::NT, P::SMEM, s>>>(jl);
         FD_CUDA(cudaGetLastError());
     }

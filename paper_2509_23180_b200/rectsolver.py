@@ -36,7 +36,7 @@ def _gpu_axis(sub: RectSubdomain) -> str:
     transformable x axis (the reference's own transform_axis = "x" branch):
     the FFT stays within one SM's shared memory and the long axis becomes the
     Thomas sweep.  Same operator, rounding-level differences only.  A periodic
-    sweep axis (cyclic Thomas) is not on the GPU path."""
+    sweep axis runs the cyclic (Sherman-Morrison) solve on the dense path."""
     def pair_of(axis):
         try:
             return sub.axis_pair(axis)
@@ -63,24 +63,38 @@ def _gpu_axis(sub: RectSubdomain) -> str:
         raise UnsupportedError(
             f"subdomain {sub.id}: neither axis is a transformable pair on the GPU path "
             f"(got y {pair_of('y')}, x {pair_of('x')} with end modifiers)")
-    sweep = "x" if axis == "y" else "y"
-    if pair_of(sweep) == "PP":
-        raise UnsupportedError(f"subdomain {sub.id}: periodic sweep axis is not on the GPU path")
     return axis
 
 
 class _Handle:
     """Owns one native plan handle."""
 
-    def __init__(self, sub: RectSubdomain, axis: str):
+    def __init__(self, sub: RectSubdomain, axis: str, cyclic: bool = False, pin_mean: bool = False):
         _native.require_cuda()
         h = _native.P()
         pair = _PAIR_CODE[sub.axis_pair(axis)]
-        _native.call("fd_plan_create_ex", ctypes_ref(h), sub.m, sub.n, float(sub.dx), float(sub.dy),
+        _native.call("fd_plan_create_sweep", ctypes_ref(h), sub.m, sub.n, float(sub.dx), float(sub.dy),
                      float(sub.kappa), float(sub.end_modifier("west")), float(sub.end_modifier("east")),
                      float(sub.end_modifier("south")), float(sub.end_modifier("north")),
-                     0 if axis == "y" else 1, pair, _native.torch().cuda.current_device())
+                     0 if axis == "y" else 1, pair, int(cyclic), int(pin_mean),
+                     _native.torch().cuda.current_device())
         self.ptr = h
+
+    def singular_modes(self) -> tuple:
+        import ctypes
+        cnt = _native.I()
+        _native.call("fd_plan_singular_modes", self.ptr, None, 0, ctypes.byref(cnt))
+        if not cnt.value:
+            return ()
+        buf = (_native.I * cnt.value)()
+        _native.call("fd_plan_singular_modes", self.ptr, buf, cnt.value, ctypes.byref(cnt))
+        return tuple(int(v) for v in buf)
+
+    def set_pinv(self, mats) -> None:
+        import ctypes
+        arr = np.ascontiguousarray(np.stack(mats), dtype=np.float64)
+        _native.call("fd_plan_set_pinv", self.ptr, len(mats),
+                     arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
 
     def __del__(self):
         try:
@@ -106,13 +120,17 @@ class RectPlan:
     off: float
     handle: _Handle = field(repr=False, compare=False)
     pin_mean: bool = False
+    cyclic: bool = False
+    singular_modes: tuple = ()
 
     @property
     def singular(self) -> bool:
-        return False
+        return bool(self.singular_modes)
 
     @property
     def x_solver_kind(self) -> str:
+        if self.cyclic:
+            return "cyclic"
         return "corner-modified" if self.solve_pair == "NN" else "standard-tridiagonal"
 
     def info(self) -> dict:
@@ -124,22 +142,53 @@ class RectPlan:
                 "transform": ("dense", "fft")[tk.value]}
 
 
+def _sweep_matrix(lam_k: float, ms: int, off: float, cyclic: bool, mod_lo: float, mod_hi: float):
+    """Dense per-mode sweep matrix of a singular mode (rectsolver.py:164-173)."""
+    d = np.full(ms, lam_k)
+    if not cyclic:
+        d[0] += mod_lo
+        d[-1] += mod_hi
+    M = np.diag(d)
+    idx = np.arange(ms - 1)
+    M[idx, idx + 1] += off
+    M[idx + 1, idx] += off
+    if cyclic:
+        M[0, ms - 1] += off
+        M[ms - 1, 0] += off
+    return M
+
+
 def plan_rect(subdomain: RectSubdomain, pin_mean: bool = False) -> RectPlan:
-    """GPU plan; SingularOperatorError on a zero pivot (ref rectsolver.py:94-180)."""
+    """GPU plan (ref rectsolver.py:94-180).  SingularOperatorError on a zero
+    pivot unless pin_mean is set; then the singular modes are solved in the
+    minimum-norm sense: their sweep matrices' pseudo-inverses are formed here
+    at plan time (host setup, like the reference's dense mode matrices) and
+    applied on the device inside the solve."""
     sub = subdomain
-    if pin_mean:
-        raise UnsupportedError("pin_mean (singular all-Neumann operators) is not on the GPU path")
     _native.require_cuda()
     axis = _gpu_axis(sub)
     if axis == "y":
         lam_plan = transforms.make_plan(sub.axis_pair("y"), sub.n, sub.delta_y, sub.delta_x, sub.kappa)
-        pair, off = sub.axis_pair("x"), sub.delta_x
+        pair, off, ms, lo, hi = sub.axis_pair("x"), sub.delta_x, sub.m, "west", "east"
     else:
         lam_plan = transforms.make_plan(sub.axis_pair("x"), sub.m, sub.delta_x, sub.delta_y, sub.kappa)
-        pair, off = sub.axis_pair("y"), sub.delta_y
-    handle = _Handle(sub, axis)
+        pair, off, ms, lo, hi = sub.axis_pair("y"), sub.delta_y, sub.n, "south", "north"
+    cyclic = pair == "PP"
+    if cyclic and ms % 2:
+        raise ValidationError(f"subdomain {sub.id}: periodic sweep axis needs an even count")
+    handle = _Handle(sub, axis, cyclic=cyclic, pin_mean=pin_mean)
+    singular = handle.singular_modes() if pin_mean else ()
+    if singular:
+        lam = np.asarray(lam_plan.eigenvalues)
+        mats = []
+        for k in singular:
+            M = _sweep_matrix(lam[k], ms, off, cyclic, sub.end_modifier(lo), sub.end_modifier(hi))
+            # lstsq(M, f, rcond=None) == pinv(M) f with the same cutoff (rectsolver.py:207)
+            mats.append(np.linalg.pinv(M, rcond=np.finfo(float).eps * ms))
+        handle.set_pinv(mats)
     return RectPlan(subdomain=sub, transform_axis=axis, y_plan=lam_plan,
-                    solve_pair=pair, off=off, handle=handle)
+                    solve_pair=pair, off=off, handle=handle, pin_mean=pin_mean,
+                    cyclic=cyclic, singular_modes=tuple(singular))
 
 
 def solve_rect(plan: RectPlan, f) -> GridField:

@@ -2,7 +2,7 @@
 
 Run in the build container only (needs /root/reference):
 
-    python tests/golden/make_golden.py small c0 c1 nn     # seconds
+    python tests/golden/make_golden.py small c0 c1 nn cyclic   # seconds
     python tests/golden/make_golden.py c2 c3              # minutes (c3 ~15 min, 16 GB)
 
 The reference package is imported from /root/reference/pkg/src; its inputs
@@ -236,12 +236,60 @@ def make_nn():
     print("nn.npz written")
 
 
+# periodic sweep axes (x periodic, transform along y): the Sherman-Morrison
+# cyclic solve (rectsolver.py:136-153,202-205), m even
+CYC_RECT_CASES = [
+    (4, 3, 1.0, 1.0, 0.0, "PPDD", ()),
+    (2, 5, 0.5, 0.25, 0.0, "PPDD", ()),              # two rows: doubled coupling
+    (16, 12, 0.1, 0.1, 0.0, "PPDD", ()),
+    (24, 16, 0.1, 0.1, -1.0, "PPNN", ()),
+    (20, 12, 0.1, 0.1, -1.0, "PPPP", ()),
+    (130, 141, 1.0 / 130, 1.0 / 141, -2.0, "PPDD", ()),
+    (256, 63, 1.0 / 256, 1.0 / 64, 0.0, "PPDD", ()),  # many carry blocks
+    (64, 255, 1.0 / 64, 1.0 / 256, 0.0, "PPDD", ()),  # an FFT length on the dense solve
+]
+# pin_mean: singular all-Neumann / periodic operators, mean-zero right-hand sides
+PIN_RECT_CASES = [
+    (3, 3, 1.0, 1.0, 0.0, "NNNN", ()),
+    (8, 6, 0.1, 0.2, 0.0, "NNNN", ()),
+    (6, 8, 0.1, 0.1, 0.0, "PPPP", ()),
+    (16, 12, 0.1, 0.1, 0.0, "PPNN", ()),
+    (12, 10, 0.1, 0.1, 0.0, "NNPP", ()),
+    (40, 33, 1.0 / 40, 1.0 / 33, 0.0, "NNNN", ()),
+]
+
+
+def make_cyclic():
+    """Periodic-sweep and pin_mean rectangle solves by the reference."""
+    out = {}
+    rng = np.random.default_rng(21)
+    for c, case in enumerate(CYC_RECT_CASES):
+        sub = rect(*case)
+        pl = rectsolver.plan_rect(sub)
+        assert pl.x_solver_kind == "cyclic"
+        f = rng.standard_normal(sub.size)
+        out[f"cyc_f_{c}"] = f
+        out[f"cyc_p_{c}"] = rectsolver.solve_rect(pl, f).values
+    for c, case in enumerate(PIN_RECT_CASES):
+        sub = rect(*case)
+        pl = rectsolver.plan_rect(sub, pin_mean=True)
+        f = rng.standard_normal(sub.size)
+        f -= f.mean()
+        out[f"pin_modes_{c}"] = np.asarray(pl.singular_modes, dtype=np.int64)
+        out[f"pin_f_{c}"] = f
+        out[f"pin_p_{c}"] = rectsolver.solve_rect(pl, f).values
+    np.savez_compressed(os.path.join(HERE, "cyclic.npz"), **out)
+    print("cyclic.npz written")
+
+
 if __name__ == "__main__":
     for what in sys.argv[1:] or ["small", "c0", "c1"]:
         if what == "small":
             make_small()
         elif what == "nn":
             make_nn()
+        elif what == "cyclic":
+            make_cyclic()
         elif what == "c1":
             make_c1()
         else:

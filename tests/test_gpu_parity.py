@@ -478,6 +478,73 @@ class TestDeviceAssembly:
         assert configs.rel_l2_device(fields, exd) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-4)
 
 
+class TestPeriodicSweep:
+    """Periodic sweep axes (Sherman-Morrison cyclic Thomas) and pin_mean
+    minimum-norm modes on the GPU (rectsolver.py:136-175,202-207), against
+    fixtures written by the reference and the oracle."""
+
+    @pytest.mark.parametrize("c", range(8))
+    def test_cyclic_golden(self, c):
+        from rects import CYC_RECT_CASES
+        g = load_golden("cyclic")
+        pl = rectsolver.plan_rect(make(CYC_RECT_CASES[c]))
+        assert pl.x_solver_kind == "cyclic"
+        p = rectsolver.solve_rect(pl, g[f"cyc_f_{c}"]).values
+        assert rel(p, g[f"cyc_p_{c}"]) < 1e-12
+
+    @pytest.mark.parametrize("c", range(6))
+    def test_pin_mean_golden(self, c):
+        from paper_2509_23180_b200.errors import SingularOperatorError
+        from rects import PIN_RECT_CASES
+        g = load_golden("cyclic")
+        sub = make(PIN_RECT_CASES[c])
+        with pytest.raises(SingularOperatorError):
+            rectsolver.plan_rect(sub)
+        pl = rectsolver.plan_rect(sub, pin_mean=True)
+        assert pl.singular and list(pl.singular_modes) == g[f"pin_modes_{c}"].tolist()
+        p = rectsolver.solve_rect(pl, g[f"pin_f_{c}"]).values
+        ref = g[f"pin_p_{c}"]
+        assert np.abs(p - ref).max() <= 1e-10 * max(np.abs(ref).max(), 1.0)
+
+    def test_pin_mean_zero_mean_solution(self):
+        """The reference's own check (test_rectsolver.py:88-95)."""
+        sub = make((3, 3, 1.0, 1.0, 0.0, "NNNN", ()))
+        pl = rectsolver.plan_rect(sub, pin_mean=True)
+        f = np.arange(9.0) - 4.0
+        p = rectsolver.solve_rect(pl, f).values
+        assert np.abs(rectsolver.apply_rect_operator(sub, p) - f).max() < 1e-10
+        assert abs(p.mean()) < 1e-12
+
+    def test_pair_sweep(self):
+        """Every transform/sweep pair, m, n <= 5 (test_rectsolver.py:15-27,
+        126-135): GPU against the oracle and the periodic-wrap residual."""
+        from rects import pair_cases, pair_rect
+        rng = np.random.default_rng(9)
+        for case in pair_cases(5):
+            sub = pair_rect(*case)
+            f = rng.standard_normal(sub.size)
+            p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f).values
+            want = O.solve(O.plan(sub), f)
+            scale = max(np.abs(want).max(), 1.0)
+            assert np.abs(p - want).max() <= 1e-11 * scale, case
+            r = rectsolver.apply_rect_operator(sub, p) - f
+            assert np.abs(r).max() <= 1e-10 * max(np.abs(f).max(), 1.0), case
+
+    @pytest.mark.parametrize("m,n", [(2, 1), (2, 1023), (512, 100), (1000, 1024)])
+    def test_against_oracle_and_residual(self, m, n, rng):
+        sub = make((m, n, 1.0 / m, 1.0 / n, -0.5, "PPDD", ()))
+        f = rng.uniform(-1, 1, sub.size)
+        p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f).values
+        assert rel(p, O.solve(O.plan(sub), f)) < 1e-11
+        r = rectsolver.apply_rect_operator(sub, p) - f
+        assert np.linalg.norm(r) / np.linalg.norm(f) < 1e-10
+
+    def test_odd_periodic_count_rejected(self):
+        from paper_2509_23180_b200.errors import ValidationError
+        with pytest.raises(ValidationError):
+            rectsolver.plan_rect(make((5, 4, 0.2, 0.25, 0.0, "PPDD", ())))
+
+
 class TestEdgeCases:
     """Error paths and degenerate inputs the reference tests."""
 

@@ -142,3 +142,48 @@ class TestNeumannTransformFixtures:
         assert rep.iterations == int(golden_nn[f"x_iters_{key}"])
         for s in comp.subdomains:
             assert rel(fields[s.id], golden_nn[f"x_p_{key}_{s.id}"]) < 1e-12
+
+
+class TestPeriodicSweepFixtures:
+    """Periodic sweep axes (Sherman-Morrison cyclic solve, rectsolver.py:136-153,
+    202-205) and pin_mean minimum-norm modes (rectsolver.py:157-175,206-207),
+    against fixtures written by the reference (make_golden.py cyclic)."""
+
+    @pytest.mark.parametrize("c", range(8))
+    def test_cyclic_rect(self, c):
+        from rects import CYC_RECT_CASES
+        g = load_golden("cyclic")
+        pl = O.plan(make(CYC_RECT_CASES[c]))
+        assert pl.cyclic
+        np.testing.assert_array_equal(O.solve(pl, g[f"cyc_f_{c}"]), g[f"cyc_p_{c}"])
+
+    @pytest.mark.parametrize("c", range(6))
+    def test_pin_mean_rect(self, c):
+        from rects import PIN_RECT_CASES
+        g = load_golden("cyclic")
+        sub = make(PIN_RECT_CASES[c])
+        with pytest.raises(O.SingularOracleError):
+            O.plan(sub)
+        pl = O.plan(sub, pin_mean=True)
+        assert list(pl.singular) == g[f"pin_modes_{c}"].tolist()
+        p = O.solve(pl, g[f"pin_f_{c}"])
+        np.testing.assert_array_equal(p, g[f"pin_p_{c}"])
+        # the GPU shim's pseudo-inverse form of lstsq (rectsolver.plan_rect)
+        for M in pl.singular_dense:
+            f = np.random.default_rng(3).standard_normal(M.shape[0])
+            f -= f.mean()
+            a = np.linalg.lstsq(M, f, rcond=None)[0]
+            b = np.linalg.pinv(M, rcond=np.finfo(float).eps * M.shape[0]) @ f
+            assert np.abs(a - b).max() <= 1e-13 * max(np.abs(a).max(), 1.0)
+
+    def test_pair_sweep_residual(self):
+        """Every transform/sweep pair on small grids: A p = f with the oracle's
+        own stencil (periodic wrap included)."""
+        from rects import pair_cases, pair_rect
+        rng = np.random.default_rng(5)
+        for case in pair_cases(5):
+            sub = pair_rect(*case)
+            f = rng.standard_normal(sub.size)
+            p = O.solve(O.plan(sub), f)
+            r = O.apply_operator(sub, p) - f
+            assert np.abs(r).max() <= 1e-10 * max(np.abs(f).max(), 1.0), case
