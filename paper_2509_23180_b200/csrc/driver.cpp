@@ -191,7 +191,8 @@ struct fd_schur_s {
     fd::Scratch sc{};
     // low-synchronisation Arnoldi: Gram rows, partials, results (device) + pinned mirror
     fd::ArnWork arn{};
-    double *arn_out = nullptr, *arn_host = nullptr;
+    double *arn_out = nullptr, *arn_host = nullptr;   // arn_host: two slots of kArnSlot
+    cudaEvent_t arn_ev[2] = {nullptr, nullptr};        // a slot's results have landed
     // interface-only (Steklov) neighbour applies: per arm the
     // line positions of the R_ic / R_ci entries and the interface-end inverse
     // pivots; line buffers [arms][L]
@@ -410,6 +411,8 @@ static void unprecond_apply(fd_schur_s *op, const double *p, double *out, cudaSt
     launch_axpby(N, 1.0, op->tmp2, -1.0, out, out, s);
 }
 
+constexpr size_t kArnSlot = 2 * kMaxArnoldi + 4;   // doubles per host result slot
+
 static void ensure_arnoldi(fd_schur_s *op) {
     if (op->arn.partials) return;
     op->arn.partials = (double *)dalloc(op, sizeof(double) * kArnPartials);
@@ -417,15 +420,23 @@ static void ensure_arnoldi(fd_schur_s *op) {
     FD_CUDA(cudaMemset(op->arn.counter, 0, sizeof(unsigned int)));
     op->arn.G = (double *)dalloc(op, sizeof(double) * kMaxArnoldi * kMaxArnoldi);
     op->arn_out = (double *)dalloc(op, sizeof(double) * (2 * kMaxArnoldi + 4));
-    op->arn_host = (double *)pinned_get(sizeof(double) * (2 * kMaxArnoldi + 4));
+    op->arn_host = (double *)pinned_get(sizeof(double) * 2 * kArnSlot);
+    for (auto &e : op->arn_ev) FD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 
 // Arnoldi step on the operator's basis with the low-synchronisation MGS of
 // ops.cu (two passes over V instead of k + 1): h[0..k] projections, h[k+1] =
 // ||w|| after, *w_norm = ||w|| before; V[k+1] = w / h[k+1] is formed on the
 // device (unused by the caller on breakdown, like the reference).
-static void arnoldi_step_ls(fd_schur_s *op, long long N, int k, double *h, double *w_norm,
-                            cudaStream_t s) {
+//
+// Split in two so the GMRES loop can pipeline: arnoldi_enqueue puts step k's
+// operator apply, both passes, the normalisation and the copy of its results
+// into host slot k % 2 on the stream; arnoldi_collect waits for that slot.
+// Step k + 1 only needs V[k+1], which the device forms itself, so the loop
+// enqueues it before it reads step k's column: the host round trip (copy,
+// wake-up, Givens, the next launches) no longer leaves the GPU idle.
+static void arnoldi_enqueue(fd_schur_s *op, long long N, int k, cudaStream_t s) {
+    precond_apply_loop(op, op->V + (long long)k * N, s);   // -> w
     ArnWork a = op->arn;
     a.out = op->arn_out;
     launch_arnoldi_dots(N, k, op->V, op->w, a, kMaxArnoldi, s);
@@ -433,12 +444,16 @@ static void arnoldi_step_ls(fd_schur_s *op, long long N, int k, double *h, doubl
     b.out = op->arn_out + kMaxArnoldi + 2;
     launch_arnoldi_update(N, k, op->V, op->w, a.out, b, s);
     launch_scale_sqrt(N, op->w, b.out, op->V + (long long)(k + 1) * N, s);
-    FD_CUDA(cudaMemcpyAsync(op->arn_host, op->arn_out, sizeof(double) * (kMaxArnoldi + 3),
+    FD_CUDA(cudaMemcpyAsync(op->arn_host + (k & 1) * kArnSlot, op->arn_out, sizeof(double) * (kMaxArnoldi + 3),
                             cudaMemcpyDeviceToHost, s));
-    FD_CUDA(cudaStreamSynchronize(s));
-    for (int i = 0; i <= k; ++i) h[i] = op->arn_host[i];
-    *w_norm = sqrt(op->arn_host[k + 1]);
-    h[k + 1] = sqrt(op->arn_host[kMaxArnoldi + 2]);
+    FD_CUDA(cudaEventRecord(op->arn_ev[k & 1], s));
+}
+static void arnoldi_collect(fd_schur_s *op, int k, double *h, double *w_norm) {
+    FD_CUDA(cudaEventSynchronize(op->arn_ev[k & 1]));
+    const double *o = op->arn_host + (k & 1) * kArnSlot;
+    for (int i = 0; i <= k; ++i) h[i] = o[i];
+    *w_norm = sqrt(o[k + 1]);
+    h[k + 1] = sqrt(o[kMaxArnoldi + 2]);
 }
 
 static void ensure_basis(fd_schur_s *op, int m) {
@@ -507,13 +522,19 @@ static int gmres_precond(fd_schur_s *op, const double *rhs, double *x, int x_is_
         g[0] = beta;
         int k_used = 0;
         bool breakdown = false;
+        if (lowsync) arnoldi_enqueue(op, N, 0, s);
         for (int k = 0; k < m; ++k) {
-            precond_apply_loop(op, op->V + (long long)k * N, s);   // -> w
             double w_norm = 0.0;
-            if (lowsync)
-                arnoldi_step_ls(op, N, k, hcol.data(), &w_norm, s);
-            else
+            if (lowsync) {
+                // step k + 1 is enqueued before step k's column is read; if step k
+                // ends the cycle (breakdown, convergence) that work is discarded:
+                // it touches only w, V[k+2], the Gram row k+1 and the other slot
+                if (k + 1 < m) arnoldi_enqueue(op, N, k + 1, s);
+                arnoldi_collect(op, k, hcol.data(), &w_norm);
+            } else {
+                precond_apply_loop(op, op->V + (long long)k * N, s);   // -> w
                 arnoldi_step(N, k, op->V, w, hcol.data(), &w_norm, sc, s);
+            }
             for (int i = 0; i <= k; ++i) Hat(i, k) = hcol[i];
             const double h_next = hcol[k + 1];
             Hat(k + 1, k) = h_next;
@@ -914,6 +935,8 @@ int fd_schur_destroy(fd_schur op) {
         if (op->V) dfree(op->V);
         if (op->sc.cap) free_scratch(op->sc);
         pinned_put(op->arn_host);
+        for (auto e : op->arn_ev)
+            if (e) cudaEventDestroy(e);
         delete op;
         ht.mark("done", 0, false);
     }
