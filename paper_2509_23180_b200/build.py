@@ -50,6 +50,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
               "-I", os.path.join(os.path.dirname(HERE), "include")] + ARCH
     if os.environ.get("FD_DIAG_BUILD"):   # trace / component-skip diagnostics (tools/dbg_sweep.sh)
         common += ["-DFD_DIAG=1"]
+    common += os.environ.get("FD_EXTRA_FLAGS", "").split()   # A/B variants (tools/ab_so.sh)
     jobs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
