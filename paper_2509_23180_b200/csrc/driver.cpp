@@ -11,6 +11,7 @@
 
 #include <chrono>
 #include <map>
+#include <unordered_map>
 #include <mutex>
 #include <set>
 #include <sstream>
@@ -203,6 +204,10 @@ struct fd_schur_s {
     };
     std::vector<Steklov> stk;
     bool steklov = false;
+    // the R_ci scatter-adds of all neighbours in one atomic launch: every centre
+    // entry receives at most two contributions (checked at create), so the sum
+    // onto the zero vector does not depend on their order
+    bool fused_add = false;
     // small problems: the preconditioned apply (a dozen short launches) replayed
     // as one CUDA graph on a fixed input buffer (0 untried, 2 warmed, 1 ready, -1 off)
     int graph_state = 0;
@@ -293,7 +298,41 @@ static void solve_user(const std::vector<UJob> &uj, cudaStream_t s) {
 // y = r on the line row and the back-substitution's interface value is
 // y / beta_end -- the arm's full solve yields exactly these values there.
 // O(L log L) per arm instead of a full arm solve.
-static void schur_apply_steklov(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
+// R_ci parts of every neighbour added into out (zero): one atomic launch when
+// fused_add holds, else one ordered launch per neighbour (ddm.py:120-122)
+static void scatter_add_parts(fd_schur_s *op, const std::vector<const int64_t *> &from,
+                              const std::vector<const double *> &src, double *out, cudaStream_t s) {
+    const size_t nnb = op->nb.size();
+    if (op->fused_add) {
+        ScatterBatch b;
+        b.count = (int)nnb;
+        for (size_t i = 0; i < nnb; ++i) {
+            const Coupling &c = op->to_c[i];
+            b.len[i] = c.len;
+            b.from[i] = from[i];
+            b.to[i] = c.to;
+            b.c[i] = c.c;
+            b.src[i] = src[i];
+            b.dst[i] = out;
+        }
+        launch_scatter_batch(b, 1, s);
+        return;
+    }
+    for (size_t i = 0; i < nnb; ++i) {
+        const Coupling &c = op->to_c[i];
+        launch_scatter(c.len, from[i], c.to, c.c, src[i], out, 1, s);
+    }
+}
+
+// Interface-only form of the same sum: for a DD line of length L adjacent to an
+// interface end of the sweep, R_ci A_i^{-1} R_ic restricted to that line is
+// c_ci c_ic Q diag(1 / beta_end) Q^T (Q the orthonormal DST-I of the line): the
+// neighbour's field is zero except on the line, so the forward elimination is
+// y = r on the line row and the back-substitution's interface value is
+// y / beta_end -- the arm's full solve yields exactly these values there.
+// O(L log L) per arm instead of a full arm solve.  out_zero: out is already
+// zero (the operator's own centre vector), no field-sized memset.
+static void schur_apply_steklov(fd_schur_s *op, const double *p, double *out, bool out_zero, cudaStream_t s) {
     const size_t nnb = op->nb.size();
     const int L = op->stk[0].L;
     FD_CUDA(cudaMemsetAsync(op->lines, 0, sizeof(double) * nnb * L, s));
@@ -308,36 +347,59 @@ static void schur_apply_steklov(fd_schur_s *op, const double *p, double *out, cu
     launch_dst_rows((int)nnb, L, op->lines_hat, op->lines, twiddles_for(op->device, L),
                     dense_table_for(op->device, L), s);
     const Plan *cp = op->center;
-    FD_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * cp->m * cp->n, s));
+    if (!out_zero) FD_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * cp->m * cp->n, s));
+    std::vector<const int64_t *> from(nnb);
+    std::vector<const double *> src(nnb);
     for (size_t i = 0; i < nnb; ++i) {
-        const Coupling &c = op->to_c[i];
-        launch_scatter(c.len, op->stk[i].pos_out, c.to, c.c, op->lines + i * L, out, 1, s);
+        from[i] = op->stk[i].pos_out;
+        src[i] = op->lines + i * L;
     }
+    scatter_add_parts(op, from, src, out, s);
 }
 
-// out = sum_i R_ci A_i^{-1} R_ic p   (ddm.py:108-123)
-static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
+// out = sum_i R_ci A_i^{-1} R_ic p   (ddm.py:108-123).  The neighbour inputs
+// stay zero between applies: the interface lines are gathered in (one launch),
+// solved out of place and cleared again (one launch).
+static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s, bool out_zero = false) {
     if (op->steklov) {
-        schur_apply_steklov(op, p, out, s);
+        schur_apply_steklov(op, p, out, out_zero, s);
         return;
     }
     const size_t nnb = op->nb.size();
+    const bool batch = nnb <= (size_t)kMaxScatter;
     std::vector<SolveJob> jobs;
+    ScatterBatch g, z;
+    g.count = z.count = batch ? (int)nnb : 0;
     for (size_t i = 0; i < nnb; ++i) {
         const Plan *q = op->nb[i];
         const Coupling &c = op->from_c[i];
-        launch_scatter(c.len, c.from, c.to, c.c, p, op->nbin[i], 0, s);   // R_ic p into a zero field
+        if (batch) {   // R_ic p into a zero field
+            g.len[i] = z.len[i] = c.len;
+            g.from[i] = z.from[i] = c.from;
+            g.to[i] = z.to[i] = c.to;
+            g.c[i] = z.c[i] = c.c;
+            g.src[i] = z.src[i] = p;
+            g.dst[i] = z.dst[i] = op->nbin[i];
+        } else {
+            launch_scatter(c.len, c.from, c.to, c.c, p, op->nbin[i], 0, s);
+        }
         jobs.push_back(job_of(q, op->nbin[i], op->nbf[i]));
     }
+    if (batch) launch_scatter_batch(g, 0, s);
     solve_batch(jobs, s);
-    for (size_t i = 0; i < nnb; ++i)   // back to all zeros for the next apply (no field-sized memset)
-        launch_zero_at(op->from_c[i].len, op->from_c[i].to, op->nbin[i], s);
+    if (batch)
+        launch_scatter_batch(z, 2, s);
+    else
+        for (size_t i = 0; i < nnb; ++i) launch_zero_at(op->from_c[i].len, op->from_c[i].to, op->nbin[i], s);
     const Plan *cp = op->center;
-    FD_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * cp->m * cp->n, s));
+    if (!out_zero) FD_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * cp->m * cp->n, s));
+    std::vector<const int64_t *> from(nnb);
+    std::vector<const double *> src(nnb);
     for (size_t i = 0; i < nnb; ++i) {
-        const Coupling &c = op->to_c[i];
-        launch_scatter(c.len, c.from, c.to, c.c, op->nbf[i], out, 1, s);
+        from[i] = op->to_c[i].from;
+        src[i] = op->nbf[i];
     }
+    scatter_add_parts(op, from, src, out, s);
 }
 
 // out = alpha * A_c^{-1} r + beta * other
@@ -348,9 +410,24 @@ static void center_solve(fd_schur_s *op, const double *r, double *out, double al
 }
 
 // (I - A_c^{-1} S) p   (ddm.py:133-136); out must not alias p
+// op->tmp is kept zero outside this function: only the interface lines are
+// written and cleared again.
 static void precond_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
-    schur_apply(op, p, op->tmp, s);
+    schur_apply(op, p, op->tmp, s, true);
     center_solve(op, op->tmp, out, -1.0, 1.0, p, s);
+    const size_t nnb = op->nb.size();
+    if (nnb <= (size_t)kMaxScatter) {
+        ScatterBatch z;
+        z.count = (int)nnb;
+        for (size_t i = 0; i < nnb; ++i) {
+            z.len[i] = op->to_c[i].len;
+            z.to[i] = op->to_c[i].to;
+            z.dst[i] = op->tmp;
+        }
+        launch_scatter_batch(z, 2, s);
+    } else {
+        for (size_t i = 0; i < nnb; ++i) launch_zero_at(op->to_c[i].len, op->to_c[i].to, op->tmp, s);
+    }
 }
 
 static void drop_graph(fd_schur_s *op) {
@@ -863,7 +940,15 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, doub
             op->nbin.push_back((double *)dalloc(op, sizeof(double) * q->m * q->n));
             FD_CUDA(cudaMemset(op->nbin.back(), 0, sizeof(double) * q->m * q->n));
         }
+        {   // at most two R_ci contributions per centre entry: one atomic scatter-add
+            std::unordered_map<int64_t, int> mult;
+            int mx = 0;
+            for (int i = 0; i < n_nb; ++i)
+                for (int t = 0; t < line_len[i]; ++t) mx = std::max(mx, ++mult[to_c_to[i][t]]);
+            op->fused_add = n_nb <= kMaxScatter && mx <= 2;
+        }
         op->tmp = (double *)dalloc(op, sizeof(double) * Nc);
+        FD_CUDA(cudaMemset(op->tmp, 0, sizeof(double) * Nc));
         op->tmp2 = (double *)dalloc(op, sizeof(double) * Nc);
         op->w = (double *)dalloc(op, sizeof(double) * Nc);
         op->r = (double *)dalloc(op, sizeof(double) * Nc);

@@ -215,6 +215,22 @@ void launch_mul(long long N, const double *x, const double *y, double *out, cuda
 void steklov_pivots(int L, int M, double delta_line, double delta_sweep, double kappa, double mod_lo,
                     double mod_hi, int end, double *inv);
 void launch_zero_at(int len, const int64_t *to, double *dst, cudaStream_t s);   // dst[to[t]] = 0
+// Several index maps in one launch (one grid row per map).  mode 0: dst[to] =
+// c src[from] (maps with distinct destinations); 1: dst[to] += c src[from] by
+// atomic add -- only for a zero destination that receives at most two
+// contributions per entry, where the result is independent of the order
+// (0 + a + b == 0 + b + a bitwise); 2: dst[to] = 0.
+constexpr int kMaxScatter = 8;
+struct ScatterBatch {
+    int count = 0;
+    int len[kMaxScatter];
+    const int64_t *from[kMaxScatter];
+    const int64_t *to[kMaxScatter];
+    double c[kMaxScatter];
+    const double *src[kMaxScatter];
+    double *dst[kMaxScatter];
+};
+void launch_scatter_batch(const ScatterBatch &b, int mode, cudaStream_t s);
 void launch_axpby(long long N, double a, const double *x, double b, const double *y, double *out,
                   cudaStream_t s);
 // deterministic reductions: result written to device scalar *out

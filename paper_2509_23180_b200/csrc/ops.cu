@@ -93,6 +93,32 @@ void launch_zero_at(int len, const int64_t *to, double *dst, cudaStream_t s) {
     FD_CUDA(cudaGetLastError());
 }
 
+__global__ void scatter_batch_kernel(const __grid_constant__ ScatterBatch b, int mode) {
+    const int i = blockIdx.y, len = b.len[i];
+    const int64_t *__restrict__ to = b.to[i];
+    double *dst = b.dst[i];
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < len; t += gridDim.x * blockDim.x) {
+        const int64_t d = to[t];
+        if (mode == 2) {
+            dst[d] = 0.0;
+            continue;
+        }
+        const double v = __dmul_rn(b.c[i], b.src[i][b.from[i][t]]);
+        if (mode == 0)
+            dst[d] = v;
+        else
+            atomicAdd(dst + d, v);
+    }
+}
+
+void launch_scatter_batch(const ScatterBatch &b, int mode, cudaStream_t s) {
+    int mx = 0;
+    for (int i = 0; i < b.count; ++i) mx = std::max(mx, b.len[i]);
+    if (b.count <= 0 || mx <= 0) return;
+    scatter_batch_kernel<<<dim3((mx + 255) / 256, b.count), 256, 0, s>>>(b, mode);
+    FD_CUDA(cudaGetLastError());
+}
+
 void launch_scatter(int len, const int64_t *from, const int64_t *to, double c, const double *src,
                     double *dst, int accumulate, cudaStream_t s) {
     if (len <= 0) return;
