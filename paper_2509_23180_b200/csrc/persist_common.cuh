@@ -339,11 +339,11 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
             for (auto v : h)
                 if (v) t0 = std::min(t0, v);
             if (pl.dbg & 4) {   // per-pass cycle stamps of pair 0 (rsolve)
-                for (int it = 0; it < 4; ++it) {
+                for (int it = 0; it < 8; ++it) {   // phase 1 items 0-3, then phase 3 items 0-3
                     const long long *c = reinterpret_cast<const long long *>(h.data()) + 2048 + it * 8;
                     if (!c[0]) continue;
-                    fprintf(stderr, "[fft cycles it %d] load %lld first %lld mid %lld last %lld post %lld\n", it,
-                            c[1] - c[0], c[2] - c[1], c[3] - c[2], c[4] - c[3], c[5] - c[4]);
+                    fprintf(stderr, "[fft cycles p%d it %d] load %lld first %lld mid %lld last %lld post %lld\n",
+                            it < 4 ? 1 : 3, it & 3, c[1] - c[0], c[2] - c[1], c[3] - c[2], c[4] - c[3], c[5] - c[4]);
                 }
             }
             for (int role = 0; role < 16; ++role) {

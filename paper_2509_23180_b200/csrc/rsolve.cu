@@ -637,7 +637,9 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 double *XA = regd(pr), *XB = regd(pr) + XR;
                 if (!(FD_DIAG && (pl.dbg & 32)))
                 F::run(regc(pr), base, rp > 1 ? base + n : nullptr, al, 0.5 * p.scale, m16, la, scr, t, pr, lane,
-                       XA, rp > 1 ? XB : nullptr);
+                       XA, rp > 1 ? XB : nullptr,
+                       (FD_DIAG && pl.trace && (pl.dbg & 4) && blockIdx.x == pl.trace_cta && it < 4)
+                           ? reinterpret_cast<long long *>(pl.trace) + 2048 + 32 + it * 8 : nullptr);
                 rsync<T>(pr);
                 trace(8 + pr, it, 1);
                 // epilogue out = alpha x + beta other, row by row from the padded X
