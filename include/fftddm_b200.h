@@ -73,7 +73,7 @@ int fd_plan_create_axis(fd_plan *out, int m, int n, double dx, double dy, double
  * cosine basis, DCT-II/III; transforms.py:32-33,83-98,106-134), 2 = PP (real
  * Fourier basis, even n; transforms.py:34-35,114-126,139-148).  A DD axis
  * needs ghost-node ends; NN/PP ends belong to the basis.  NN and PP run on
- * the dense periodic-table transform (n <= 1024); a periodic sweep axis
+ * the dense periodic-table transform (n <= 2048); a periodic sweep axis
  * needs fd_plan_create_sweep. */
 int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double kappa,
                       double mod_west, double mod_east, double mod_south, double mod_north,
@@ -90,7 +90,7 @@ int fd_plan_create_ex(fd_plan *out, int m, int n, double dx, double dy, double k
  *    fd_plan_singular_modes and attaches each mode's sweep-matrix
  *    pseudo-inverse with fd_plan_set_pinv before the first solve (a solve
  *    before that returns FD_ERR_SINGULAR).
- * Periodic-sweep and pin_mean plans run the dense-transform solve (n <= 1024). */
+ * Periodic-sweep and pin_mean plans run the dense-transform solve (n <= 2048). */
 int fd_plan_create_sweep(fd_plan *out, int m, int n, double dx, double dy, double kappa,
                          double mod_west, double mod_east, double mod_south, double mod_north,
                          int transform_axis, int transform_pair, int sweep_cyclic, int pin_mean,
@@ -103,7 +103,7 @@ int fd_plan_singular_modes(fd_plan plan, int *modes, int cap, int *count);
  * n for an x transform), in fd_plan_singular_modes order. */
 int fd_plan_set_pinv(fd_plan plan, int count, const double *pinv);
 /* GPU transform available for length n: 1 = FFT (n+1 = 2^p, 256..4096),
- * 0 = dense (n <= 1024), -1 = none.  DD pair; fd_transform_kind_pair for NN. */
+ * 0 = dense (n <= 2048), -1 = none.  DD pair; fd_transform_kind_pair for NN. */
 int fd_transform_kind(int n);
 int fd_transform_kind_pair(int n, int pair);
 int fd_plan_destroy(fd_plan plan);
@@ -132,7 +132,7 @@ int fd_dst_rows(int rows, int n, const double *in, double *out, int device, void
  * mod_* on the four boundary-adjacent lines (geometry.py:118-128). */
 /* apply_Q (inverse = 1) / apply_Qt (inverse = 0) of any pair along rows of
  * length n (transforms.py:106-148): DD on the FFT or dense path, NN and PP on
- * the dense periodic-table path (n <= 1024, PP even n). */
+ * the dense periodic-table path (n <= 2048, PP even n). */
 int fd_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out, int device,
                       void *stream);
 /* Device-side problem assembly: f = lap p + kappa p at the

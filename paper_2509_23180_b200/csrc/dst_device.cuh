@@ -430,8 +430,7 @@ struct Fft2 {
 // N = n + 1.  The sine is periodic in (j+1)(k+1) mod 2N, so a 2N-entry table
 // (host-built, exact argument reduction) staged in shared memory serves every
 // (j, k); each thread walks its index by k + 1 per j.  MPT modes per thread
-// (n <= 128 MPT), G rows per group share every table load.
-constexpr int kDenseMax = 1024;
+// (n <= 256 MPT), G rows per group share every table load.
 template <int MPT_, int NT_ = 128, int S_ = 1>
 struct DenseDstT {
     // NT_ mode columns x S_ threads each: the S_ threads of a mode split the
@@ -440,7 +439,7 @@ struct DenseDstT {
     static constexpr int NMODE = NT_;
     static constexpr int NT = NT_ * S_;
     static constexpr int G = NT_ <= 160 ? 4 : 8;   // small n: fewer rows per CTA, more CTAs
-    static constexpr int MINB = S_ > 1 ? 1 : 2;
+    static constexpr int MINB = (S_ > 1 || MPT_ >= 8) ? 1 : 2;   // n > 1024: one CTA per SM (shared memory)
     static constexpr int MPT = MPT_;
     static constexpr int NMAX = NT_ * MPT_;
     // rows + the periodic basis table: 2(n+1) entries (DD sine), 4n (NN cosine) or 2n (PP)

@@ -110,6 +110,7 @@ inline bool rs_supported(int n) {
 }
 
 enum Transform { kDense = 0, kFFT = 1 };
+constexpr int kDenseMax = 2048;   // longest dense periodic-table transform (dst_device.cuh)
 
 // Device allocations of plans, operators and the Krylov basis come from the
 // device's stream-ordered pool with an unbounded release threshold, so the

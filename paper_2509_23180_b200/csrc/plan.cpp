@@ -394,7 +394,7 @@ const double2 *twiddles_for(int device, int n) {
 }
 
 const double *dense_table_for(int device, int n, int pair, bool force) {
-    if (transform_kind(n, pair) != kDense && !(force && n <= 1024)) return nullptr;
+    if (transform_kind(n, pair) != kDense && !(force && n <= kDenseMax)) return nullptr;
     std::lock_guard<std::mutex> g(g_tab_mu);
     auto key = std::make_pair(device, n + (pair << 24));
     auto it = g_dense.find(key);
@@ -443,11 +443,11 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
     int tk = transform_kind(n, pair);
     // the correction and pseudo-inverse terms live in the three-kernel dense solve
     const bool forced = tk == kFFT && (cyclic || pin);
-    if (forced) tk = n <= 1024 ? kDense : -1;   // dense transform limit (dst_device.cuh kDenseMax)
+    if (forced) tk = n <= kDenseMax ? kDense : -1;   // dense transform limit (dst_device.cuh kDenseMax)
     if (tk < 0) {
         std::ostringstream os;
         os << "plan: no GPU transform for n = " << n
-           << " (supported: n+1 a power of two in [256, 4096], or n <= 1024)";
+           << " (supported: n+1 a power of two in [256, 4096], or n <= 2048)";
         FD_FAIL(FD_ERR_UNSUPPORTED, os.str());
     }
     const int R = forced ? 8 : rows_per_block(n, pair);   // forced: the dense path's rows per group

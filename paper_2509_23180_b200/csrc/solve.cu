@@ -622,7 +622,8 @@ void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
         else if (n <= 160) run_solve<DenseDstT<1, 160, 4>>(jobs, s);
         else if (n <= 256) run_solve<DenseDstT<1, 256>>(jobs, s);
         else if (n <= 512) run_solve<DenseDstT<2, 256>>(jobs, s);
-        else run_solve<DenseDstT<4, 256>>(jobs, s);
+        else if (n <= 1024) run_solve<DenseDstT<4, 256>>(jobs, s);
+        else run_solve<DenseDstT<8, 256>>(jobs, s);
         return;
     }
     if (jobs[0].ws && launch_persist(jobs, s, *jobs[0].ws)) return;
@@ -659,7 +660,8 @@ void launch_transform_rows(int rows, int n, int pair, int inverse, const double 
     else if (n <= 160) run_dense_rows<DenseDstT<1, 160>>(rows, n, pair, inverse, in, out, dense, s);
     else if (n <= 256) run_dense_rows<DenseDstT<1, 256>>(rows, n, pair, inverse, in, out, dense, s);
     else if (n <= 512) run_dense_rows<DenseDstT<2, 256>>(rows, n, pair, inverse, in, out, dense, s);
-    else run_dense_rows<DenseDstT<4, 256>>(rows, n, pair, inverse, in, out, dense, s);
+    else if (n <= 1024) run_dense_rows<DenseDstT<4, 256>>(rows, n, pair, inverse, in, out, dense, s);
+    else run_dense_rows<DenseDstT<8, 256>>(rows, n, pair, inverse, in, out, dense, s);
 }
 
 void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,
@@ -670,7 +672,8 @@ void launch_dst_rows(int rows, int n, const double *in, double *out, const doubl
         else if (n <= 160) run_dst<DenseDstT<1, 160>>(rows, n, in, out, tw, dense, s);
         else if (n <= 256) run_dst<DenseDstT<1, 256>>(rows, n, in, out, tw, dense, s);
         else if (n <= 512) run_dst<DenseDstT<2, 256>>(rows, n, in, out, tw, dense, s);
-        else run_dst<DenseDstT<4, 256>>(rows, n, in, out, tw, dense, s);
+        else if (n <= 1024) run_dst<DenseDstT<4, 256>>(rows, n, in, out, tw, dense, s);
+        else run_dst<DenseDstT<8, 256>>(rows, n, in, out, tw, dense, s);
         return;
     }
     switch (lg_of(n)) {

@@ -4,7 +4,7 @@
 for the Dirichlet-Dirichlet pair run the sm_100a DST-I kernel (Q = Q^T =
 sqrt(2/(n+1)) DST-I, transforms.py:112-113,135-136) on torch CUDA tensors;
 numpy input is copied to the device and the result back.  NN (DCT-II/III)
-and PP (real Fourier) run on the dense periodic-table transform (n <= 1024,
+and PP (real Fourier) run on the dense periodic-table transform (n <= 2048,
 PP even n); other lengths raise UnsupportedError.
 """
 

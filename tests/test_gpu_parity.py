@@ -254,7 +254,7 @@ class TestTransposedAxis:
 
     @pytest.mark.parametrize("m,n,kappa,half", [(255, 127, -3.0, ("south",)),
                                                 (141, 63, 0.0, ("south", "north")),
-                                                (255, 1500, 0.0, ()), (141, 1100, -10.0, ()),
+                                                (255, 2100, 0.0, ()), (141, 3000, -10.0, ()),
                                                 (1023, 2500, 2.0, ())])
     def test_against_oracle(self, m, n, kappa, half, rng):
         h = 1.0 / max(m, n)
@@ -285,9 +285,9 @@ class TestTransposedAxis:
         assert (torch.linalg.norm(p1 - outs[1]) / torch.linalg.norm(p1)).item() < 1e-12
 
     def test_cross_with_transposed_arms(self):
-        """Cross whose south/north arms (127 x 1100) take the x transform, against
+        """Cross whose south/north arms (127 x 2100) take the x transform, against
         the oracle's ddm_solve (which transforms them along y, like the reference)."""
-        comp = configs.cross_composite(127, arm=1100, kappa=-10.0)
+        comp = configs.cross_composite(127, arm=2100, kappa=-10.0)
         f, exact = configs.manufactured_rhs(comp, "sin")
         fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
         ofields, orep = O.ddm_solve(comp, f, m=50, tol=1e-10)
@@ -346,7 +346,7 @@ class TestNeumannTransform:
         p = rectsolver.solve_rect(pl, g[f"nn_f_{c}"]).values
         assert rel(p, g[f"nn_p_{c}"]) < 1e-12
 
-    @pytest.mark.parametrize("n", [2, 8, 64, 142, 1000])
+    @pytest.mark.parametrize("n", [2, 8, 64, 142, 1000, 1500, 2048])
     def test_periodic_against_oracle_and_residual(self, n, rng):
         """PP transform axis (even n), half-cell sweep end; A p = f with the
         periodic wrap stencil (rectsolver.py:274-276)."""
@@ -355,17 +355,19 @@ class TestNeumannTransform:
         p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f).values
         assert rel(p, O.solve(O.plan(sub), f)) < 1e-12
         r = rectsolver.apply_rect_operator(sub, p) - f
-        assert np.linalg.norm(r) / np.linalg.norm(f) < 1e-11
+        # ||A|| grows as 1/h_y^2 = n^2: the residual of a solve exact to rounding with it
+        assert np.linalg.norm(r) / np.linalg.norm(f) < (1e-11 if n <= 1024 else 1e-10)
         np.testing.assert_array_equal(rectsolver.apply_rect_operator(sub, f), O.apply_operator(sub, f))
 
-    @pytest.mark.parametrize("n", [1, 2, 7, 64, 141, 1000])
+    @pytest.mark.parametrize("n", [1, 2, 7, 64, 141, 1000, 1337, 2048])
     def test_against_oracle_and_residual(self, n, rng):
         sub = make((33, n, 1.0 / 33, 1.0 / max(n, 2), -1.0, "DDNN", ("west",)))
         f = rng.uniform(-1, 1, sub.size)
         p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f).values
         assert rel(p, O.solve(O.plan(sub), f)) < 1e-12
         r = rectsolver.apply_rect_operator(sub, p) - f
-        assert np.linalg.norm(r) / np.linalg.norm(f) < 1e-11
+        # ||A|| grows as 1/h_y^2 = n^2: the residual of a solve exact to rounding with it
+        assert np.linalg.norm(r) / np.linalg.norm(f) < (1e-11 if n <= 1024 else 1e-10)
 
     @pytest.mark.parametrize("k_n,kappa", [(2, 0.0), (4, -3.0), (8, 0.0), (16, -3.0), (16, 0.0)])
     def test_reference_cross(self, k_n, kappa):
@@ -446,8 +448,9 @@ class TestTransformPairs:
     """apply_Q / apply_Qt for every pair (transforms.py:106-148) against the
     oracle's restatement of the reference's FFT formulations."""
 
-    @pytest.mark.parametrize("bc,n", [("DD", 7), ("DD", 1023), ("NN", 1), ("NN", 16), ("NN", 141), ("NN", 1000),
-                                      ("PP", 2), ("PP", 16), ("PP", 142), ("PP", 1024)])
+    @pytest.mark.parametrize("bc,n", [("DD", 7), ("DD", 1023), ("DD", 1500), ("DD", 2048), ("NN", 1), ("NN", 16),
+                                      ("NN", 141), ("NN", 1000), ("NN", 1700), ("NN", 2048),
+                                      ("PP", 2), ("PP", 16), ("PP", 142), ("PP", 1024), ("PP", 1800), ("PP", 2048)])
     def test_q_and_qt(self, bc, n, rng):
         pl = transforms.make_plan(bc, n, 1.0, 1.0)
         x = rng.standard_normal((5, n))
@@ -515,6 +518,22 @@ class TestPeriodicSweep:
         assert np.abs(rectsolver.apply_rect_operator(sub, p) - f).max() < 1e-10
         assert abs(p.mean()) < 1e-12
 
+    @pytest.mark.parametrize("m,n", [(40, 1500), (24, 2048)])
+    def test_pin_mean_long_transform(self, m, n, rng):
+        """pin_mean on a transform longer than 1024 (dense path up to 2048):
+        zero-mean data is solved to rounding with a zero-mean solution, and
+        the result matches the oracle's minimum-norm solve."""
+        sub = make((m, n, 1.0 / m, 1.0 / n, 0.0, "NNNN", ()))
+        pl = rectsolver.plan_rect(sub, pin_mean=True)
+        f = rng.uniform(-1, 1, sub.size)
+        f -= f.mean()
+        p = rectsolver.solve_rect(pl, f).values
+        r = rectsolver.apply_rect_operator(sub, p) - f
+        assert np.linalg.norm(r) / np.linalg.norm(f) < 1e-10
+        assert abs(p.mean()) < 1e-10 * np.abs(p).max()
+        want = O.solve(O.plan(sub, pin_mean=True), f)
+        assert rel(p, want) < 1e-10
+
     def test_pair_sweep(self):
         """Every transform/sweep pair, m, n <= 5 (test_rectsolver.py:15-27,
         126-135): GPU against the oracle and the periodic-wrap residual."""
@@ -530,7 +549,7 @@ class TestPeriodicSweep:
             r = rectsolver.apply_rect_operator(sub, p) - f
             assert np.abs(r).max() <= 1e-10 * max(np.abs(f).max(), 1.0), case
 
-    @pytest.mark.parametrize("m,n", [(2, 1), (2, 1023), (512, 100), (1000, 1024)])
+    @pytest.mark.parametrize("m,n", [(2, 1), (2, 1023), (512, 100), (1000, 1024), (300, 1500), (64, 2047)])
     def test_against_oracle_and_residual(self, m, n, rng):
         sub = make((m, n, 1.0 / m, 1.0 / n, -0.5, "PPDD", ()))
         f = rng.uniform(-1, 1, sub.size)

@@ -102,8 +102,8 @@ def test_errors_map_to_reference_classes():
 def test_transform_kind(lib):
     """GPU transform availability per length (drives the axis choice)."""
     assert [lib.fd_transform_kind(n) for n in (255, 511, 1023, 2047, 4095)] == [1] * 5
-    assert [lib.fd_transform_kind(n) for n in (1, 141, 1000, 1024)] == [0] * 4
-    assert [lib.fd_transform_kind(n) for n in (1025, 1500, 8191, 16383)] == [-1] * 4
+    assert [lib.fd_transform_kind(n) for n in (1, 141, 1000, 1024, 1025, 1500, 2048)] == [0] * 7
+    assert [lib.fd_transform_kind(n) for n in (2049, 3000, 8191, 16383)] == [-1] * 4
 
 
 @pytest.mark.parametrize("m,n,bc,half,axis", [
@@ -112,8 +112,9 @@ def test_transform_kind(lib):
     (4095, 16383, "DDDD", (), "x"),         # c4 south/north arm: no 16384-point transform -> x
     (255, 127, "DDDD", ("south",), "x"),    # y half-cell -> x, as the reference
     (9, 31, "IDDD", ("east",), "y"),        # sweep-axis modifiers only
-    (40, 1500, "DDDD", (), "x"),            # n without a GPU length, m with one -> x
-    (1500, 1500, "DDDD", (), "y"),          # neither: the reference's y (plan creation reports it)
+    (40, 3000, "DDDD", (), "x"),            # n without a GPU length, m with one -> x
+    (40, 1500, "DDDD", (), "y"),            # n <= 2048: dense transform along y, as the reference
+    (3000, 3000, "DDDD", (), "y"),          # neither: the reference's y (plan creation reports it)
 ])
 def test_gpu_axis_choice(lib, m, n, bc, half, axis):
     from paper_2509_23180_b200.rectsolver import _gpu_axis
