@@ -284,6 +284,25 @@ class TestTransposedAxis:
         p1 = rectsolver.solve_rect(plans[1], f[1]).values
         assert (torch.linalg.norm(p1 - outs[1]) / torch.linalg.norm(p1)).item() < 1e-12
 
+    @pytest.mark.parametrize("N,arm", [(1, 3), (2, 5), (3, 3)])
+    def test_tiny_centre_scatter_paths(self, N, arm):
+        """Centre 1 x 1: its one entry takes all four arm parts (the ordered
+        per-arm scatter-add); 2 x 2 and 3 x 3: at most two parts per entry
+        (the single atomic scatter-add).  Both against the oracle."""
+        comp = configs.cross_composite(N, arm=arm, kappa=-1.0)
+        f, _ = configs.manufactured_rhs(comp, "sin_exp")
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+        ofields, orep = O.ddm_solve(comp, f, m=50, tol=1e-10)
+        assert abs(rep.iterations - orep.iterations) <= 1
+        num = sum(float(np.sum((fields[s].values - ofields[s]) ** 2)) for s in ofields)
+        den = sum(float(np.sum(ofields[s] ** 2)) for s in ofields)
+        assert (num / den) ** 0.5 < 1e-10
+        op, oo = ddm.build_schur_operator(comp), O.Schur(comp)
+        p = np.random.default_rng(N).uniform(-1, 1, op.size)
+        for got, want in [(op.schur(p), oo.schur(p)), (op.preconditioned(p), oo.preconditioned(p))]:
+            got = got.cpu().numpy() if hasattr(got, "cpu") else np.asarray(got)
+            assert rel(got, want) < 1e-12
+
     def test_cross_with_transposed_arms(self):
         """Cross whose south/north arms (127 x 2100) take the x transform, against
         the oracle's ddm_solve (which transforms them along y, like the reference)."""
