@@ -304,7 +304,7 @@ static void scatter_add_parts(fd_schur_s *op, const std::vector<const int64_t *>
                               const std::vector<const double *> &src, double *out, cudaStream_t s) {
     const size_t nnb = op->nb.size();
     if (op->fused_add) {
-        ScatterBatch b;
+        ScatterBatch b{};
         b.count = (int)nnb;
         for (size_t i = 0; i < nnb; ++i) {
             const Coupling &c = op->to_c[i];
@@ -368,7 +368,7 @@ static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream
     const size_t nnb = op->nb.size();
     const bool batch = nnb <= (size_t)kMaxScatter;
     std::vector<SolveJob> jobs;
-    ScatterBatch g, z;
+    ScatterBatch g{}, z{};
     g.count = z.count = batch ? (int)nnb : 0;
     for (size_t i = 0; i < nnb; ++i) {
         const Plan *q = op->nb[i];
@@ -417,7 +417,7 @@ static void precond_apply(fd_schur_s *op, const double *p, double *out, cudaStre
     center_solve(op, op->tmp, out, -1.0, 1.0, p, s);
     const size_t nnb = op->nb.size();
     if (nnb <= (size_t)kMaxScatter) {
-        ScatterBatch z;
+        ScatterBatch z{};
         z.count = (int)nnb;
         for (size_t i = 0; i < nnb; ++i) {
             z.len[i] = op->to_c[i].len;
