@@ -429,6 +429,13 @@ __global__ void __launch_bounds__(256) arnoldi_update_kernel(long long N, int k,
          i += (long long)gridDim.x * blockDim.x) {
         double x = w[i];
         int j = 0;
+        for (; j + 7 <= k; j += 8) {   // 8 basis loads in flight per thread
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = V[(long long)(j + q) * N + i];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) x = __dsub_rn(x, __dmul_rn(sh[j + q], v[q]));
+        }
         for (; j + 3 <= k; j += 4) {
             const double v0 = V[(long long)j * N + i], v1 = V[(long long)(j + 1) * N + i];
             const double v2 = V[(long long)(j + 2) * N + i], v3 = V[(long long)(j + 3) * N + i];
