@@ -297,7 +297,8 @@ __device__ __forceinline__ void arn_finish(ArnWork a, int nd, const double *bacc
                                            bool want_h) {
     __shared__ bool last;
     __syncthreads();
-    for (int d = threadIdx.x; d < nd; d += blockDim.x) a.partials[size_t(blockIdx.x) * nd + d] = bacc[d];
+    // [d][block]: the last block's reduction reads each d coalesced over blocks
+    for (int d = threadIdx.x; d < nd; d += blockDim.x) a.partials[size_t(d) * gridDim.x + blockIdx.x] = bacc[d];
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -309,10 +310,10 @@ __device__ __forceinline__ void arn_finish(ArnWork a, int nd, const double *bacc
     __threadfence();
     __shared__ double tot[2 * kMaxArnoldi + 2];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const volatile double *pp = a.partials;
+    const double *pp = a.partials;   // read past L1 (__ldcg): other blocks' writes
     for (int d = wid; d < nd; d += int(blockDim.x >> 5)) {   // fixed order: lanes stride blocks, then a tree
         double v = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) v += pp[size_t(b) * nd + d];
+        for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(pp + size_t(d) * gridDim.x + b);
         v = warp_sum(v);
         if (lane == 0) tot[d] = v;
     }
@@ -329,9 +330,27 @@ __device__ __forceinline__ void arn_finish(ArnWork a, int nd, const double *bacc
         __syncwarp();
         // lane owns rows i = lane, lane + 32 (k + 1 <= 64)
         double h0 = lane <= k ? tot[lane] : 0.0, h1 = lane + 32 <= k ? tot[lane + 32] : 0.0;
-        for (int j = 0; j < k; ++j) {
+        const int i0 = lane, i1 = lane + 32;
+        int j = 0;
+        // the Gram entries of 8 steps loaded ahead of their dependent chain (an
+        // L2 round trip per step otherwise sits on this serial tail)
+        for (; j + 8 <= k; j += 8) {
+            double g0[8], g1[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                g0[q] = (i0 > j + q && i0 <= k) ? G[size_t(i0) * ldg + j + q] : 0.0;
+                g1[q] = (i1 > j + q && i1 <= k) ? G[size_t(i1) * ldg + j + q] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int jj = j + q;
+                const double hj = __shfl_sync(0xffffffffu, jj < 32 ? h0 : h1, jj & 31);
+                if (i0 > jj && i0 <= k) h0 = __dsub_rn(h0, __dmul_rn(g0[q], hj));
+                if (i1 > jj && i1 <= k) h1 = __dsub_rn(h1, __dmul_rn(g1[q], hj));
+            }
+        }
+        for (; j < k; ++j) {
             const double hj = __shfl_sync(0xffffffffu, j < 32 ? h0 : h1, j & 31);
-            const int i0 = lane, i1 = lane + 32;
             if (i0 > j && i0 <= k) h0 = __dsub_rn(h0, __dmul_rn(G[size_t(i0) * ldg + j], hj));
             if (i1 > j && i1 <= k) h1 = __dsub_rn(h1, __dmul_rn(G[size_t(i1) * ldg + j], hj));
         }
