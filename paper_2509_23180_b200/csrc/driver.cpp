@@ -14,6 +14,7 @@
 #include <unordered_map>
 #include <mutex>
 #include <set>
+#include <thread>
 #include <sstream>
 #include <tuple>
 
@@ -86,26 +87,30 @@ struct Scratch {
 // allocations cost milliseconds, so released blocks are kept for reuse (one
 // size class; the few blocks a process needs are never returned to the OS).
 static std::mutex g_pin_mu;
-static std::vector<void *> *g_pin_free = new std::vector<void *>();   // never destroyed
+static std::multimap<size_t, void *> *g_pin_free = new std::multimap<size_t, void *>();   // never destroyed
+static std::map<void *, size_t> *g_pin_size = new std::map<void *, size_t>();
 constexpr size_t kPinBytes = 8192;
 static void *pinned_get(size_t bytes) {
-    if (bytes > kPinBytes) throw Error{FD_ERR_VALIDATION, "pinned mirror too large"};
+    bytes = std::max(bytes, kPinBytes);
     {
         std::lock_guard<std::mutex> g(g_pin_mu);
-        if (!g_pin_free->empty()) {
-            void *p = g_pin_free->back();
-            g_pin_free->pop_back();
+        auto it = g_pin_free->lower_bound(bytes);
+        if (it != g_pin_free->end()) {
+            void *p = it->second;
+            g_pin_free->erase(it);
             return p;
         }
     }
     void *p = nullptr;
-    FD_CUDA(cudaMallocHost(&p, kPinBytes));
+    FD_CUDA(cudaMallocHost(&p, bytes));
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    (*g_pin_size)[p] = bytes;
     return p;
 }
 static void pinned_put(void *p) {
     if (!p) return;
     std::lock_guard<std::mutex> g(g_pin_mu);
-    g_pin_free->push_back(p);
+    g_pin_free->emplace((*g_pin_size)[p], p);
 }
 
 static Scratch make_scratch(int cap) {
@@ -124,14 +129,24 @@ static void free_scratch(Scratch &s) {   // callers synchronise the device first
     dfree(s.dval);
     pinned_put(s.hval);
 }
+// One scratch per (device, stream, host thread): calls on different streams
+// or from different host threads never share a counter, partials or the
+// pinned mirror.  Capacity grows with the request (restart length + 3).
 static std::mutex g_scr_mu;
-static std::map<int, Scratch> g_scratch;
-static Scratch &device_scratch() {
+static std::map<std::tuple<int, cudaStream_t, std::thread::id>, Scratch> g_scratch;
+static Scratch &device_scratch(cudaStream_t s, int need = 64) {
     int dev = 0;
     FD_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> g(g_scr_mu);
-    auto it = g_scratch.find(dev);
-    if (it == g_scratch.end()) it = g_scratch.emplace(dev, make_scratch(1024)).first;
+    auto key = std::make_tuple(dev, s, std::this_thread::get_id());
+    auto it = g_scratch.find(key);
+    if (it != g_scratch.end() && it->second.cap < need) {
+        FD_CUDA(cudaStreamSynchronize(s));
+        free_scratch(it->second);
+        g_scratch.erase(it);
+        it = g_scratch.end();
+    }
+    if (it == g_scratch.end()) it = g_scratch.emplace(key, make_scratch(std::max(need, 64))).first;
     return it->second;
 }
 
@@ -189,6 +204,7 @@ struct fd_schur_s {
     double *V = nullptr;
     int vcap = 0;
     double *w = nullptr, *r = nullptr, *ydev = nullptr;
+    int ycap = 0;
     fd::Scratch sc{};
     // low-synchronisation Arnoldi: Gram rows, partials, results (device) + pinned mirror
     fd::ArnWork arn{};
@@ -535,6 +551,14 @@ static void arnoldi_collect(fd_schur_s *op, int k, double *h, double *w_norm) {
 
 static void ensure_basis(fd_schur_s *op, int m) {
     ensure_arnoldi(op);
+    if (op->ycap < m + 1) {   // back-solve coefficients y (k_used <= m)
+        if (op->ydev) {
+            FD_CUDA(cudaDeviceSynchronize());
+            dfree(op->ydev);
+        }
+        op->ydev = (double *)dmalloc(sizeof(double) * (m + 1));
+        op->ycap = m + 1;
+    }
     if (op->vcap >= m + 1) return;
     if (op->V) {
         FD_CUDA(cudaDeviceSynchronize());
@@ -561,8 +585,7 @@ static int gmres_precond(fd_schur_s *op, const double *rhs, double *x, int x_is_
     const long long N = (long long)op->center->m * op->center->n;
     const int m = (int)std::min<long long>(mcfg, N);
     ensure_basis(op, m);
-    static const bool force_mgs = getenv("FD_MGS") != nullptr;   // A/B switch: classic k+1-pass MGS
-    const bool lowsync = m + 1 <= kMaxArnoldi && !force_mgs;
+    const bool lowsync = m + 1 <= kMaxArnoldi;   // else classic (k+1)-pass MGS
     Scratch &sc = op->sc;
     double *r = op->r, *w = op->w;
     if (x_is_zero) {
@@ -952,7 +975,6 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, doub
         op->tmp2 = (double *)dalloc(op, sizeof(double) * Nc);
         op->w = (double *)dalloc(op, sizeof(double) * Nc);
         op->r = (double *)dalloc(op, sizeof(double) * Nc);
-        op->ydev = (double *)dalloc(op, sizeof(double) * 4096);
         op->sc = make_scratch(128);
     } catch (...) {
         cudaDeviceSynchronize();
@@ -1018,6 +1040,7 @@ int fd_schur_destroy(fd_schur op) {
         if (op->gstream) cudaStreamDestroy(op->gstream);
         for (void *a : op->allocs) dfree(a);
         if (op->V) dfree(op->V);
+        if (op->ydev) dfree(op->ydev);
         if (op->sc.cap) free_scratch(op->sc);
         pinned_put(op->arn_host);
         for (auto e : op->arn_ev)
@@ -1084,8 +1107,10 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     std::vector<UJob> ujobs;
     for (size_t i = 0; i < nnb; ++i) ujobs.push_back(UJob{op->nb[i], f_nb[i], p_nb[i]});
     solve_user(ujobs, s);
-    // f' = f_c - sum_i R_ci q_i  (ddm.py:252-254); tmp2 holds f'
-    double *fp = op->tmp2;
+    // f' = f_c - sum_i R_ci q_i  (ddm.py:252-254) in a buffer of its own:
+    // unprecond_apply (the true residual below) uses tmp2 as scratch
+    double *fp = nullptr;
+    FD_CUDA(cudaMallocAsync(&fp, sizeof(double) * Nc, s));
     FD_CUDA(cudaMemcpyAsync(fp, f_center, sizeof(double) * Nc, cudaMemcpyDeviceToDevice, s));
     for (size_t i = 0; i < nnb; ++i) {
         const Coupling &c = op->to_c[i];
@@ -1107,6 +1132,7 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     launch_axpby(Nc, 1.0, rhs, -1.0, fp, rhs, s);
     rep->true_residual = norm2(Nc, rhs, op->sc, s);
     FD_CUDA(cudaFreeAsync(rhs, s));
+    FD_CUDA(cudaFreeAsync(fp, s));
     // back-substitution p_i = q_i - A_i^{-1} R_ic p_c (ddm.py:259-269)
     std::vector<SolveJob> jobs;
     for (size_t i = 0; i < nnb; ++i) {
@@ -1136,14 +1162,15 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
 int fd_arnoldi_step(int N, int k, const double *V, double *w, double *h, double *w_norm,
                     void *stream) {
     FD_API_BEGIN
-    arnoldi_step(N, k, V, w, h, w_norm, device_scratch(), S(stream));
+    if (k < 0) FD_FAIL(FD_ERR_VALIDATION, "arnoldi: negative step");
+    arnoldi_step(N, k, V, w, h, w_norm, device_scratch(S(stream), k + 3), S(stream));
     FD_API_END
 }
 
 int fd_basis_update(int N, int k, const double *V, const double *y, double *x, void *stream) {
     FD_API_BEGIN
-    Scratch &sc = device_scratch();
-    if (k > sc.cap) FD_FAIL(FD_ERR_VALIDATION, "basis update: k too large");
+    if (k < 0) FD_FAIL(FD_ERR_VALIDATION, "basis update: negative k");
+    Scratch &sc = device_scratch(S(stream), k);
     memcpy(sc.hval, y, sizeof(double) * k);
     FD_CUDA(cudaMemcpyAsync(sc.dval, sc.hval, sizeof(double) * k, cudaMemcpyHostToDevice, S(stream)));
     launch_basis_update(N, k, V, sc.dval, x, S(stream));
@@ -1159,13 +1186,13 @@ int fd_axpby(int N, double a, const double *x, double b, const double *y, double
 
 int fd_norm(int N, const double *x, double *result, void *stream) {
     FD_API_BEGIN
-    *result = norm2(N, x, device_scratch(), S(stream));
+    *result = norm2(N, x, device_scratch(S(stream)), S(stream));
     FD_API_END
 }
 
 int fd_dot(int N, const double *x, const double *y, double *result, void *stream) {
     FD_API_BEGIN
-    Scratch &sc = device_scratch();
+    Scratch &sc = device_scratch(S(stream));
     launch_dot(N, x, y, sc.dval, sc.red, S(stream));
     FD_CUDA(cudaMemcpyAsync(sc.hval, sc.dval, sizeof(double), cudaMemcpyDeviceToHost, S(stream)));
     FD_CUDA(cudaStreamSynchronize(S(stream)));

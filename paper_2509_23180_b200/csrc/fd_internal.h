@@ -42,6 +42,7 @@ struct Error {
 struct PlanDev {
     int m, n, R, nb;
     double off;          // delta_x: constant off-diagonal of the sweep system
+    double nio;          // -1 / off
     double mod_w, mod_e; // sweep-axis end modifiers on rows 0 and m-1
     double scale;        // sqrt(2/(n+1)): orthonormal DST-I factor
     const int *ex_off;   // [n]
@@ -246,7 +247,7 @@ void launch_dot(long long N, const double *x, const double *y, double *out, RedW
 void launch_mgs(long long N, double *w, const double *vprev, const double *h_prev,
                 const double *vi, double *h_out, RedWork wk, cudaStream_t s);
 // low-synchronisation MGS Arnoldi (see ops.cu)
-constexpr int kMaxArnoldi = 64;            // basis vectors V_0..V_k per step, k + 1 <= 64
+constexpr int kMaxArnoldi = 128;           // basis vectors V_0..V_k per step, k + 1 <= 128 (m <= 127)
 struct ArnWork {
     double *partials;        // [grid][2 * kMaxArnoldi + 2]
     unsigned int *counter;

@@ -291,7 +291,6 @@ namespace fd {
 constexpr int kArnThreads = 512;
 constexpr int kArnWarps = kArnThreads / 32;
 constexpr int kArnChunk = 2048;
-constexpr int kArnJPW = (kMaxArnoldi + kArnWarps - 1) / kArnWarps;   // basis vectors per warp
 
 __device__ __forceinline__ void arn_finish(ArnWork a, int nd, const double *bacc, int k, int ldg,
                                            bool want_h) {
@@ -325,41 +324,61 @@ __device__ __forceinline__ void arn_finish(ArnWork a, int nd, const double *bacc
     }
     // tot = [s_0..s_k | c_0..c_{k-1} | w.w]; Gram row k <- c; h by forward substitution
     if (wid == 0) {
+        constexpr int RL = kMaxArnoldi / 32;   // rows per lane: i = lane + 32 r
         double *G = a.G;
         for (int j = lane; j < k; j += 32) G[size_t(k) * ldg + j] = tot[k + 1 + j];
         __syncwarp();
-        // lane owns rows i = lane, lane + 32 (k + 1 <= 64)
-        double h0 = lane <= k ? tot[lane] : 0.0, h1 = lane + 32 <= k ? tot[lane + 32] : 0.0;
-        const int i0 = lane, i1 = lane + 32;
+        double h[RL];
+#pragma unroll
+        for (int r = 0; r < RL; ++r) h[r] = lane + 32 * r <= k ? tot[lane + 32 * r] : 0.0;
+        const int rows = k / 32 + 1;   // rows r in use (warp-uniform)
+        auto hj_of = [&](int jj) {
+            double v = h[0];
+#pragma unroll
+            for (int r = 1; r < RL; ++r)
+                if ((jj >> 5) == r) v = h[r];
+            return __shfl_sync(0xffffffffu, v, jj & 31);
+        };
         int j = 0;
         // the Gram entries of 8 steps loaded ahead of their dependent chain (an
         // L2 round trip per step otherwise sits on this serial tail)
         for (; j + 8 <= k; j += 8) {
-            double g0[8], g1[8];
+            double g[RL][8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                g0[q] = (i0 > j + q && i0 <= k) ? G[size_t(i0) * ldg + j + q] : 0.0;
-                g1[q] = (i1 > j + q && i1 <= k) ? G[size_t(i1) * ldg + j + q] : 0.0;
+            for (int r = 0; r < RL; ++r) {
+                const int i = lane + 32 * r;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) g[r][q] = (r < rows && i > j + q && i <= k) ? G[size_t(i) * ldg + j + q] : 0.0;
             }
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 const int jj = j + q;
-                const double hj = __shfl_sync(0xffffffffu, jj < 32 ? h0 : h1, jj & 31);
-                if (i0 > jj && i0 <= k) h0 = __dsub_rn(h0, __dmul_rn(g0[q], hj));
-                if (i1 > jj && i1 <= k) h1 = __dsub_rn(h1, __dmul_rn(g1[q], hj));
+                const double hj = hj_of(jj);
+#pragma unroll
+                for (int r = 0; r < RL; ++r) {
+                    const int i = lane + 32 * r;
+                    if (i > jj && i <= k) h[r] = __dsub_rn(h[r], __dmul_rn(g[r][q], hj));
+                }
             }
         }
         for (; j < k; ++j) {
-            const double hj = __shfl_sync(0xffffffffu, j < 32 ? h0 : h1, j & 31);
-            if (i0 > j && i0 <= k) h0 = __dsub_rn(h0, __dmul_rn(G[size_t(i0) * ldg + j], hj));
-            if (i1 > j && i1 <= k) h1 = __dsub_rn(h1, __dmul_rn(G[size_t(i1) * ldg + j], hj));
+            const double hj = hj_of(j);
+#pragma unroll
+            for (int r = 0; r < RL; ++r) {
+                const int i = lane + 32 * r;
+                if (i > j && i <= k) h[r] = __dsub_rn(h[r], __dmul_rn(G[size_t(i) * ldg + j], hj));
+            }
         }
-        if (lane <= k) a.out[lane] = h0;
-        if (lane + 32 <= k) a.out[lane + 32] = h1;
+#pragma unroll
+        for (int r = 0; r < RL; ++r)
+            if (lane + 32 * r <= k) a.out[lane + 32 * r] = h[r];
         if (lane == 0) a.out[k + 1] = tot[2 * k + 1];   // ||w||^2 before orthogonalisation
     }
 }
 
+// JPW basis vectors per warp: 4 covers k + 1 <= 64 (the m = 50 configs), 8
+// covers k + 1 <= 128 (the reference's default m = 80)
+template <int JPW>
 __global__ void __launch_bounds__(kArnThreads) arnoldi_dots_kernel(long long N, int k, const double *__restrict__ V,
                                                                     const double *__restrict__ w, ArnWork a, int ldg,
                                                                     int chunk) {
@@ -369,9 +388,9 @@ __global__ void __launch_bounds__(kArnThreads) arnoldi_dots_kernel(long long N, 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int nd = 2 * k + 2;
     const double *vk = V + (long long)k * N;
-    double as[kArnJPW], ac[kArnJPW];
+    double as[JPW], ac[JPW];
 #pragma unroll
-    for (int q = 0; q < kArnJPW; ++q) as[q] = ac[q] = 0.0;
+    for (int q = 0; q < JPW; ++q) as[q] = ac[q] = 0.0;
     double ww = 0.0;
     for (long long c0 = (long long)blockIdx.x * chunk; c0 < N; c0 += (long long)gridDim.x * chunk) {
         const int len = (int)min((long long)chunk, N - c0);
@@ -384,7 +403,7 @@ __global__ void __launch_bounds__(kArnThreads) arnoldi_dots_kernel(long long N, 
         }
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kArnJPW; ++q) {
+        for (int q = 0; q < JPW; ++q) {
             const int j = wid + q * kArnWarps;
             if (j > k) break;
             const double *vj = V + (long long)j * N + c0;
@@ -415,7 +434,7 @@ __global__ void __launch_bounds__(kArnThreads) arnoldi_dots_kernel(long long N, 
         }
     }
 #pragma unroll
-    for (int q = 0; q < kArnJPW; ++q) {
+    for (int q = 0; q < JPW; ++q) {
         const int j = wid + q * kArnWarps;
         const double s = warp_sum(as[q]), c = warp_sum(ac[q]);
         if (lane == 0 && j <= k) {
@@ -496,8 +515,12 @@ static int arn_grid(long long N) {
 
 void launch_arnoldi_dots(long long N, int k, const double *V, const double *w, ArnWork a, int ldg,
                          cudaStream_t s) {
-    if (k + 1 > kMaxArnoldi) throw Error{FD_ERR_VALIDATION, "arnoldi: restart length above 64"};
-    arnoldi_dots_kernel<<<arn_grid(N), kArnThreads, 0, s>>>(N, k, V, w, a, ldg, arn_chunk(N));
+    if (k + 1 > kMaxArnoldi) throw Error{FD_ERR_VALIDATION, "arnoldi: more basis vectors than kMaxArnoldi"};
+    if (k + 1 <= 4 * kArnWarps)
+        arnoldi_dots_kernel<4><<<arn_grid(N), kArnThreads, 0, s>>>(N, k, V, w, a, ldg, arn_chunk(N));
+    else
+        arnoldi_dots_kernel<kMaxArnoldi / kArnWarps><<<arn_grid(N), kArnThreads, 0, s>>>(N, k, V, w, a, ldg,
+                                                                                        arn_chunk(N));
     FD_CUDA(cudaGetLastError());
 }
 

@@ -289,30 +289,10 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
             blocks += pj.nblk;
             row0 += sj.p.m;
         }
-        // items and segments per CTA (mirrors the kernel's enumeration)
-        int bstride = 1;
-        for (int c = 0; c < grid; ++c) {
-            int items = 0, segs_c = 0;
-            for (long long v = c; v < V; v += grid) {
-                const long long lo_v = lo(v), hi_v = lo(v + 1);
-                long long r0 = 0;
-                for (int j = 0; j < pl.count; ++j) {
-                    const long long r1 = r0 + jobs[j0 + j].p.m;
-                    if (r0 < hi_v && r1 > lo_v) {
-                        const long long len = std::min(hi_v, r1) - std::max(lo_v, r0);
-                        items += int((len + C::G - 1) / C::G);
-                        ++segs_c;
-                    }
-                    r0 = r1;
-                }
-            }
-            bstride = std::max(bstride, items + segs_c);
-        }
         const size_t carry_sz = size_t(blocks) * kCarryVals * pl.n;
-        double *wsp = ws.get(carry_sz + size_t(grid) * bstride * pl.n);
-        pl.carry = wsp;
-        pl.bsave = wsp + carry_sz;
-        pl.bstride = bstride;
+        pl.carry = ws.get(carry_sz);
+        pl.bsave = nullptr;
+        pl.bstride = 0;
         static const bool timing = getenv("FD_PHASE_TIMING") != nullptr;
         unsigned long long *ts = nullptr;
         if (timing) FD_CUDA(cudaMallocAsync(&ts, sizeof(unsigned long long) * 8 * grid, s));

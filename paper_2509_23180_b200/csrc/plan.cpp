@@ -480,6 +480,7 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.R = R;
         d.nb = (m + R - 1) / R;
         d.off = T.soff;
+        d.nio = -1.0 / d.off;
         d.mod_w = mod_w;
         d.mod_e = mod_e;
         d.tpair = pair;
@@ -517,15 +518,7 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.dib = upload(p, dib);
         d.db = upload(p, db);
         if (tk == kFFT) {
-            if (rs_supported(n) && !getenv("FD_OLD")) {
-                build_long_table(T, m, n, d.off, rs_kt_cap(n + 1));
-            } else {
-                // smem budget of the complex-FFT persistent kernel for one group's slice: 13 KB
-                int lg = 0;
-                while ((1 << lg) < 2 * (n + 1)) ++lg;
-                const int G = 16384 >> lg;                     // rows per group at 512 threads
-                build_long_table(T, m, n, d.off, std::max(0, (13 * 1024 / (G * 24)) & ~1));
-            }
+            build_long_table(T, m, n, d.off, rs_kt_cap(n + 1));
         }
         d.kt = T.kt;
         d.ktp = T.ktp;

@@ -149,6 +149,8 @@ def dist_ddm_solve(comp, f, gmres_cfg=None, coupled_id=None, backend=None, group
         q = be.solve(a["plan"], g)
         return q, a["to_c"].coupling * q[a["to_from"]]
 
+    if rank != 0 and not local:
+        return {}, None                                        # no arm here: nothing to serve
     if rank != 0:
         # pre-solve lines to rank 0, then serve operator applications
         for i in sorted(local):
@@ -214,21 +216,25 @@ def dist_ddm_solve(comp, f, gmres_cfg=None, coupled_id=None, backend=None, group
     def preconditioned(p):
         return p - be.solve(cplan, schur(p))
 
-    rhs = be.solve(cplan, f_prime)                             # krylov.py:178
-    x, report = be.gmres(preconditioned, rhs, cfg)
-    resid = be.stencil(center, x) - schur(x) - f_prime         # krylov.py:189
-    report = krylov.SolveReport(report.converged, report.iterations, report.residual_history,
-                                report.wall_time, be.norm(resid))
-    # back-substitution p_i = q_i - A_i^{-1} R_ic p_c
-    broadcast_lines(CMD_BACKSUB, x)
-    out = {coupled_id: x}
-    for i in range(len(arms)):
-        if own[i] == 0:
-            q, _ = arm_apply(i, x[c_from[i]])
-            out[local[i]["sub"].id] = local[i]["q"] - q
-    for r in range(1, world):
-        if any(o == r for o in own):
-            send(be.array([float(CMD_DONE)]), r)
+    # every serving rank always gets CMD_DONE, also when GMRES raises
+    # (ConvergenceError) or anything else fails on rank 0
+    try:
+        rhs = be.solve(cplan, f_prime)                         # krylov.py:178
+        x, report = be.gmres(preconditioned, rhs, cfg)
+        resid = be.stencil(center, x) - schur(x) - f_prime     # krylov.py:189
+        report = krylov.SolveReport(report.converged, report.iterations, report.residual_history,
+                                    report.wall_time, be.norm(resid))
+        # back-substitution p_i = q_i - A_i^{-1} R_ic p_c
+        broadcast_lines(CMD_BACKSUB, x)
+        out = {coupled_id: x}
+        for i in range(len(arms)):
+            if own[i] == 0:
+                q, _ = arm_apply(i, x[c_from[i]])
+                out[local[i]["sub"].id] = local[i]["q"] - q
+    finally:
+        for r in range(1, world):
+            if any(o == r for o in own):
+                send(be.array([float(CMD_DONE)]), r)
     return out, report
 
 

@@ -75,7 +75,49 @@ def _worker(rank, world, port, N, kappa, outdir):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("N,kappa", [(8, 0.0), (15, -100.0)])
-def test_sharded_solve_matches_single_process(tmp_path, world, N, kappa):
+def test_sharded_solve_matches_single_process_ws(tmp_path, world, N, kappa):
+    _run_and_compare(tmp_path, world, N, kappa)
+
+
+def test_more_ranks_than_arms(tmp_path):
+    """world 6 > 4 arms + 1: the rank without an arm returns at once instead of
+    waiting for commands that never come."""
+    _run_and_compare(tmp_path, 6, 8, 0.0)
+
+
+def _fail_worker(rank, world, port, outdir):
+    from paper_2509_23180_b200.errors import ConvergenceError
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    try:
+        comp = configs.cross_composite(15, kappa=0.0)
+        f, _ = configs.manufactured_rhs(comp, "sin_exp")
+        be = OracleBackend()
+        if rank == 0:
+            def gmres(op, rhs, cfg):
+                raise ConvergenceError("forced")
+            be.gmres = gmres
+        status = "ok"
+        try:
+            pdist.dist_ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10), backend=be)
+        except ConvergenceError:
+            status = "raised"
+        with open(os.path.join(outdir, f"rank{rank}.txt"), "w") as fh:
+            fh.write(status)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gmres_failure_releases_workers(tmp_path):
+    """GMRES raising on rank 0 still sends CMD_DONE: the arm ranks return."""
+    port = _free_port()
+    mp.spawn(_fail_worker, args=(3, port, str(tmp_path)), nprocs=3, join=True)
+    assert (tmp_path / "rank0.txt").read_text() == "raised"
+    assert (tmp_path / "rank1.txt").read_text() == "ok"
+    assert (tmp_path / "rank2.txt").read_text() == "ok"
+
+
+def _run_and_compare(tmp_path, world, N, kappa):
     port = _free_port()
     mp.spawn(_worker, args=(world, port, N, kappa, str(tmp_path)), nprocs=world, join=True)
     comp = configs.cross_composite(N, kappa=kappa)

@@ -165,6 +165,30 @@ class TestSchur:
         assert rel(op.preconditioned(p), oo.preconditioned(p)) < 1e-11
 
 
+def assert_true_residual(got, want):
+    """SolveReport.true_residual = ||(A_c - S) x - f'|| (krylov.py:187-195).  At
+    convergence it is set by the last GMRES correction, so two runs whose
+    solutions agree to 1e-10 agree on it to its leading digit, not to 1e-10:
+    the bound is a factor of 2 (a wrong residual, e.g. ||S x||, is off by
+    orders of magnitude)."""
+    assert 0.5 * want <= got <= 2.0 * want, (got, want)
+
+
+def check_solve_report(rep, g):
+    """Large-config solve report against the reference run: the same
+    iteration count, the per-step residual history (the last entry is the
+    cycle-end true relative residual, rounding-level), and the true residual.
+    The histories agree to 1e-5 over the first iterations and drift to ~5e-5
+    relative near 1e-10 (c3: 2.4e-11 absolute), where each entry is a
+    rounding-sensitive quotient of Givens products; the bound is 1e-3."""
+    assert rep.converged
+    assert rep.iterations == int(g["iterations"])
+    np.testing.assert_allclose(rep.residual_history[:10], g["history"][:10], rtol=1e-5)
+    np.testing.assert_allclose(rep.residual_history[:-1], g["history"][:-1], rtol=1e-3)
+    assert rep.residual_history[-1] <= 1e-10
+    assert_true_residual(rep.true_residual, float(g["true_residual"]))
+
+
 class TestDdmSolve:
     @pytest.mark.parametrize("N", [4, 8, 15, 31])
     @pytest.mark.parametrize("kappa", [0.0, -100.0])
@@ -176,6 +200,8 @@ class TestDdmSolve:
         assert rep.iterations == int(golden_small[f"x_iters_{tag}"])
         for sid in range(5):
             assert rel(fields[sid].values, golden_small[f"x_sol_{tag}_{sid}"]) < 1e-10
+        np.testing.assert_allclose(rep.residual_history[:-1], golden_small[f"x_hist_{tag}"][:-1], rtol=1e-5)
+        assert_true_residual(rep.true_residual, float(golden_small[f"x_true_{tag}"]))
 
     def test_c0(self):
         g = load_golden("c0")
@@ -188,6 +214,7 @@ class TestDdmSolve:
         assert np.sqrt(num / den) < 1e-10
         assert configs.rel_l2(fields, exact) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-6)
         np.testing.assert_allclose(rep.residual_history[:-1], g["history"][:-1], rtol=1e-6)
+        assert_true_residual(rep.true_residual, float(g["true_residual"]))
 
     def test_second_order(self):
         errs = []
@@ -216,7 +243,7 @@ class TestDdmSolve:
         g = load_golden("c2")
         comp, f, exact, _ = configs.build_cross_case("c2")
         fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
-        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        check_solve_report(rep, g)
         for sid in range(5):
             v = fields[sid].values
             assert rel(v[g[f"idx_{sid}"]], g[f"val_{sid}"]) < 1e-10
@@ -233,7 +260,7 @@ class TestDdmSolve:
         fd = {k: dev(v) for k, v in f.items()}
         del f
         fields, rep = ddm.ddm_solve(comp, fd, krylov.GmresConfig(m=50, tol=1e-10))
-        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        check_solve_report(rep, g)
         for sid in range(5):
             v = fields[sid].values
             idx = torch.as_tensor(g[f"idx_{sid}"], device="cuda")
@@ -293,7 +320,7 @@ class TestTransposedAxis:
         f, _ = configs.manufactured_rhs(comp, "sin_exp")
         fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
         ofields, orep = O.ddm_solve(comp, f, m=50, tol=1e-10)
-        assert abs(rep.iterations - orep.iterations) <= 1
+        assert rep.iterations == orep.iterations
         num = sum(float(np.sum((fields[s].values - ofields[s]) ** 2)) for s in ofields)
         den = sum(float(np.sum(ofields[s] ** 2)) for s in ofields)
         assert (num / den) ** 0.5 < 1e-10
@@ -325,7 +352,7 @@ class TestTransposedAxis:
         fd = {k: dev(v) for k, v in f.items()}
         del f
         fields, rep = ddm.ddm_solve(comp, fd, krylov.GmresConfig(m=50, tol=1e-10))
-        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        check_solve_report(rep, g)
         for sid in range(5):
             v = fields[sid].values
             idx = torch.as_tensor(g[f"idx_{sid}"], device="cuda")
@@ -431,7 +458,7 @@ class TestInterfaceOnlyVariant:
         comp, f, exact, _ = configs.build_cross_case("c2")
         fd = {k: dev(v) for k, v in f.items()}
         fields, rep = ddm.ddm_solve(comp, fd, krylov.GmresConfig(m=50, tol=1e-10), interface_only=True)
-        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        check_solve_report(rep, g)
         for sid in range(5):
             v = fields[sid].values
             idx = torch.as_tensor(g[f"idx_{sid}"], device="cuda")
@@ -447,7 +474,7 @@ class TestComparisonStudies:
         g = load_golden("nn")
         comp, f, _, _ = configs.build_cross_case("c0", N=15)
         fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10, preconditioner=pre))
-        assert abs(rep.iterations - int(g[f"pre_iters_{pre}"])) <= 1
+        assert rep.iterations == int(g[f"pre_iters_{pre}"])
         num = sum(float(np.sum((fields[s].values - g[f"pre_p_{pre}_{s}"]) ** 2)) for s in range(5))
         den = sum(float(np.sum(g[f"pre_p_{pre}_{s}"] ** 2)) for s in range(5))
         assert (num / den) ** 0.5 < 1e-9
@@ -496,7 +523,7 @@ class TestDeviceAssembly:
         g = load_golden("c2")
         comp, fd, exd, _ = configs.build_cross_case("c2", device=True)
         fields, rep = ddm.ddm_solve(comp, fd, krylov.GmresConfig(m=50, tol=1e-10))
-        assert abs(rep.iterations - int(g["iterations"])) <= 1
+        check_solve_report(rep, g)
         assert configs.rel_l2_device(fields, exd) == pytest.approx(float(g["rel_l2_exact"]), rel=1e-4)
 
 
