@@ -680,17 +680,8 @@ struct RsK {
     static const void *fn() { return (const void *)rsolve_kernel<NL>; }
 };
 
-bool launch_k3(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
-
-// build-time A/B switch (FD_EXTRA_FLAGS=-DFD_K3=0): the lockstep kernel below
-// for every FFT length
-#ifndef FD_K3
-#define FD_K3 0
-#endif
-
 // the FFT-path solve of a batch of plans with one transform length
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
-    if (FD_K3 && launch_k3(jobs, s, ws)) return true;
     const int n = jobs[0].p.n;
     if (!rs_supported(n) || !jobs[0].p.ralpha) return false;
     switch (n + 1) {
