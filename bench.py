@@ -40,9 +40,17 @@ METRIC = "grid points solved/sec (fp64, 1e-10 res); precond-apply HBM GB/s vs pe
 WORKLOAD = "c1: batched precond apply, 5 x 1023^2 fp64 Dirichlet, kappa=0, DST-I->Thomas->DST-I"
 
 
+def bench_config(world: int) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": WORKLOAD, "points_per_step": POINTS, "batch": COUNT, "n": N_SIDE, "kappa": KAPPA,
+            "l2_policy": "8 rotating buffer sets = 670 MB > 126 MB L2 (GPU arm)",
+            "parallelism": f"replicas x{world} (independent batches, no collective)"}
+
+
 def ncu_traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_rsolve_c1_ncu_full.json")
+    """DRAM bytes per launch of the dominant kernel: ncu --set full capture of a
+    launch inside the rotating-buffer loop of this benchmark (profiles/)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_rsolve_c1_loop_ncu.json")
     try:
         d = json.load(open(path))
         mb = lambda s: float(s.split()[0]) * (1e6 if "Mbyte" in s else 1e3 if "Kbyte" in s else 1e9 if "Gbyte" in s else 1.0)
@@ -146,7 +154,7 @@ def cpu_reference(steps: int, warmup: int, sample_subdomains: int = COUNT, max_s
     subs = configs.batch_rects(N_SIDE, sample_subdomains, KAPPA)
     f = make_rhs()[:sample_subdomains]
     plans = [O.plan(s) for s in subs]
-    cores = min(sample_subdomains, len(os.sched_getaffinity(0)))
+    cores = min(sample_subdomains, len(os.sched_getaffinity(0)))   # one thread per subdomain
     pool = ThreadPoolExecutor(max_workers=cores)
     run = lambda: list(pool.map(lambda a: O.solve(*a), zip(plans, f)))  # noqa: E731
     for _ in range(warmup):
@@ -163,7 +171,30 @@ def cpu_reference(steps: int, warmup: int, sample_subdomains: int = COUNT, max_s
     per = statistics.median(times)
     pts = sample_subdomains * N_SIDE * N_SIDE
     return pts / per, cores, (f"{len(times)} timed steps x {sample_subdomains} x 1023^2 solves "
-                              f"(median step {per:.3f} s), {cores} threads")
+                              f"(median step {per:.3f} s), {cores} threads on "
+                              f"{len(os.sched_getaffinity(0))} host cores")
+
+
+def cpu_full_solve(name="c0", threads=(1, 4)):
+    """Algorithm 1 end to end on the CPU in this run: the oracle restatement of
+    the reference ddm_solve on a BASELINE cross (c0), single-threaded and with
+    the neighbour solves on a thread pool like the reference's SOLVER_THREADS
+    (ddm.py:152-201).  Wall time of one solve after a warm-up call."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import fftddm_oracle as O
+    from paper_2509_23180_b200 import configs
+
+    comp, f, _, meta = configs.build_cross_case(name)
+    host = len(os.sched_getaffinity(0))
+    out = {"config": name, "points": meta["points"], "host_cores": host, "kind": "port"}
+    for th in threads:
+        th = max(1, min(th, host))
+        O.ddm_solve(comp, f, m=50, tol=1e-10, threads=th)
+        t0 = time.perf_counter()
+        _, rep = O.ddm_solve(comp, f, m=50, tol=1e-10, threads=th)
+        wall = time.perf_counter() - t0
+        out[f"threads_{th}"] = {"wall_s": wall, "value": meta["points"] / wall, "iterations": rep.iterations}
+    return out
 
 
 def run_reference(args, world, rank):
@@ -174,9 +205,10 @@ def run_reference(args, world, rank):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": POINTS / value * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (uniform[-1,1], seed 0)",
-            "config": {"workload": WORKLOAD, "points_per_step": POINTS},
+            "config": bench_config(world),
             "cpu_baseline": {"value": value, "unit": "grid_points/s", "cores": cores,
                              "kind": "port", "sample": sample},
+            "full_solve_cpu": cpu_full_solve(),
             "e2e": {"value": value, "unit": "grid_points/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -250,15 +282,46 @@ def full_solve(dev, name="c2", reps=3):
         del fields4, f4, ex4
     out["c4_device_assembled"] = dict(c4, points=meta4["points"],
                                       timing="assembly + ddm_solve, best of 2 (the first call of each builds plan tables)",
-                                      reference={"iterations": 67, "wall_s": 1373.4, "rel_l2_vs_exact": 4.933e-8,
-                                                 "where": "reference fftddm on the build container's CPU (SURVEY 6)"})
-    gpath = os.path.join(ROOT, "tests", "golden", f"{name}.npz")
-    if os.path.exists(gpath):
-        g = np.load(gpath)
-        out["reference"] = {"iterations": int(g["iterations"]), "wall_s": float(g["wall"]),
-                            "rel_l2_vs_exact": float(g["rel_l2_exact"]),
-                            "where": "reference fftddm on the build container's CPU (golden run)"}
+                                      reference=golden_ref("c4"))
+    # c3 (84M points, kappa = -100, random RHS) and c0 (latency-bound), RHS on the device
+    for extra in ("c3", "c0"):
+        compx, fx, _, metax = configs.build_cross_case(extra)
+        fxd = {k: torch.as_tensor(v, device=dev) for k, v in fx.items()}
+        del fx
+        ddm.ddm_solve(compx, fxd, cfg)
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, repx = ddm.ddm_solve(compx, fxd, cfg)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        wx = statistics.median(ts)
+        out[extra] = {"points": metax["points"], "iterations": repx.iterations, "wall_s": wx,
+                      "value": metax["points"] / wx, "us_per_iteration": rep_us(repx),
+                      "true_residual": repx.true_residual, "reference": golden_ref(extra)}
+        del fxd
+    out["reference"] = golden_ref(name)
     return out
+
+
+def rep_us(rep):
+    return rep.wall_time / max(rep.iterations, 1) * 1e6
+
+
+def golden_ref(name):
+    """The reference run recorded with the golden fixture (tests/golden/<name>.npz):
+    iterations, wall time on the build container's CPU, error vs the exact solution."""
+    gpath = os.path.join(ROOT, "tests", "golden", f"{name}.npz")
+    if not os.path.exists(gpath):
+        return None
+    g = np.load(gpath)
+    ref = {"iterations": int(g["iterations"]), "wall_s": float(g["wall"]), "true_residual": float(g["true_residual"]),
+           "threads": int(g["threads"]) if "threads" in g.files else None,
+           "where": "reference fftddm on the build container's CPU (golden run, not this host)"}
+    if "rel_l2_exact" in g.files:
+        ref["rel_l2_vs_exact"] = float(g["rel_l2_exact"])
+    return ref
 
 
 def run_gpu(args, world, rank, local):
@@ -380,6 +443,24 @@ def run_gpu(args, world, rank, local):
     io_bytes = sum(r.nbytes for r in rhs)
 
 
+    # the kappa = -10 half of BASELINE config 1: same kernel, other plan tables
+    subs10 = configs.batch_rects(N_SIDE, COUNT, -10.0)
+    plans10 = [rectsolver.plan_rect(s_) for s_ in subs10]
+    hp10 = _native.ptr_array([p_.handle.ptr for p_ in plans10])
+    for i in range(3):
+        _native.check(lib.fd_rect_solve_batched(COUNT, hp10, fps[i % SETS], ops[i % SETS], sp))
+    barrier()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k_steps = max(10, min(args.steps, 500))
+    k0.record(stream)
+    for i in range(k_steps):
+        lib.fd_rect_solve_batched(COUNT, hp10, fps[i % SETS], ops[i % SETS], sp)
+    k1.record(stream)
+    barrier()
+    ms10 = k0.elapsed_time(k1) / k_steps
+    kappa_m10 = {"ms_per_step": ms10, "value": POINTS / (ms10 * 1e-3), "unit": "grid_points/s",
+                 "roofline_frac": B_ALG * POINTS / (ms10 * 1e-3) / 1e9 / peaks()[0], "steps": k_steps}
+
     solve = None
     if not args.no_solve:
         try:
@@ -398,16 +479,13 @@ def run_gpu(args, world, rank, local):
         if world == 1 and not args.no_cpu:
             v, cores, sample = cpu_reference(steps=8, warmup=1, max_seconds=15.0)
             cpu = {"value": v, "unit": "grid_points/s", "cores": cores, "kind": "port",
-                   "sample": sample}
+                   "sample": sample, "host_cores": len(os.sched_getaffinity(0)),
+                   "full_solve_c0": cpu_full_solve()}
         line = {"metric": METRIC, "value": value, "unit": "grid_points/s", "n_gpus": world,
                 "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (uniform[-1,1], seed 0; BASELINE config 1)",
-                "config": {"workload": WORKLOAD, "points_per_step": POINTS,
-                           "batch": COUNT, "n": N_SIDE, "kappa": KAPPA,
-                           "l2_policy": f"{SETS} rotating buffer sets = "
-                                        f"{SETS * 2 * io_bytes / 1e6:.0f} MB > 126 MB L2",
-                           "parallelism": f"replicas x{world} (independent batches, no collective)"},
+                "config": bench_config(world),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak,
                              # dram__bytes_read.sum + dram__bytes_write.sum per launch from
@@ -422,6 +500,7 @@ def run_gpu(args, world, rank, local):
                         "ms_per_step": e_ms,
                         "pipeline": "3 buffer sets, one DMA per direction per step; H2D, solve, D2H on 3 streams (D2H of step i overlaps H2D of i+1); timed over 100 steps incl. pipeline fill and drain",
                         "pcie_floor_ms": "0.89 (concurrent pinned H2D + D2H of 41.9 MB each, tools/pcie_probe.py)"},
+                "kappa_m10": kappa_m10,
                 "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk.summary(),
                 "check": {"rel_residual_Ap_minus_f": resid,

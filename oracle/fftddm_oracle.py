@@ -350,7 +350,10 @@ def coupling(comp, iface, from_id):
 class Schur:
     """Matrix-free (A_c - sum_i R_ci A_i^-1 R_ic) on the centre (ddm.py:94-136)."""
 
-    def __init__(self, comp, coupled_id=None):
+    def __init__(self, comp, coupled_id=None, threads=1):
+        # threads > 1: neighbour solves on a pool, like the reference's
+        # ThreadPoolExecutor over arms (ddm.py:182-201, 112-123)
+        self.pool = None
         if coupled_id is None:
             ids = sorted(comp.coupled_ids)
             coupled_id = ids[0] if ids else min(s.id for s in comp.subdomains)
@@ -363,6 +366,9 @@ class Schur:
             self.neighbors.append((plan(comp.subdomain(other)),
                                    coupling(comp, f, other),          # R_ci
                                    coupling(comp, f, coupled_id)))    # R_ic
+        if threads > 1 and len(self.neighbors) > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            self.pool = ThreadPoolExecutor(max_workers=min(threads, len(self.neighbors)))
 
     @property
     def size(self):
@@ -370,6 +376,11 @@ class Schur:
 
     def schur(self, p):
         out = np.zeros(self.size)
+        if self.pool is not None:   # solves in parallel, parts added in neighbour order
+            parts = list(self.pool.map(lambda nb: nb[1].apply(solve(nb[0], nb[2].apply(p))), self.neighbors))
+            for part in parts:
+                out += part
+            return out
         for pl, to_c, from_c in self.neighbors:
             out += to_c.apply(solve(pl, from_c.apply(p)))
         return out
@@ -461,10 +472,10 @@ def gmres(op, rhs, m=80, tol=1e-10, max_restarts=200, x0=None):
     raise RuntimeError(f"oracle GMRES did not converge in {its} iterations")
 
 
-def ddm_solve(comp, f, m=50, tol=1e-10, max_restarts=200):
+def ddm_solve(comp, f, m=50, tol=1e-10, max_restarts=200, threads=1):
     """Algorithm 1: arm pre-solves, reduced RHS, GMRES on the preconditioned
     Schur system, back-substitution (ddm.py:210-270, krylov.py:168-195)."""
-    op = Schur(comp)
+    op = Schur(comp, threads=threads)
     qs = [solve(pl, np.asarray(f[pl.sub.id], dtype=float)) for pl, _, _ in op.neighbors]
     fp = np.array(f[op.coupled_id], dtype=float)
     for (pl, to_c, _), q in zip(op.neighbors, qs):

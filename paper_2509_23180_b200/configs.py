@@ -218,6 +218,46 @@ def reference_cross(k_n: int, L: float = 1.0 / 7.0, kappa: float = 0.0, api=None
     return comp
 
 
+def _psi_coeffs(L: float):
+    """Phase polynomials of the reference cross's manufactured solution
+    (reference bench.py derive_psi_coeffs): psi_x(x) = x (A1 + A2 (x - L) +
+    A3 (x^2 - 4 L x + 3 L^2)) hits pi/2, 3pi/2, 3pi at x = L, 3L, 7L and psi_y
+    hits pi/2, 3pi/2, 2pi at y = 2L, 6L, 7L (3 x 3 solves per axis), so
+    p = sin psi_x sin psi_y vanishes on the outer Dirichlet edges."""
+    def axis(xs, targets, shift, q):
+        M = np.array([[x, x * (x - shift), x * q(x)] for x in xs])
+        return np.linalg.solve(M, np.asarray(targets))
+    a = axis([L, 3 * L, 7 * L], [np.pi / 2, 3 * np.pi / 2, 3 * np.pi], L, lambda x: x * x - 4 * L * x + 3 * L * L)
+    b = axis([2 * L, 6 * L, 7 * L], [np.pi / 2, 3 * np.pi / 2, 2 * np.pi], 2 * L,
+             lambda y: y * y - 8 * L * y + 12 * L * L)
+    return a, b
+
+
+def reference_cross_case(k_n: int, L: float = 1.0 / 7.0, kappa: float = 0.0, api=None):
+    """reference_cross(k_n) with its manufactured problem (reference bench.py
+    manufactured_solution / manufactured_rhs / rhs_fields): f = Laplacian of
+    p = sin psi_x(x) sin psi_y(y) (+ kappa p) at the nodes, no lifting (p is
+    zero on the Dirichlet edges).  Returns (comp, f, exact)."""
+    comp = reference_cross(k_n, L, kappa, api)
+    (A1, A2, A3), (B1, B2, B3) = _psi_coeffs(L)
+    f, exact = {}, {}
+    for sub in comp.subdomains:
+        x, y = (a.ravel() for a in node_grid(sub))
+        px = x * (A1 + A2 * (x - L) + A3 * (x * x - 4 * L * x + 3 * L * L))
+        dpx = A1 + A2 * (2 * x - L) + A3 * (3 * x * x - 8 * L * x + 3 * L * L)
+        ddpx = 2 * A2 + A3 * (6 * x - 8 * L)
+        py = y * (B1 + B2 * (y - 2 * L) + B3 * (y * y - 8 * L * y + 12 * L * L))
+        dpy = B1 + B2 * (2 * y - 2 * L) + B3 * (3 * y * y - 16 * L * y + 12 * L * L)
+        ddpy = 2 * B2 + B3 * (6 * y - 16 * L)
+        sx, cx, sy, cy = np.sin(px), np.cos(px), np.sin(py), np.cos(py)
+        rhs = (ddpx * cx - dpx * dpx * sx) * sy + sx * (ddpy * cy - dpy * dpy * sy)
+        if kappa:
+            rhs = rhs + kappa * sx * sy
+        f[sub.id] = rhs
+        exact[sub.id] = sx * sy
+    return comp, f, exact
+
+
 def batch_rects(n: int = 1023, count: int = 5, kappa: float = 0.0, api=None):
     """c1: `count` independent all-Dirichlet n x n rectangles, h = 1/n."""
     api = api or default_api()

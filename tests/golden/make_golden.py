@@ -282,6 +282,58 @@ def make_cyclic():
     print("cyclic.npz written")
 
 
+def make_acceptance():
+    """The reference's acceptance gates C3-C5 (tests/test_acceptance.py:78-128)
+    run by the reference on its own cross: C3 node-error sup norms at k_n = 4..64
+    (default GmresConfig), C4 fft / identity iteration counts at k_n = 16
+    (m = 80, tol 1e-7, 25 restarts), C5 iteration counts at k_n = 8..128
+    (m = 80, tol 1e-7).  Also checks that configs.reference_cross_case
+    reproduces the reference's bench.rhs_fields / exact_fields bitwise."""
+    from fftddm import bench
+    from fftddm.errors import ConvergenceError
+    from fftddm.geometry import GridField
+    out = {}
+    for kn in (4, 8, 16, 32, 64):
+        case = bench.build_cross(k_n=kn)
+        comp, f, exact = configs.reference_cross_case(kn, api=API)
+        ref_f = bench.rhs_fields(case)
+        ref_x = bench.exact_fields(case)
+        for sid in f:
+            assert np.array_equal(f[sid], ref_f[sid].values), ("rhs", kn, sid)
+            assert np.array_equal(exact[sid], ref_x[sid].values), ("exact", kn, sid)
+        t0 = time.perf_counter()
+        fields, rep = bench.solve_case(case)
+        linf, l2 = bench.error_norms(case, fields)
+        out[f"c3_linf_{kn}"] = linf
+        out[f"c3_l2_{kn}"] = l2
+        out[f"c3_iters_{kn}"] = rep.iterations
+        print("C3", kn, linf, rep.iterations, time.perf_counter() - t0, flush=True)
+    case = bench.build_cross(k_n=16)
+    op = ddm.build_schur_operator(case.composite)
+    f = bench.rhs_fields(case)
+    f_prime = f[op.coupled_id].values.copy()
+    for nb in op.neighbors:
+        f_prime -= nb.to_center.apply(rectsolver.solve_rect(nb.plan, f[nb.plan.subdomain.id]).values)
+    rhs = GridField(op.coupled_id, f_prime)
+    for mode in ("fft", "identity"):
+        cfg = krylov.GmresConfig(m=80, tol=1e-7, max_restarts=25, preconditioner=mode)
+        try:
+            _, rep = krylov.solve_coupled(op, rhs, cfg)
+            out[f"c4_iters_{mode}"] = rep.iterations
+            out[f"c4_conv_{mode}"] = 1
+        except ConvergenceError as exc:
+            out[f"c4_iters_{mode}"] = exc.report.iterations
+            out[f"c4_conv_{mode}"] = 0
+        print("C4", mode, out[f"c4_iters_{mode}"], flush=True)
+    rows = bench.run_scaling([8, 16, 32, 64, 128], tol_list=(1e-7,), m=80)
+    for r in rows:
+        out[f"c5_iters_{r['k_n']}"] = r["iterations"]
+    out["c5_exponent"] = rows[0]["fitted_exponent"]
+    print("C5", {r["k_n"]: r["iterations"] for r in rows}, rows[0]["fitted_exponent"], flush=True)
+    np.savez_compressed(os.path.join(HERE, "acceptance.npz"), **out)
+    print("acceptance.npz written")
+
+
 if __name__ == "__main__":
     for what in sys.argv[1:] or ["small", "c0", "c1"]:
         if what == "small":
@@ -290,6 +342,8 @@ if __name__ == "__main__":
             make_nn()
         elif what == "cyclic":
             make_cyclic()
+        elif what == "acceptance":
+            make_acceptance()
         elif what == "c1":
             make_c1()
         else:

@@ -187,3 +187,21 @@ class TestPeriodicSweepFixtures:
             p = O.solve(O.plan(sub), f)
             r = O.apply_operator(sub, p) - f
             assert np.abs(r).max() <= 1e-10 * max(np.abs(f).max(), 1.0), case
+
+
+def test_reference_cross_acceptance_goldens():
+    """The oracle on the reference's own cross (configs.reference_cross_case,
+    NN arms, half-cell ends) reproduces the reference's C3 run at k_n = 4, 8:
+    same iteration counts, node errors to 1e-9 (pins the restated
+    manufactured problem used by the GPU acceptance tests)."""
+    import numpy as np
+    from conftest import load_golden
+    from paper_2509_23180_b200 import configs
+    import fftddm_oracle as O
+    g = load_golden("acceptance")
+    for kn in (4, 8):
+        comp, f, exact = configs.reference_cross_case(kn)
+        fields, rep = O.ddm_solve(comp, f, m=80, tol=1e-10)
+        assert rep.iterations == int(g[f"c3_iters_{kn}"])
+        linf = max(float(np.abs(fields[s] - exact[s]).max()) for s in exact)
+        assert abs(linf - float(g[f"c3_linf_{kn}"])) <= 1e-9 * float(g[f"c3_linf_{kn}"])
