@@ -62,6 +62,7 @@ struct PlanDev {
     const double2 *tw;   // FFT twiddles e^{-2 pi i t / L}, t < L = 2(n+1), or nullptr
     const double *ralpha;// [n+1] real-DST pre-weights (rsolve.cu), alpha_j = s/2 sin(pi j/N) + s/4
     int tpair;           // transform-axis pair: kPairDD (sine), kPairNN (shifted cosine), kPairPP (real Fourier)
+    int tkind;           // Transform of the plan (kFFT, kDense, kSep)
     // periodic sweep axis (rectsolver.py:136-153,202-205): the factors above are
     // those of the rank-one modified system; phat -= q_k (vy_k / denom_k)
     int cyclic;
@@ -110,8 +111,9 @@ inline bool rs_supported(int n) {
     return N >= kRsMinN && N <= kRsMaxN && (N & (N - 1)) == 0;
 }
 
-enum Transform { kDense = 0, kFFT = 1 };
+enum Transform { kDense = 0, kFFT = 1, kSep = 2 };   // kSep: any-length transform passes + sweeps
 constexpr int kDenseMax = 2048;   // longest dense periodic-table transform (dst_device.cuh)
+constexpr int kSepMax = 65535;    // longest any-length transform (fft_any.cu: power-of-two sizes <= 2^18)
 
 // Device allocations of plans, operators and the Krylov basis come from the
 // device's stream-ordered pool with an unbounded release threshold, so the
@@ -193,6 +195,11 @@ struct JobList {
 int rows_per_block(int n, int pair = kPairDD);
 int transform_kind(int n, int pair = kPairDD);
 void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s);
+// any-length transforms (fft_any.cu): complex DFT rows (power of two: Stockham;
+// otherwise Bluestein) and the real row transforms of the three pairs
+void dft_rows(long long rows, int M, const double2 *in, double2 *out, int inverse, cudaStream_t st);
+void transform_rows_any(long long rows, int n, int pair, int inverse, const double *in, double *out, double alpha,
+                        double beta, const double *other, cudaStream_t st);
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
 void launch_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out,
                            const double *dense, cudaStream_t s);

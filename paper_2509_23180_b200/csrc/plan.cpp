@@ -443,15 +443,14 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
     int tk = transform_kind(n, pair);
     // the correction and pseudo-inverse terms live in the three-kernel dense solve
     const bool forced = tk == kFFT && (cyclic || pin);
-    if (forced) tk = n <= kDenseMax ? kDense : -1;   // dense transform limit (dst_device.cuh kDenseMax)
+    if (forced) tk = n <= kDenseMax ? kDense : kSep;   // dense transform limit (dst_device.cuh kDenseMax)
     if (tk < 0) {
         std::ostringstream os;
-        os << "plan: no GPU transform for n = " << n
-           << " (supported: n+1 a power of two in [256, 4096], or n <= 2048)";
+        os << "plan: no GPU transform for n = " << n << (pair == kPairPP && (n & 1) ? " (periodic axes need an even length)" : "");
         FD_FAIL(FD_ERR_UNSUPPORTED, os.str());
     }
     const int R = forced ? 8 : rows_per_block(n, pair);   // forced: the dense path's rows per group
-    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R, tk == kDense, pair, cyclic);
+    HostTables T = build_tables(m, n, dx, dy, kappa, mod_w, mod_e, R, tk != kFFT, pair, cyclic);
     if (!T.bad_modes.empty() && !pin) {
         std::ostringstream os;
         os << "operator singular in spectral modes (";
@@ -484,6 +483,7 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.mod_w = mod_w;
         d.mod_e = mod_e;
         d.tpair = pair;
+        d.tkind = tk;
         d.scale = (pair == kPairNN || pair == kPairPP) ? sqrt(2.0 / n) : sqrt(2.0 / (n + 1));
         d.ex_off = upload(p, T.off);
         d.ex_len = upload(p, T.len);
@@ -540,7 +540,7 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.ye = d.fs = nullptr;   // per-plan scratch (plan_create)
         d.tw = tk == kFFT ? twiddles_for(device, n) : nullptr;
         d.ralpha = d.tw ? reinterpret_cast<const double *>(d.tw + 2 * (n + 1)) : nullptr;
-        d.dense = dense_table_for(device, n, pair, forced);
+        d.dense = tk == kDense ? dense_table_for(device, n, pair, forced) : nullptr;
         p->flags = flags;
         d.cyclic = !T.smq.empty();
         d.smq = d.cyclic ? upload(p, T.smq) : nullptr;
@@ -627,7 +627,7 @@ Plan *plan_create(int m, int n, double dx, double dy, double kappa, double mod_w
     p->sing_modes = proto->sing_modes;
     p->dev.pinv = nullptr;   // pseudo-inverses are attached per plan (fd_plan_set_pinv)
     p->dev.sf = p->dev.sph = nullptr;
-    if (p->transform == kDense) {   // pass-1/carry scratch of the three-kernel solve
+    if (p->transform == kDense || p->transform == kSep) {   // pass-1/carry scratch of the three-kernel solves
         try {
             if (p->dev.nsing) {
                 const size_t sb = sizeof(double) * size_t(p->dev.nsing) * m;

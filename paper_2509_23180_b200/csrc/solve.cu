@@ -490,6 +490,177 @@ __global__ void __launch_bounds__(P::NT, P::MINB) pass2_kernel(const __grid_cons
     }
 }
 
+// ---------------------------------------------------------------------------
+// Separate-transform solve (kSep: transform lengths without a fused kernel):
+// the rows are transformed by the any-length passes of fft_any.cu; the two
+// sweeps below are pass1/pass2 without the transform, every CTA handling one
+// carry block for a slice of kSepModes modes (coalesced over modes), so any n
+// fits.  Same recurrences and carries as the dense path.
+constexpr int kSepThreads = 256, kSepMPT = 4, kSepModes = kSepThreads * kSepMPT, kSepG = 8;
+__device__ __forceinline__ void sep_block(const JobList &jl, int &job, int &b, int &k0) {
+    job = find_job(jl, blockIdx.x);
+    const int local = blockIdx.x - jl.block_start[job];
+    const int slices = (jl.job[job].p.n + kSepModes - 1) / kSepModes;
+    b = local / slices;
+    k0 = (local % slices) * kSepModes;
+}
+
+// pass 1: local forward elimination of the transformed rows (in) -> yhat (out)
+__global__ void __launch_bounds__(kSepThreads) sep_pass1_kernel(const __grid_constant__ JobList jl) {
+    int job, b, k0;
+    sep_block(jl, job, b, k0);
+    const SolveJob &J = jl.job[job];
+    const PlanDev &p = J.p;
+    const int n = p.n, m = p.m;
+    const int s = b * p.R, e = min(m, s + p.R) - 1;
+#pragma unroll 1
+    for (int u = 0; u < kSepMPT; ++u) {
+        const int k = k0 + threadIdx.x + u * kSepThreads;
+        if (k >= n) continue;
+        ModeView mv;
+        mv.load(p, k);
+        const int si = p.nsing ? __ldg(p.sidx + k) : -1;
+        double y = 0.0, w = 0.0, f = 0.0;
+#pragma unroll 1
+        for (int g0 = s; g0 <= e; g0 += kSepG) {
+            const int rows = min(kSepG, e - g0 + 1);
+            double rv[kSepG], lv[kSepG], ibv[kSepG];   // the group's rows and factors ahead of the chain
+#pragma unroll
+            for (int rr = 0; rr < kSepG; ++rr) {
+                const int i = g0 + rr;
+                const bool in = rr < rows;
+                const bool ex = in && i < mv.len;
+                const double *er = p.ex + 4 * size_t(mv.off + i);
+                rv[rr] = in ? J.in[size_t(i) * n + k] : 0.0;
+                lv[rr] = ex ? __ldg(er) : mv.l_inf;
+                ibv[rr] = (i == m - 1) ? mv.ib_last : (ex ? __ldg(er + 1) : mv.ib_inf);
+            }
+#pragma unroll
+            for (int rr = 0; rr < kSepG; ++rr) {
+                if (rr >= rows) break;
+                const int i = g0 + rr;
+                const double r = rv[rr];
+                if (si >= 0) p.sf[size_t(si) * m + i] = r;   // fhat column of a pinned mode
+                if (i == s) {
+                    y = r;
+                    w = 1.0;
+                } else {
+                    const double l = lv[rr];
+                    y = __dsub_rn(r, __dmul_rn(l, y));   // rectsolver.py:86
+                    w = -l * w;
+                }
+                f = fma(y, w * ibv[rr], f);
+                J.out[size_t(i) * n + k] = y;
+            }
+        }
+        p.ye[size_t(b) * n + k] = y;
+        p.fs[size_t(b) * n + k] = f;
+    }
+}
+
+// pass 2: carry fix-up + back-substitution of yhat (out) -> xhat (out, in place)
+__global__ void __launch_bounds__(kSepThreads) sep_pass2_kernel(const __grid_constant__ JobList jl) {
+    int job, b, k0;
+    sep_block(jl, job, b, k0);
+    const SolveJob &J = jl.job[job];
+    const PlanDev &p = J.p;
+    const int n = p.n, m = p.m;
+    const int s = b * p.R, e = min(m, s + p.R) - 1;
+    const double off = p.off;
+#pragma unroll 1
+    for (int u = 0; u < kSepMPT; ++u) {
+        const int k = k0 + threadIdx.x + u * kSepThreads;
+        if (k >= n) continue;
+        ModeView mv;
+        mv.load(p, k);
+        const double yin = b > 0 ? p.ye[size_t(b - 1) * n + k] : 0.0;
+        double x = b < p.nb - 1 ? p.fs[size_t(b + 1) * n + k] : 0.0;
+        double pcur = __ldg(p.blk + (size_t(b) * 3 + 0) * n + k);   // P at row e
+        double cc = 0.0;
+        if (p.cyclic) {   // Sherman-Morrison factor from the carried ends (rectsolver.py:203-205)
+            const double x0 = p.fs[k];
+            const double xl = __ddiv_rn(p.ye[size_t(p.nb - 1) * n + k], __ldg(p.last + 2 * k));
+            const double vy = __dadd_rn(x0, __dmul_rn(__ldg(p.cyc + 2 * k), xl));
+            cc = __ddiv_rn(vy, __ldg(p.cyc + 2 * k + 1));
+        }
+        const int si = p.nsing ? __ldg(p.sidx + k) : -1;
+        const int glast = s + ((e - s) / kSepG) * kSepG;
+#pragma unroll 1
+        for (int g0 = glast; g0 >= s; g0 -= kSepG) {
+            const int rows = min(kSepG, e - g0 + 1);
+            double yv[kSepG], Pv[kSepG], bv[kSepG];
+#pragma unroll
+            for (int rr = 0; rr < kSepG; ++rr) {
+                const int i = g0 + rr;
+                const bool in = rr < rows;
+                const bool ex = in && i < mv.len;
+                const double *er = p.ex + 4 * size_t(mv.off + i);
+                yv[rr] = in ? J.out[size_t(i) * n + k] : 0.0;
+                Pv[rr] = ex ? __ldg(er + 3) : 0.0;
+                bv[rr] = (i == m - 1) ? mv.b_last : (ex ? __ldg(er + 2) : mv.b_inf);
+            }
+#pragma unroll
+            for (int rr = kSepG - 1; rr >= 0; --rr) {
+                if (rr >= rows) continue;
+                const int i = g0 + rr;
+                double y = yv[rr];
+                if (b > 0) {
+                    const double Pi = i < mv.len ? Pv[rr] : pcur;
+                    y = fma(Pi, yin, y);
+                    pcur *= mv.inv_nl;
+                }
+                x = __ddiv_rn(__dsub_rn(y, __dmul_rn(off, x)), bv[rr]);   // rectsolver.py:90
+                double xo = x;
+                if (p.cyclic) xo = __dsub_rn(x, __dmul_rn(__ldg(p.smq + size_t(i) * n + k), cc));
+                if (si >= 0) xo = p.sph[size_t(si) * m + i];   // rectsolver.py:206-207
+                J.out[size_t(i) * n + k] = xo;
+            }
+        }
+    }
+}
+
+// jobs of one (n, pair): Q^T of every rectangle into its plan scratch, the two
+// sweeps with the carries in between, Q back into out with the epilogue
+static void run_sep(const std::vector<SolveJob> &jobs, cudaStream_t s) {
+    for (size_t j0 = 0; j0 < jobs.size(); j0 += kMaxJobs) {
+        JobList jl{}, jc{};
+        jl.count = jc.count = (int)std::min<size_t>(kMaxJobs, jobs.size() - j0);
+        int tot = 0, totc = 0;
+        for (int j = 0; j < jl.count; ++j) {
+            SolveJob sj = jobs[j0 + j];
+            const PlanDev &p = sj.p;
+            double *T = sj.ws->get(size_t(p.m) * p.n);   // transformed right-hand side
+            transform_rows_any(p.m, p.n, p.tpair, 0, sj.in, T, 1.0, 0.0, nullptr, s);
+            sj.in = T;
+            jl.job[j] = sj;
+            jc.job[j] = sj;
+            jl.block_start[j] = tot;
+            jc.block_start[j] = totc;
+            tot += p.nb * ((p.n + kSepModes - 1) / kSepModes);
+            totc += (p.n + kCarryModes - 1) / kCarryModes;
+        }
+        jl.block_start[jl.count] = tot;
+        jc.block_start[jc.count] = totc;
+        sep_pass1_kernel<<<tot, kSepThreads, 0, s>>>(jl);
+        FD_CUDA(cudaGetLastError());
+        carry_kernel<<<totc, kCarryThreads, 0, s>>>(jc);
+        FD_CUDA(cudaGetLastError());
+        for (int j = 0; j < jl.count; ++j) {
+            const PlanDev &p = jl.job[j].p;
+            if (!p.nsing) continue;
+            if (!p.pinv) FD_FAIL(FD_ERR_SINGULAR, "plan is singular (pin_mean plan without pseudo-inverses)");
+            pinv_kernel<<<dim3((p.m + 255) / 256, p.nsing), 256, 0, s>>>(p.m, p.nsing, p.pinv, p.sf, p.sph);
+            FD_CUDA(cudaGetLastError());
+        }
+        sep_pass2_kernel<<<tot, kSepThreads, 0, s>>>(jl);
+        FD_CUDA(cudaGetLastError());
+        for (int j = 0; j < jl.count; ++j) {
+            const SolveJob &sj = jl.job[j];
+            transform_rows_any(sj.p.m, sj.p.n, sj.p.tpair, 1, sj.out, sj.out, sj.alpha, sj.beta, sj.other, s);
+        }
+    }
+}
+
 // plain row transform (apply_Q): rows of `in` -> `out`
 template <class P>
 __global__ void __launch_bounds__(P::NT) dst_rows_kernel(int rows_total, int n, const double *in,
@@ -525,15 +696,18 @@ __global__ void __launch_bounds__(P::NT) dense_rows_kernel(int rows_total, int n
 // host side
 int transform_kind(int n, int pair) {
     const int N = n + 1;
+    if (n < 1) return -1;
     if (pair == kPairDD && (N & (N - 1)) == 0 && N >= 256 && N <= 4096) return kFFT;
     if (pair == kPairPP && (n & 1)) return -1;   // periodic transforms need an even length
     if (n <= kDenseMax) return kDense;   // any pair: periodic-table dense transform
+    if (n <= kSepMax) return kSep;       // any length: Stockham / Bluestein passes + sweeps
     return -1;
 }
 
 int rows_per_block(int n, int pair) {
     const int N = n + 1;
     if (transform_kind(n, pair) == kFFT) return N >= 4096 ? 8 : 16;
+    if (transform_kind(n, pair) == kSep) return 32;
     // one group per carry block: more CTAs for the small dense solves
     return n <= 160 ? DenseDstT<1, 160, 4>::G : DenseDstT<1, 256>::G;
 }
@@ -617,6 +791,11 @@ void launch_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
         if (j.p.n != n) FD_FAIL(FD_ERR_VALIDATION, "launch_solve: mixed transform lengths in one batch");
     for (auto &j : jobs)
         if (j.p.tpair != jobs[0].p.tpair) FD_FAIL(FD_ERR_VALIDATION, "launch_solve: mixed transform pairs in one batch");
+    if (jobs[0].p.tkind == kSep) {
+        if (!jobs[0].ws) FD_FAIL(FD_ERR_VALIDATION, "launch_solve: separate-transform solve needs plan scratch");
+        run_sep(jobs, s);
+        return;
+    }
     if (jobs[0].p.dense) {
         if (n <= 128) run_solve<DenseDstT<1, 128, 4>>(jobs, s);
         else if (n <= 160) run_solve<DenseDstT<1, 160, 4>>(jobs, s);
@@ -655,6 +834,10 @@ static void run_dense_rows(int rows, int n, int pair, int inverse, const double 
 void launch_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out,
                            const double *dense, cudaStream_t s) {
     if (rows <= 0) return;
+    if (transform_kind(n, pair) == kSep) {
+        transform_rows_any(rows, n, pair, inverse, in, out, 1.0, 0.0, nullptr, s);
+        return;
+    }
     if (!dense) FD_FAIL(FD_ERR_UNSUPPORTED, "no dense table for this transform");
     if (n <= 128) run_dense_rows<DenseDstT<1, 128>>(rows, n, pair, inverse, in, out, dense, s);
     else if (n <= 160) run_dense_rows<DenseDstT<1, 160>>(rows, n, pair, inverse, in, out, dense, s);
@@ -667,6 +850,10 @@ void launch_transform_rows(int rows, int n, int pair, int inverse, const double 
 void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,
                      const double *dense, cudaStream_t s) {
     if (rows <= 0) return;
+    if (transform_kind(n) == kSep) {
+        transform_rows_any(rows, n, kPairDD, 0, in, out, 1.0, 0.0, nullptr, s);
+        return;
+    }
     if (transform_kind(n) == kDense) {
         if (n <= 128) run_dst<DenseDstT<1, 128>>(rows, n, in, out, tw, dense, s);
         else if (n <= 160) run_dst<DenseDstT<1, 160>>(rows, n, in, out, tw, dense, s);

@@ -50,12 +50,17 @@ def _gpu_axis(sub: RectSubdomain) -> str:
         lo, hi = ("south", "north") if axis == "y" else ("west", "east")
         return pair == "DD" and not sub.end_modifier(lo) and not sub.end_modifier(hi)
 
-    def has_kernel(axis):
+    # kernel ranking: the fused FFT solve, then the dense-table solve, then the
+    # any-length (Stockham / Bluestein) passes; none
+    rank_of = {1: 3, 0: 2, 2: 1}
+
+    def rank(axis):
         length = sub.n if axis == "y" else sub.m
-        return _native.lib().fd_transform_kind_pair(int(length), _PAIR_CODE[pair_of(axis)]) >= 0
+        return rank_of.get(_native.lib().fd_transform_kind_pair(int(length), _PAIR_CODE[pair_of(axis)]), 0)
 
     y_ok, x_ok = ok("y"), ok("x")
-    if y_ok and (has_kernel("y") or not (x_ok and has_kernel("x"))):
+    # the reference prefers y (rectsolver.py:102-109); x only for a strictly faster kernel
+    if y_ok and (not x_ok or rank("y") >= rank("x")):
         axis = "y"
     elif x_ok:
         axis = "x"
@@ -139,7 +144,7 @@ class RectPlan:
         _native.call("fd_plan_info", self.handle.ptr, ctypes.byref(br), ctypes.byref(ex),
                      ctypes.byref(tk))
         return {"block_rows": br.value, "explicit_rows": ex.value,
-                "transform": ("dense", "fft")[tk.value]}
+                "transform": ("dense", "fft", "sep")[tk.value]}
 
 
 def _sweep_matrix(lam_k: float, ms: int, off: float, cyclic: bool, mod_lo: float, mod_hi: float):

@@ -1,11 +1,13 @@
 """Eigenbasis transforms of the 1-D axis operators (ref fftddm/transforms.py).
 
 `eigenvalues`/`make_plan` are host-side setup (O(n)).  `apply_Q`/`apply_Qt`
-for the Dirichlet-Dirichlet pair run the sm_100a DST-I kernel (Q = Q^T =
-sqrt(2/(n+1)) DST-I, transforms.py:112-113,135-136) on torch CUDA tensors;
-numpy input is copied to the device and the result back.  NN (DCT-II/III)
-and PP (real Fourier) run on the dense periodic-table transform (n <= 2048,
-PP even n); other lengths raise UnsupportedError.
+run on torch CUDA tensors (numpy input is copied to the device and the result
+back) for every length: the DD pair (Q = Q^T = sqrt(2/(n+1)) DST-I,
+transforms.py:112-113,135-136) on the real-symmetric FFT kernel when n + 1 is
+a power of two in [256, 4096], on the dense periodic-table transform for
+n <= 2048, otherwise on the any-length passes (power-of-two Stockham or
+Bluestein, csrc/fft_any.cu); NN (DCT-II/III) and PP (real Fourier, even n)
+likewise (dense table up to 2048, any-length passes above).
 """
 
 from __future__ import annotations
