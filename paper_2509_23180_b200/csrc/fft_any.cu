@@ -13,12 +13,13 @@
 //   PP   Q^T: F = FFT_n(v), cosine / sine amplitudes (transforms.py:139-148)
 //        Q:   half spectrum -> inverse DFT (transforms.py:114-126)
 //
-// The complex DFT of length M: power-of-two M by radix-4/2 Stockham passes in
-// shared memory (M <= 4096 in one pass over the row; larger M as a four-step
-// P1 x P2 split, lines staged through shared memory several at a time so the
-// strided accesses coalesce); any other M by Bluestein's chirp-z
-// (X_k = w_k sum_j (x_j w_j) conj(w_{k-j}), w_j = e^{-i pi j^2 / M}) as a
-// power-of-two cyclic convolution of length P >= 2M - 1.
+// The complex DFT of length M: 7-smooth M by mixed-radix (4, 2, 3, 5, 7)
+// Stockham passes in shared memory (M <= 4096 in one kernel over the row;
+// larger M as a four-step P1 x P2 split, lines staged through shared memory
+// several at a time so the strided accesses coalesce); any other M by
+// Bluestein's chirp-z (X_k = w_k sum_j (x_j w_j) conj(w_{k-j}),
+// w_j = e^{-i pi j^2 / M}) as a power-of-two cyclic convolution of length
+// P >= 2M - 1.
 #include <math.h>
 
 #include <map>
@@ -46,6 +47,8 @@ struct Lines {
     const double2 *post;         // optional W_P^j, j < P: output (l, k) times W_P^{l k}
     int P;
     int inverse;                 // conjugate twiddles (e^{+2 pi i jk/L}), unnormalised
+    int nfac;                    // radix sequence of L (4, 2, 3, 5, 7), product L
+    int fac[24];
 };
 
 constexpr int kFftThreads = 256;
@@ -56,9 +59,75 @@ __device__ __forceinline__ double2 twv(const double2 *tw, int idx, int inverse) 
     return make_double2(w.x, inverse ? -w.y : w.y);
 }
 
-// LB lines of length L per CTA; Stockham radix-4 passes, one radix-2 pass when
-// log2(L) is odd; natural-order output
-__global__ void __launch_bounds__(kFftThreads) fft_lines_kernel(Lines s) {
+// in-place R-point DFT (R = 2, 3, 4, 5, 7) with roots e^{-+2 pi i / R}
+template <int R>
+__device__ __forceinline__ void small_dft(double2 (&v)[7], int inverse) {
+    if constexpr (R == 2) {
+        const double2 a = v[0];
+        v[0] = cadd(a, v[1]);
+        v[1] = csub(a, v[1]);
+    } else if constexpr (R == 4) {
+        const double2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]), s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
+        const double2 rd13 = inverse ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);
+        v[0] = cadd(s02, s13);
+        v[1] = cadd(d02, rd13);
+        v[2] = csub(s02, s13);
+        v[3] = csub(d02, rd13);
+    } else {
+        // cos / sin (2 pi m / R), m < R
+        constexpr double c3[3] = {1.0, -0.5, -0.5}, s3[3] = {0.0, 0.8660254037844386467637, -0.8660254037844386467637};
+        constexpr double c5[5] = {1.0, 0.3090169943749474241023, -0.8090169943749474241023, -0.8090169943749474241023,
+                                  0.3090169943749474241023};
+        constexpr double s5[5] = {0.0, 0.9510565162951535721164, 0.5877852522924731291687, -0.5877852522924731291687,
+                                  -0.9510565162951535721164};
+        constexpr double c7[7] = {1.0, 0.623489801858733530525, -0.2225209339563144042889, -0.9009688679024191262361,
+                                  -0.9009688679024191262361, -0.2225209339563144042889, 0.623489801858733530525};
+        constexpr double s7[7] = {0.0, 0.7818314824680298087084, 0.9749279121818236070181, 0.4338837391175581204758,
+                                  -0.4338837391175581204758, -0.9749279121818236070181, -0.7818314824680298087084};
+        double2 o[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            double2 acc = v[0];
+#pragma unroll
+            for (int j = 1; j < R; ++j) {
+                const int mm = (j * k) % R;
+                const double cs = R == 3 ? c3[mm] : R == 5 ? c5[mm] : c7[mm];
+                const double sn = R == 3 ? s3[mm] : R == 5 ? s5[mm] : s7[mm];
+                acc = cadd(acc, cmul(v[j], make_double2(cs, inverse ? sn : -sn)));
+            }
+            o[k] = acc;
+        }
+#pragma unroll
+        for (int k = 0; k < R; ++k) v[k] = o[k];
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void stockham_pass(const Lines &s, const double2 *x, double2 *y, int nl, int Ns) {
+    const int L = s.L, span = L / R;
+    for (int q = threadIdx.x; q < nl * span; q += kFftThreads) {
+        const int li = q / span, j = q % span;
+        const double2 *xl = x + li * L;
+        double2 *yl = y + li * L;
+        double2 v[7];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = xl[j + r * span];
+        const int k = j % Ns;
+        if (k) {
+            const int step = L / (R * Ns);   // e^{-2 pi i k r / (R Ns)} = W_L^{k r step}
+#pragma unroll
+            for (int r = 1; r < R; ++r) v[r] = cmul(v[r], twv(s.tw, (k * r * step) % L, s.inverse));
+        }
+        small_dft<R>(v, s.inverse);
+        const int o = (j / Ns) * Ns * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) yl[o + r * Ns] = v[r];
+    }
+}
+
+// LB lines of length L per CTA, one Stockham pass per radix of L (natural-order
+// output, ping-pong buffers in shared memory)
+__global__ void __launch_bounds__(kFftThreads) fft_lines_kernel(const __grid_constant__ Lines s) {
     extern __shared__ __align__(16) double2 fsm[];
     const int L = s.L;
     const int LB = max(1, min(kFftSmemC / 2 / L, 32));
@@ -79,47 +148,15 @@ __global__ void __launch_bounds__(kFftThreads) fft_lines_kernel(Lines s) {
     }
     __syncthreads();
     int Ns = 1;
-    for (; Ns * 4 <= L; Ns *= 4) {   // radix 4
-        const int quarter = L / 4;
-        for (int q = threadIdx.x; q < nl * quarter; q += kFftThreads) {
-            const int li = q / quarter, j = q % quarter;
-            const double2 *xl = x + li * L;
-            double2 *yl = y + li * L;
-            double2 v0 = xl[j], v1 = xl[j + quarter], v2 = xl[j + 2 * quarter], v3 = xl[j + 3 * quarter];
-            const int k = j % Ns;
-            const int step = L / (4 * Ns);   // twiddle e^{-2 pi i k r / (4 Ns)} = W_L^{k r step}
-            if (k) {
-                v1 = cmul(v1, twv(s.tw, (k * step) % L, s.inverse));
-                v2 = cmul(v2, twv(s.tw, (2 * k * step) % L, s.inverse));
-                v3 = cmul(v3, twv(s.tw, (3 * k * step) % L, s.inverse));
-            }
-            // 4-point DFT (inverse: conjugate the -i rotations)
-            const double2 s02 = cadd(v0, v2), d02 = csub(v0, v2), s13 = cadd(v1, v3), d13 = csub(v1, v3);
-            const double2 rd13 = s.inverse ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);
-            const int o = (j / Ns) * Ns * 4 + k;
-            yl[o] = cadd(s02, s13);
-            yl[o + Ns] = cadd(d02, rd13);
-            yl[o + 2 * Ns] = csub(s02, s13);
-            yl[o + 3 * Ns] = csub(d02, rd13);
+    for (int f = 0; f < s.nfac; ++f) {
+        switch (s.fac[f]) {
+            case 4: stockham_pass<4>(s, x, y, nl, Ns); break;
+            case 2: stockham_pass<2>(s, x, y, nl, Ns); break;
+            case 3: stockham_pass<3>(s, x, y, nl, Ns); break;
+            case 5: stockham_pass<5>(s, x, y, nl, Ns); break;
+            default: stockham_pass<7>(s, x, y, nl, Ns); break;
         }
-        __syncthreads();
-        double2 *t = x;
-        x = y;
-        y = t;
-    }
-    if (Ns < L) {   // radix 2
-        const int half = L / 2;
-        for (int q = threadIdx.x; q < nl * half; q += kFftThreads) {
-            const int li = q / half, j = q % half;
-            const double2 *xl = x + li * L;
-            double2 *yl = y + li * L;
-            double2 a = xl[j], b = xl[j + half];
-            const int k = j % Ns;
-            if (k) b = cmul(b, twv(s.tw, (k * (L / (2 * Ns))) % L, s.inverse));
-            const int o = (j / Ns) * Ns * 2 + k;
-            yl[o] = cadd(a, b);
-            yl[o + Ns] = csub(a, b);
-        }
+        Ns *= s.fac[f];
         __syncthreads();
         double2 *t = x;
         x = y;
@@ -132,6 +169,18 @@ __global__ void __launch_bounds__(kFftThreads) fft_lines_kernel(Lines s) {
         if (s.post) v = cmul(v, twv(s.post, int((long long)(l0 + li) * e % s.P), s.inverse));
         out[(l0 + li) * s.out_ls + e * s.out_es] = v;
     }
+}
+
+// radix sequence of L (4s first, then 2, 3, 5, 7); false unless L is 7-smooth
+static bool factor_smooth(int L, Lines &s) {
+    s.nfac = 0;
+    int v = L;
+    for (int r : {4, 2, 3, 5, 7})
+        while (v % r == 0 && s.nfac < 24) {
+            s.fac[s.nfac++] = r;
+            v /= r;
+        }
+    return v == 1;
 }
 
 static size_t lines_smem() { return size_t(kFftSmemC) * sizeof(double2); }
@@ -155,7 +204,7 @@ static void run_lines(const Lines &s, cudaStream_t st) {
 static std::mutex g_any_mu;
 static std::map<std::pair<int, int>, double2 *> g_pow2_tw;   // (device, P) -> W_P^k
 
-static const double2 *pow2_twiddles(int device, int P) {
+static const double2 *pow2_twiddles(int device, int P) {   // W_P^k, k < P (any P)
     std::lock_guard<std::mutex> g(g_any_mu);
     auto key = std::make_pair(device, P);
     auto it = g_pow2_tw.find(key);
@@ -178,17 +227,31 @@ static int ilog2(long long v) {
     return l;
 }
 
-// rows x P (row stride P) power-of-two DFT, in -> out (out may equal in for
-// P <= 4096; the four-step split goes through `tmp`, rows x P)
-static void fft_pow2(long long rows, int P, const double2 *in, double2 *out, double2 *tmp, int inverse,
-                     cudaStream_t st, int device) {
-    const int lp = ilog2(P);
-    if (lp <= 12) {
+// M = P1 * P2 with both factors <= 4096 (any such split of a 7-smooth M),
+// P1 the smallest factor >= sqrt(M); false when there is none
+static bool smooth_split(int M, int &P1, int &P2) {
+    Lines t{};
+    if (!factor_smooth(M, t)) return false;
+    for (int a = 1; a <= 4096; ++a) {
+        if (M % a || (long long)a * a < M) continue;
+        if (M / a <= 4096) {
+            P1 = a;
+            P2 = M / a;
+            return true;
+        }
+    }
+    return false;
+}
+
+// rows x P (row stride P) DFT of a 7-smooth length P, in -> out (out may equal
+// in for P <= 4096; the four-step split goes through `tmp`, rows x P)
+static void fft_smooth(long long rows, int P, const double2 *in, double2 *out, double2 *tmp, int inverse,
+                       cudaStream_t st, int device) {
+    if (P <= 4096) {
         Lines s{};
         s.in = in;
         s.out = out;
         s.L = P;
-        s.logL = lp;
         s.lines = 1;
         s.rows = rows;
         s.in_row = s.out_row = P;
@@ -196,18 +259,18 @@ static void fft_pow2(long long rows, int P, const double2 *in, double2 *out, dou
         s.in_es = s.out_es = 1;
         s.tw = pow2_twiddles(device, P);
         s.inverse = inverse;
+        if (!factor_smooth(P, s)) FD_FAIL(FD_ERR_UNSUPPORTED, "fft: length is not 7-smooth");
         run_lines(s, st);
         return;
     }
-    if (lp > 18) FD_FAIL(FD_ERR_UNSUPPORTED, "fft: length above 2^18");
-    // four-step: n = n1 * P2 + n2 ... x[n2 + P2 n1]; k = k1 + P1 k2
-    const int P1 = 1 << ((lp + 1) / 2), P2 = P / P1;
-    // A: for each n2, FFT over n1 (stride P2) -> times W_P^{n2 k1} -> tmp[k1 * P2 + n2]
+    int P1 = 0, P2 = 0;
+    if (!smooth_split(P, P1, P2)) FD_FAIL(FD_ERR_UNSUPPORTED, "fft: no four-step split of this length");
+    // four-step: x[n2 + P2 n1], X[k1 + P1 k2]
+    // A: for each n2, DFT over n1 (stride P2), times W_P^{n2 k1} -> tmp[k1 * P2 + n2]
     Lines a{};
     a.in = in;
     a.out = tmp;
     a.L = P1;
-    a.logL = ilog2(P1);
     a.lines = P2;
     a.rows = rows;
     a.in_row = a.out_row = P;
@@ -219,13 +282,13 @@ static void fft_pow2(long long rows, int P, const double2 *in, double2 *out, dou
     a.post = pow2_twiddles(device, P);
     a.P = P;
     a.inverse = inverse;
+    factor_smooth(P1, a);
     run_lines(a, st);
-    // B: for each k1, FFT over n2 (contiguous in tmp) -> out[k1 + P1 k2]
+    // B: for each k1, DFT over n2 (contiguous in tmp) -> out[k1 + P1 k2]
     Lines b{};
     b.in = tmp;
     b.out = out;
     b.L = P2;
-    b.logL = ilog2(P2);
     b.lines = P1;
     b.rows = rows;
     b.in_row = b.out_row = P;
@@ -235,7 +298,13 @@ static void fft_pow2(long long rows, int P, const double2 *in, double2 *out, dou
     b.out_es = P1;
     b.tw = pow2_twiddles(device, P2);
     b.inverse = inverse;
+    factor_smooth(P2, b);
     run_lines(b, st);
+}
+static void fft_pow2(long long rows, int P, const double2 *in, double2 *out, double2 *tmp, int inverse,
+                     cudaStream_t st, int device) {
+    if (P > (1 << 18)) FD_FAIL(FD_ERR_UNSUPPORTED, "fft: length above 2^18");
+    fft_smooth(rows, P, in, out, tmp, inverse, st, device);
 }
 
 // Bluestein data of a length M: chirp w_j = e^{-i pi j^2 / M} (j < M) and the
@@ -329,12 +398,14 @@ void dft_rows(long long rows, int M, const double2 *in, double2 *out, int invers
     if (rows <= 0) return;
     int device = 0;
     FD_CUDA(cudaGetDevice(&device));
-    if ((M & (M - 1)) == 0) {
+    int P1 = 0, P2 = 0;
+    if (M <= 4096 ? [&] { Lines t{}; return factor_smooth(M, t); }() : smooth_split(M, P1, P2)) {
+        // 7-smooth: mixed-radix Stockham passes (four-step above 4096)
         const long long chunk = std::max<long long>(1, kDftChunk / M);
         double2 *tmp = M > 4096 ? any_scratch(device, size_t(std::min(rows, chunk)) * M) : nullptr;
         for (long long r0 = 0; r0 < rows; r0 += chunk) {
             const long long rr = std::min(chunk, rows - r0);
-            fft_pow2(rr, M, in + r0 * M, out + r0 * M, tmp, inverse, st, device);
+            fft_smooth(rr, M, in + r0 * M, out + r0 * M, tmp, inverse, st, device);
         }
         return;
     }

@@ -748,9 +748,13 @@ class TestAnyLength:
     Stockham or Bluestein DFT passes + the separate-transform sweeps, for every
     pair, against the oracle (reference transforms.py:74-148 formulations)."""
 
+    # DFT length M = 2(n+1) (DD), 2n (NN), n (PP): Bluestein for 2049 / 3000 /
+    # 5000 / 5003 / 5002, power-of-two four-step for 8191 / 16383 / NN 4096,
+    # mixed-radix four-step for DD 4999 (10000) and NN 2100 (4200), mixed-radix
+    # single pass for PP 3000, 2430 (radix 3s and 5s), 2100 (radix 7)
     LENGTHS = [("DD", 2049), ("DD", 3000), ("DD", 5000), ("DD", 8191), ("DD", 16383), ("DD", 4999),
-               ("NN", 2049), ("NN", 3000), ("NN", 4096), ("NN", 5003),
-               ("PP", 2050), ("PP", 3000), ("PP", 4096), ("PP", 5002)]
+               ("NN", 2049), ("NN", 3000), ("NN", 4096), ("NN", 5003), ("NN", 2100),
+               ("PP", 2050), ("PP", 3000), ("PP", 4096), ("PP", 5002), ("PP", 2430), ("PP", 2100)]
 
     @pytest.mark.parametrize("bc,n", LENGTHS)
     def test_q_and_qt(self, bc, n, rng):
