@@ -324,6 +324,44 @@ def golden_ref(name):
     return ref
 
 
+def sharded_solves(dev, world, rank, names=("c3", "c4")):
+    """Algorithm 1 sharded over the `world` ranks (one process per GPU; native
+    fd_ddm_solve_dist over an NCCL communicator: rank 0 centre + GMRES, arms
+    dealt to ranks 1..world-1).  Device time (CUDA events on each
+    rank's stream, max over ranks) of one solve after a warm-up solve."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_23180_b200 import configs, krylov
+    from paper_2509_23180_b200 import dist as pdist
+
+    comm = pdist.nccl_comm()
+    cfg = krylov.GmresConfig(m=50, tol=1e-10)
+    out = {}
+    for name in names:
+        comp, f, _, meta = configs.build_cross_case(name, device=(name == "c4"))
+        fd = {k: (v if hasattr(v, "device") else torch.as_tensor(v, device=dev)) for k, v in f.items()}
+        del f
+        pdist.sharded_ddm_solve(comp, fd, comm, cfg)   # plans, basis, NCCL channels
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fields, rep = pdist.sharded_ddm_solve(comp, fd, comm, cfg)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        it = torch.tensor([rep.iterations if rep else 0], device=dev)
+        dist.all_reduce(it, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+        out[name] = {"points": meta["points"], "iterations": int(it.item()), "wall_s": wall,
+                     "value": meta["points"] / wall, "unit": "grid_points/s", "ranks": world,
+                     "layout": "rank 0: centre + GMRES; arms round-robin on ranks 1..N-1 (NCCL send/recv of interface lines)"}
+        del fields, fd
+    return out
+
+
 def run_gpu(args, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -464,7 +502,7 @@ def run_gpu(args, world, rank, local):
     solve = None
     if not args.no_solve:
         try:
-            solve = full_solve(dev)
+            solve = full_solve(dev) if world == 1 else sharded_solves(dev, world, rank)
         except Exception as exc:   # the apply line must still print
             solve = {"error": f"{type(exc).__name__}: {exc}"}
 

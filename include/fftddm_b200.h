@@ -37,6 +37,7 @@ extern "C" {
 
 typedef struct fd_plan_s *fd_plan;
 typedef struct fd_schur_s *fd_schur;
+typedef struct fd_comm_s *fd_comm;
 
 /* GMRES report; replaces krylov.SolveReport (krylov.py:52-58). */
 typedef struct {
@@ -215,6 +216,29 @@ int fd_axpby(int N, double a, const double *x, double b, const double *y, double
 /* host result: ||x||_2 with the library's deterministic reduction order */
 int fd_norm(int N, const double *x, double *result, void *stream);
 int fd_dot(int N, const double *x, const double *y, double *result, void *stream);
+
+/* --- subdomain-sharded solve (replaces the reference's thread
+ * pool over neighbour solves, ddm.py:112-123,241-261, by one process per GPU).
+ * fd_comm_unique_id: 128-byte NCCL id on rank 0 (broadcast it out of band);
+ * fd_comm_init: NCCL communicator of this rank over NVLink/NVSwitch (libnccl
+ * opened at run time).  fd_comm_init_loopback: nranks in-process ranks (host
+ * threads) on one device, the test transport of the protocol. */
+int fd_comm_unique_id(char *id128);
+int fd_comm_init(fd_comm *out, int nranks, int rank, const char *id128, int device);
+int fd_comm_init_loopback(fd_comm *outs, int nranks, int device);
+int fd_comm_rank(fd_comm comm, int *rank, int *nranks);
+int fd_comm_destroy(fd_comm comm);
+/* Attach a communicator to an operator built identically on every rank:
+ * owner[i] = rank that solves neighbour i (rank 0 holds the centre). */
+int fd_schur_set_comm(fd_schur op, fd_comm comm, const int *owner);
+/* fd_ddm_solve over the ranks: every rank calls it; rank 0 runs GMRES and
+ * drives the interface-line exchange of each operator application (two
+ * point-to-point messages of <= 32 KB per remote arm), arm owners pre-solve,
+ * serve the applies and back-substitute their own fields.  f_nb / p_nb are
+ * read / written for owned arms only; rep / history are filled on rank 0. */
+int fd_ddm_solve_dist(fd_schur op, const double *f_center, const double *const *f_nb, double *p_center,
+                      double *const *p_nb, int m, double tol, int max_restarts, double *history,
+                      int hist_cap, fd_report *rep, void *stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

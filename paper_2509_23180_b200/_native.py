@@ -29,6 +29,8 @@ EXPORTS = (
     "fd_transform_rows", "fd_assemble_rhs", "fd_stencil_apply", "fd_stencil_apply_ex", "fd_schur_create", "fd_schur_destroy", "fd_schur_apply",
     "fd_center_solve", "fd_precond_apply", "fd_unprecond_apply", "fd_gmres_precond",
     "fd_ddm_solve", "fd_schur_set_steklov", "fd_schur_use_steklov", "fd_arnoldi_step", "fd_basis_update", "fd_axpby", "fd_norm", "fd_dot",
+    "fd_comm_unique_id", "fd_comm_init", "fd_comm_init_loopback", "fd_comm_rank", "fd_comm_destroy",
+    "fd_schur_set_comm", "fd_ddm_solve_dist",
 )
 
 
@@ -91,6 +93,14 @@ def _declare(lib):
         "fd_axpby": (I, [I, D, P, D, P, P, P]),
         "fd_norm": (I, [I, P, DP, P]),
         "fd_dot": (I, [I, P, P, DP, P]),
+        "fd_comm_unique_id": (I, [ctypes.c_char_p]),
+        "fd_comm_init": (I, [ctypes.POINTER(P), I, I, ctypes.c_char_p, I]),
+        "fd_comm_init_loopback": (I, [ctypes.POINTER(P), I, I]),
+        "fd_comm_rank": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I)]),
+        "fd_comm_destroy": (I, [P]),
+        "fd_schur_set_comm": (I, [P, P, ctypes.POINTER(I)]),
+        "fd_ddm_solve_dist": (I, [P, P, ctypes.POINTER(P), P, ctypes.POINTER(P), I, D, I, DP, I,
+                                  ctypes.POINTER(FdReport), P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

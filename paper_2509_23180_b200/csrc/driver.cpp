@@ -231,7 +231,18 @@ struct fd_schur_s {
     cudaStream_t gstream = nullptr;
     double *gin = nullptr;
     double *lines = nullptr, *lines_hat = nullptr;
+    // sharded solve: arm i is solved on rank owner[i]; rank 0 holds
+    // the centre, the Krylov basis and drives the protocol; every rank holds
+    // the same operator object (plans, couplings, work fields of its arms)
+    fd_comm_s *comm = nullptr;
+    std::vector<int> owner;
+    int64_t *iota = nullptr;                  // 0 .. max line length - 1
+    std::vector<double *> sline, rline;       // per arm: line out / line back (device)
+    long long *cmd = nullptr;                 // device command word
+    long long *cmd_host = nullptr;            // pinned mirror
     std::vector<void *> allocs;
+    bool remote(size_t i) const { return comm && owner[i] != comm->t->rank; }
+    bool dist() const { return comm && comm->t->nranks > 1; }
 };
 
 namespace fd {
@@ -373,12 +384,70 @@ static void schur_apply_steklov(fd_schur_s *op, const double *p, double *out, bo
     scatter_add_parts(op, from, src, out, s);
 }
 
+// command words of the sharded protocol (rank 0 -> arm owners)
+enum : long long { kCmdDone = 0, kCmdApply = 1, kCmdBacksub = 2 };
+
+static void send_command(fd_schur_s *op, long long cmd, cudaStream_t s) {
+    Transport &t = *op->comm->t;
+    *op->cmd_host = cmd;
+    FD_CUDA(cudaMemcpyAsync(op->cmd, op->cmd_host, sizeof(long long), cudaMemcpyHostToDevice, s));
+    t.group_start();
+    for (int r = 1; r < t.nranks; ++r) t.send(op->cmd, sizeof(long long), r, s);
+    t.group_end();
+    // the pinned word is rewritten by the next command: wait for this copy
+    FD_CUDA(cudaStreamSynchronize(s));
+}
+
+// rank 0: R_ic lines of the remote arms to their owners (c_ic p[from])
+static void send_lines(fd_schur_s *op, const double *p, cudaStream_t s) {
+    Transport &t = *op->comm->t;
+    for (size_t i = 0; i < op->nb.size(); ++i)
+        if (op->remote(i)) {
+            const Coupling &c = op->from_c[i];
+            launch_scatter(c.len, c.from, op->iota, c.c, p, op->sline[i], 0, s);
+        }
+    t.group_start();
+    for (size_t i = 0; i < op->nb.size(); ++i)
+        if (op->remote(i)) t.send(op->sline[i], sizeof(double) * op->from_c[i].len, op->owner[i], s);
+    t.group_end();
+}
+
 // out = sum_i R_ci A_i^{-1} R_ic p   (ddm.py:108-123).  The neighbour inputs
 // stay zero between applies: the interface lines are gathered in (one launch),
-// solved out of place and cleared again (one launch).
+// solved out of place and cleared again (one launch).  Sharded: the remote
+// arms' lines go to their owners first, the local arms are solved meanwhile,
+// and the returned R_ci lines are added in neighbour order with the local ones.
 static void schur_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s, bool out_zero = false) {
     if (op->steklov) {
         schur_apply_steklov(op, p, out, out_zero, s);
+        return;
+    }
+    if (op->dist()) {
+        Transport &t = *op->comm->t;
+        send_command(op, kCmdApply, s);
+        send_lines(op, p, s);
+        std::vector<SolveJob> jobs;
+        for (size_t i = 0; i < op->nb.size(); ++i) {
+            if (op->remote(i)) continue;
+            const Coupling &c = op->from_c[i];
+            launch_scatter(c.len, c.from, c.to, c.c, p, op->nbin[i], 0, s);
+            jobs.push_back(job_of(op->nb[i], op->nbin[i], op->nbf[i]));
+        }
+        if (!jobs.empty()) solve_batch(jobs, s);
+        for (size_t i = 0; i < op->nb.size(); ++i)
+            if (!op->remote(i)) launch_zero_at(op->from_c[i].len, op->from_c[i].to, op->nbin[i], s);
+        t.group_start();
+        for (size_t i = 0; i < op->nb.size(); ++i)
+            if (op->remote(i)) t.recv(op->rline[i], sizeof(double) * op->to_c[i].len, op->owner[i], s);
+        t.group_end();
+        const Plan *cp = op->center;
+        if (!out_zero) FD_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * cp->m * cp->n, s));
+        // R_ci parts in neighbour order (remote parts arrive already scaled by c_ci)
+        for (size_t i = 0; i < op->nb.size(); ++i) {
+            const Coupling &c = op->to_c[i];
+            if (op->remote(i)) launch_scatter(c.len, op->iota, c.to, 1.0, op->rline[i], out, 1, s);
+            else launch_scatter(c.len, c.from, c.to, c.c, op->nbf[i], out, 1, s);
+        }
         return;
     }
     const size_t nnb = op->nb.size();
@@ -459,7 +528,7 @@ static void drop_graph(fd_schur_s *op) {
 static void precond_apply_loop(fd_schur_s *op, const double *p, cudaStream_t s) {
     const long long N = (long long)op->center->m * op->center->n;
     if (op->graph_state == 0) {
-        bool ok = N <= (1LL << 18) && op->center->transform == kDense;
+        bool ok = N <= (1LL << 18) && op->center->transform == kDense && !op->dist();
         for (const Plan *q : op->nb) ok = ok && (op->steklov || q->transform == kDense);
         op->graph_state = ok ? 2 : -1;
         precond_apply(op, p, op->w, s);
@@ -1151,6 +1220,180 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
             launch_axpby((long long)q->m * q->n, 1.0, p_nb[i], -1.0, op->nbf[i], p_nb[i], s);
     }
     ht.mark("residual+backsub", s);
+    if (st != FD_OK) {
+        std::ostringstream os;
+        os << "GMRES did not reach tol=" << tol << " in " << rep->iterations << " iterations";
+        FD_FAIL(st, os.str());
+    }
+    FD_API_END
+}
+
+int fd_schur_set_comm(fd_schur op, fd_comm comm, const int *owner) {
+    FD_API_BEGIN
+    if (!op || !comm || !owner) FD_FAIL(FD_ERR_VALIDATION, "null argument");
+    const int nr = comm->t->nranks;
+    FD_CUDA(cudaSetDevice(op->device));
+    op->owner.assign(owner, owner + op->nb.size());
+    for (int o : op->owner)
+        if (o < 0 || o >= nr) FD_FAIL(FD_ERR_VALIDATION, "arm owner outside the communicator");
+    int lmax = 1;
+    for (size_t i = 0; i < op->nb.size(); ++i) lmax = std::max(lmax, std::max(op->from_c[i].len, op->to_c[i].len));
+    if (!op->iota) {
+        std::vector<int64_t> h(lmax);
+        for (int t = 0; t < lmax; ++t) h[t] = t;
+        op->iota = (int64_t *)dalloc(op, sizeof(int64_t) * lmax);
+        FD_CUDA(cudaMemcpy(op->iota, h.data(), sizeof(int64_t) * lmax, cudaMemcpyHostToDevice));
+        for (size_t i = 0; i < op->nb.size(); ++i) {
+            op->sline.push_back((double *)dalloc(op, sizeof(double) * lmax));
+            op->rline.push_back((double *)dalloc(op, sizeof(double) * lmax));
+        }
+        op->cmd = (long long *)dalloc(op, sizeof(long long));
+        op->cmd_host = (long long *)pinned_get(sizeof(long long));
+    }
+    op->comm = comm;
+    drop_graph(op);
+    FD_API_END
+}
+
+// Algorithm 1 sharded over the communicator's ranks: rank 0 owns
+// the centre, runs GMRES and drives every operator application; an arm owner
+// pre-solves its arms, then serves commands (apply: solve the received R_ic
+// line and return R_ci of the result; back-substitution: finish its fields).
+// Arguments as fd_ddm_solve; on rank r only the owned arms' f_nb / p_nb (and
+// on rank 0 f_center / p_center) are read or written.
+int fd_ddm_solve_dist(fd_schur op, const double *f_center, const double *const *f_nb, double *p_center,
+                      double *const *p_nb, int m, double tol, int max_restarts, double *history, int hist_cap,
+                      fd_report *rep, void *stream) {
+    FD_API_BEGIN
+    if (!op || !rep || !op->comm) FD_FAIL(FD_ERR_VALIDATION, "sharded solve: operator without communicator");
+    cudaStream_t s = S(stream);
+    Transport &t = *op->comm->t;
+    const int rank = t.rank;
+    const size_t nnb = op->nb.size();
+    memset(rep, 0, sizeof(*rep));
+    // pre-solves q_i = A_i^{-1} f_i of the owned arms (ddm.py:249-250)
+    std::vector<UJob> ujobs;
+    for (size_t i = 0; i < nnb; ++i)
+        if (!op->remote(i)) {
+            if (!f_nb[i] || !p_nb[i]) FD_FAIL(FD_ERR_VALIDATION, "sharded solve: owned arm without fields");
+            ujobs.push_back(UJob{op->nb[i], f_nb[i], p_nb[i]});
+        }
+    solve_user(ujobs, s);
+    if (rank != 0) {
+        // R_ci q_i lines to rank 0, then serve commands
+        t.group_start();
+        for (size_t i = 0; i < nnb; ++i)
+            if (!op->remote(i)) {
+                const Coupling &c = op->to_c[i];
+                launch_scatter(c.len, c.from_user, op->iota, c.c, p_nb[i], op->sline[i], 0, s);
+                t.send(op->sline[i], sizeof(double) * c.len, 0, s);
+            }
+        t.group_end();
+        for (;;) {
+            t.recv(op->cmd, sizeof(long long), 0, s);
+            FD_CUDA(cudaMemcpyAsync(op->cmd_host, op->cmd, sizeof(long long), cudaMemcpyDeviceToHost, s));
+            FD_CUDA(cudaStreamSynchronize(s));
+            const long long cmd = *op->cmd_host;
+            if (cmd == kCmdDone) break;
+            std::vector<SolveJob> jobs;
+            t.group_start();
+            for (size_t i = 0; i < nnb; ++i)
+                if (!op->remote(i)) t.recv(op->rline[i], sizeof(double) * op->from_c[i].len, 0, s);
+            t.group_end();
+            for (size_t i = 0; i < nnb; ++i)
+                if (!op->remote(i)) {
+                    const Coupling &c = op->from_c[i];
+                    launch_scatter(c.len, op->iota, c.to, 1.0, op->rline[i], op->nbin[i], 0, s);
+                    jobs.push_back(job_of(op->nb[i], op->nbin[i], op->nbf[i]));
+                }
+            solve_batch(jobs, s);
+            for (size_t i = 0; i < nnb; ++i)
+                if (!op->remote(i)) launch_zero_at(op->from_c[i].len, op->from_c[i].to, op->nbin[i], s);
+            if (cmd == kCmdApply) {
+                t.group_start();
+                for (size_t i = 0; i < nnb; ++i)
+                    if (!op->remote(i)) {
+                        const Coupling &c = op->to_c[i];
+                        launch_scatter(c.len, c.from, op->iota, c.c, op->nbf[i], op->sline[i], 0, s);
+                        t.send(op->sline[i], sizeof(double) * c.len, 0, s);
+                    }
+                t.group_end();
+            } else {   // back-substitution p_i = q_i - A_i^{-1} R_ic p_c (ddm.py:259-269)
+                for (size_t i = 0; i < nnb; ++i) {
+                    if (op->remote(i)) continue;
+                    const Plan *q = op->nb[i];
+                    if (q->transposed)
+                        launch_transpose(q->m, q->n, op->nbf[i], p_nb[i], -1.0, 1.0, p_nb[i], s);
+                    else
+                        launch_axpby((long long)q->m * q->n, 1.0, p_nb[i], -1.0, op->nbf[i], p_nb[i], s);
+                }
+            }
+        }
+        FD_CUDA(cudaStreamSynchronize(s));
+        return FD_OK;
+    }
+    // ---- rank 0
+    if (!f_center || !p_center) FD_FAIL(FD_ERR_VALIDATION, "sharded solve: rank 0 needs the centre fields");
+    const long long Nc = (long long)op->center->m * op->center->n;
+    int st = FD_OK;
+    std::string err;
+    double *fp = nullptr, *rhs = nullptr;
+    bool done_sent = false;
+    try {
+        FD_CUDA(cudaMallocAsync(&fp, sizeof(double) * Nc, s));
+        FD_CUDA(cudaMallocAsync(&rhs, sizeof(double) * Nc, s));
+        FD_CUDA(cudaMemcpyAsync(fp, f_center, sizeof(double) * Nc, cudaMemcpyDeviceToDevice, s));
+        t.group_start();
+        for (size_t i = 0; i < nnb; ++i)
+            if (op->remote(i)) t.recv(op->rline[i], sizeof(double) * op->to_c[i].len, op->owner[i], s);
+        t.group_end();
+        for (size_t i = 0; i < nnb; ++i) {   // f' = f_c - sum_i R_ci q_i, neighbour order (ddm.py:252-254)
+            const Coupling &c = op->to_c[i];
+            if (op->remote(i)) launch_scatter(c.len, op->iota, c.to, -1.0, op->rline[i], fp, 1, s);
+            else launch_scatter(c.len, c.from_user, c.to, -c.c, p_nb[i], fp, 1, s);
+        }
+        center_solve(op, fp, rhs, 1.0, 0.0, nullptr, s);
+        std::vector<double> hist;
+        st = gmres_precond(op, rhs, p_center, 1, m, tol, max_restarts, hist, rep, s);
+        copy_hist(hist, history, hist_cap, rep);
+        unprecond_apply(op, p_center, rhs, s);   // true residual ||(A_c - S) x - f'|| (krylov.py:189)
+        launch_axpby(Nc, 1.0, rhs, -1.0, fp, rhs, s);
+        rep->true_residual = norm2(Nc, rhs, op->sc, s);
+        // back-substitution: remote arms by their owners, local arms here
+        send_command(op, kCmdBacksub, s);
+        send_lines(op, p_center, s);
+        std::vector<SolveJob> jobs;
+        for (size_t i = 0; i < nnb; ++i) {
+            if (op->remote(i)) continue;
+            const Coupling &c = op->from_c[i];
+            launch_scatter(c.len, c.from, c.to, c.c, p_center, op->nbin[i], 0, s);
+            jobs.push_back(job_of(op->nb[i], op->nbin[i], op->nbf[i]));
+        }
+        if (!jobs.empty()) solve_batch(jobs, s);
+        for (size_t i = 0; i < nnb; ++i) {
+            if (op->remote(i)) continue;
+            launch_zero_at(op->from_c[i].len, op->from_c[i].to, op->nbin[i], s);
+            const Plan *q = op->nb[i];
+            if (q->transposed)
+                launch_transpose(q->m, q->n, op->nbf[i], p_nb[i], -1.0, 1.0, p_nb[i], s);
+            else
+                launch_axpby((long long)q->m * q->n, 1.0, p_nb[i], -1.0, op->nbf[i], p_nb[i], s);
+        }
+        send_command(op, kCmdDone, s);
+        done_sent = true;
+    } catch (const Error &e) {
+        st = e.code;
+        err = e.msg;
+    }
+    if (!done_sent) {   // release the arm owners whatever happened here
+        try {
+            send_command(op, kCmdDone, s);
+        } catch (...) {
+        }
+    }
+    if (fp) cudaFreeAsync(fp, s);
+    if (rhs) cudaFreeAsync(rhs, s);
+    if (!err.empty()) FD_FAIL(st, err);
     if (st != FD_OK) {
         std::ostringstream os;
         os << "GMRES did not reach tol=" << tol << " in " << rep->iterations << " iterations";

@@ -13,6 +13,17 @@
 namespace fd {
 
 // ---------------------------------------------------------------------------
+// rank-to-rank transport of the sharded solve (comm.cpp): NCCL or loopback
+struct Transport {
+    int nranks = 1, rank = 0;
+    virtual ~Transport() = default;
+    virtual void send(const void *buf, size_t bytes, int peer, cudaStream_t s) = 0;
+    virtual void recv(void *buf, size_t bytes, int peer, cudaStream_t s) = 0;
+    virtual void group_start() {}
+    virtual void group_end() {}
+};
+
+// ---------------------------------------------------------------------------
 // error plumbing
 void set_error(const std::string &msg);
 struct Error {
@@ -277,3 +288,8 @@ void launch_basis_update(long long N, int k, const double *V, const double *y_de
 void launch_scale(long long N, const double *x, const double *s_dev, double *out, cudaStream_t s);
 
 }  // namespace fd
+
+struct fd_comm_s {
+    std::unique_ptr<fd::Transport> t;
+    int device;
+};

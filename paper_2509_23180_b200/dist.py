@@ -17,10 +17,16 @@ reduced right-hand side f' (ddm.py:249-254) and the back-substitution
 the single-GPU path's; only where it runs changes, so results equal the
 single-process solve to rounding.
 
-The local arithmetic is a pluggable backend: `GpuBackend` (production:
-native plans/solves, device GMRES with native Arnoldi kernels) or any object
-with the same methods (tests/test_dist_gloo.py drives the protocol on CPU
-with the oracle).
+The local arithmetic is a pluggable backend: `GpuBackend` (native plans and
+solves, GMRES driven from Python) or any object with the same methods
+(tests/test_dist_gloo.py drives the protocol on CPU with the oracle).
+
+`sharded_ddm_solve` is the production path: the same protocol inside the
+native library (fd_ddm_solve_dist: NCCL point-to-point on the caller's
+stream, the low-synchronisation device GMRES on rank 0, no Python in the
+loop), with a communicator from `nccl_comm` (one process per GPU, the NCCL id
+broadcast over torch.distributed) or `loopback_comms` (in-process ranks on one
+device: the test transport).
 """
 
 from __future__ import annotations
@@ -242,3 +248,108 @@ def check_world(comp, world):
     n_arms = max(len(comp.interfaces_of(s.id)) for s in comp.subdomains)
     if world > n_arms + 1:
         raise ValidationError(f"{world} ranks for {n_arms} arms: extra ranks would idle")
+
+
+# ---------------------------------------------------------------------------
+# native sharded solve (fd_ddm_solve_dist)
+
+class Comm:
+    """Owns one native communicator handle (fd_comm)."""
+
+    def __init__(self, ptr, rank, world):
+        self.ptr, self.rank, self.world = ptr, rank, world
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                from . import _native
+                _native.lib().fd_comm_destroy(self.ptr)
+        except Exception:
+            pass
+
+
+def nccl_comm(group=None):
+    """NCCL communicator over the torch.distributed process group: rank 0
+    draws the NCCL unique id, every rank receives it by broadcast."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from . import _native
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    ident = ctypes.create_string_buffer(128)
+    if rank == 0:
+        _native.call("fd_comm_unique_id", ident)
+    obj = [bytes(ident.raw)]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    h = _native.P()
+    _native.call("fd_comm_init", ctypes.byref(h), world, rank, obj[0], torch.cuda.current_device())
+    return Comm(h, rank, world)
+
+
+def loopback_comms(world: int):
+    """`world` in-process ranks on the current device (the protocol's test
+    transport: host-side hand-off, no kernel waits on another rank)."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+    arr = (_native.P * world)()
+    _native.call("fd_comm_init_loopback", arr, world, torch.cuda.current_device())
+    return [Comm(_native.P(arr[r]), r, world) for r in range(world)]
+
+
+def sharded_ddm_solve(comp, f, comm: Comm, gmres_cfg=None, coupled_id=None, owner=None):
+    """Algorithm 1 sharded over `comm`'s ranks inside the native library.  Every
+    rank passes the same composite and the right-hand sides of the subdomains
+    it owns (rank 0: the centre; arms: `owners`).  Returns ({sid: field} of the
+    owned subdomains, SolveReport on rank 0 / None elsewhere)."""
+    import ctypes
+
+    import numpy as np
+
+    from . import _native, krylov
+    from ._fields import empty, to_device
+    from .ddm import build_schur_operator
+    from .errors import ConvergenceError
+    from .geometry import GridField
+
+    validate(comp).require()
+    cfg = gmres_cfg or krylov.GmresConfig()
+    op = build_schur_operator(comp, coupled_id=coupled_id)
+    nbs = [nb.plan.subdomain for nb in op.neighbors]
+    own = list(owner) if owner is not None else owners(len(nbs), comm.world)
+    _native.call("fd_schur_set_comm", op.handle.ptr, comm.ptr, (ctypes.c_int * max(len(own), 1))(*own))
+    mine = [own[i] == comm.rank for i in range(len(nbs))]
+    rhs = {}
+    for i, s_ in enumerate(nbs):
+        if mine[i]:
+            fi = f[s_.id]
+            rhs[s_.id] = to_device(fi.values if isinstance(fi, GridField) else fi, s_.size)[0]
+    p_nb = [empty(s_.size) if mine[i] else None for i, s_ in enumerate(nbs)]
+    f_nb = _native.ptr_array([_native.dptr(rhs[s_.id]) if mine[i] else 0 for i, s_ in enumerate(nbs)])
+    pp_nb = _native.ptr_array([_native.dptr(x) if x is not None else 0 for x in p_nb])
+    hist = np.zeros(cfg.m * cfg.max_restarts + 2)
+    rep = _native.FdReport()
+    fc = pc = None
+    if comm.rank == 0:
+        fi = f[op.coupled_id]
+        fc = to_device(fi.values if isinstance(fi, GridField) else fi, op.size)[0]
+        pc = empty(op.size)
+    st = _native.lib().fd_ddm_solve_dist(
+        op.handle.ptr, _native.dptr(fc) if fc is not None else None, f_nb,
+        _native.dptr(pc) if pc is not None else None, pp_nb, cfg.m, cfg.tol, cfg.max_restarts,
+        hist.ctypes.data_as(_native.DP), hist.size, ctypes.byref(rep), _native.stream_ptr())
+    fields = {s_.id: GridField(s_.id, x) for s_, x in zip(nbs, p_nb) if x is not None}
+    report = None
+    if comm.rank == 0:
+        fields[op.coupled_id] = GridField(op.coupled_id, pc)
+        report = krylov.report_from_native(rep, hist)
+        if st == _native.FD_ERR_NOT_CONVERGED:
+            err = ConvergenceError(_native.lib().fd_last_error().decode(), report=report)
+            err.solution = pc
+            raise err
+    _native.check(st)
+    return fields, report

@@ -103,7 +103,9 @@ def test_transform_kind(lib):
     """GPU transform availability per length (drives the axis choice)."""
     assert [lib.fd_transform_kind(n) for n in (255, 511, 1023, 2047, 4095)] == [1] * 5
     assert [lib.fd_transform_kind(n) for n in (1, 141, 1000, 1024, 1025, 1500, 2048)] == [0] * 7
-    assert [lib.fd_transform_kind(n) for n in (2049, 3000, 8191, 16383)] == [-1] * 4
+    # any other length: the separate Stockham / Bluestein passes (kSep)
+    assert [lib.fd_transform_kind(n) for n in (2049, 3000, 8191, 16383, 65535)] == [2] * 5
+    assert [lib.fd_transform_kind(n) for n in (0, 65536)] == [-1] * 2
 
 
 @pytest.mark.parametrize("m,n,bc,half,axis", [
