@@ -103,8 +103,10 @@ int fd_plan_singular_modes(fd_plan plan, int *modes, int cap, int *count);
  * memory, count x ms x ms row-major (ms = sweep length: m for a y transform,
  * n for an x transform), in fd_plan_singular_modes order. */
 int fd_plan_set_pinv(fd_plan plan, int count, const double *pinv);
-/* GPU transform available for length n: 1 = FFT (n+1 = 2^p, 256..4096),
- * 0 = dense (n <= 2048), -1 = none.  DD pair; fd_transform_kind_pair for NN. */
+/* GPU transform for length n: 1 = fused real-symmetric FFT solve (DD,
+ * n+1 = 2^p in 256..4096), 0 = dense periodic table (n <= 2048), 2 = any-length
+ * mixed-radix / Bluestein passes + separate sweeps (n <= 65535), -1 = none
+ * (PP with odd n).  DD pair; fd_transform_kind_pair for NN (1) / PP (2). */
 int fd_transform_kind(int n);
 int fd_transform_kind_pair(int n, int pair);
 int fd_plan_destroy(fd_plan plan);
@@ -125,17 +127,18 @@ int fd_rect_solve_batched(int count, const fd_plan *plans, const double *const *
                           double *const *out, void *stream);
 
 /* --- transforms.apply_Q / apply_Qt for the DD pair (transforms.py:106-136):
- * out[r, :] = sqrt(2/(n+1)) DST-I(in[r, :]), rows x n, may alias. */
+ * out[r, :] = sqrt(2/(n+1)) DST-I(in[r, :]), rows x n, may alias; any n up to
+ * 65535 (see fd_transform_rows). */
 int fd_dst_rows(int rows, int n, const double *in, double *out, int device, void *stream);
 
-/* --- rectsolver.apply_rect_operator (rectsolver.py:264-289), non-periodic:
- * out = 5-point stencil of v on an m x n grid, delta = 1/h^2, end modifiers
- * mod_* on the four boundary-adjacent lines (geometry.py:118-128). */
 /* apply_Q (inverse = 1) / apply_Qt (inverse = 0) of any pair along rows of
- * length n (transforms.py:106-148): DD on the FFT or dense path, NN and PP on
- * the dense periodic-table path (n <= 2048, PP even n). */
+ * length n (transforms.py:106-148): DD on the real-symmetric FFT kernel
+ * (n + 1 = 2^p in [256, 4096]) or the dense periodic-table transform
+ * (n <= 2048), NN and PP (even n) on the dense table up to 2048, every other
+ * length on the mixed-radix / Bluestein passes (n <= 65535). */
 int fd_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out, int device,
                       void *stream);
+
 /* Device-side problem assembly: f = lap p + kappa p at the
  * cell-centred nodes (origin + (i - 1/2) h, geometry.py:82-86) of an m x n
  * rectangle, minus lift_e * delta * p(ghost) on the line next to each edge
@@ -145,19 +148,23 @@ int fd_transform_rows(int rows, int n, int pair, int inverse, const double *in, 
 int fd_assemble_rhs(int m, int n, double x0, double y0, double dx, double dy, double kappa, int solution,
                     double lift_west, double lift_east, double lift_south, double lift_north, double *f,
                     double *exact, void *stream);
+
+/* --- rectsolver.apply_rect_operator (rectsolver.py:264-289), non-periodic:
+ * out = 5-point stencil of v on an m x n grid, delta = 1/h^2, end modifiers
+ * mod_* on the four boundary-adjacent lines (geometry.py:118-128). */
 int fd_stencil_apply(int m, int n, double delta_x, double delta_y, double kappa,
                      double mod_west, double mod_east, double mod_south, double mod_north,
                      const double *v, double *out, void *stream);
-
-/* --- ddm.build_schur_operator (ddm.py:182-201).  For neighbour i:
- * to_center maps its line into the centre  (R_ci, ddm.py:85),
- * from_center maps the centre line into it (R_ic, ddm.py:86).
- * Index arrays are HOST int64 of length line_len[i]; they are copied. */
 /* Same with periodic axes (wrap-around neighbours instead of end modifiers,
  * rectsolver.py:274-285). */
 int fd_stencil_apply_ex(int m, int n, double delta_x, double delta_y, double kappa,
                         double mod_west, double mod_east, double mod_south, double mod_north,
                         int periodic_x, int periodic_y, const double *v, double *out, void *stream);
+
+/* --- ddm.build_schur_operator (ddm.py:182-201).  For neighbour i:
+ * to_center maps its line into the centre  (R_ci, ddm.py:85),
+ * from_center maps the centre line into it (R_ic, ddm.py:86).
+ * Index arrays are HOST int64 of length line_len[i]; they are copied. */
 int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south,
                     double center_mod_north, int n_nb, const fd_plan *nb,
                     const int *line_len,

@@ -22,7 +22,7 @@ import numpy as np
 from . import _native, krylov
 from ._fields import empty, is_torch, like_input, to_device
 from .errors import ConvergenceError, ValidationError
-from .geometry import CompositeDomain, GridField, Interface, line_indices, validate
+from .geometry import adopt, CompositeDomain, GridField, Interface, line_indices, validate
 from .rectsolver import RectPlan, plan_rect, solve_rect
 
 
@@ -58,6 +58,7 @@ class CouplingMap:
 
 def make_coupling(comp: CompositeDomain, iface: Interface, from_id: int) -> CouplingMap:
     """Coupling map leaving `from_id` across `iface` (ref ddm.py:54-70)."""
+    comp, iface = adopt(comp), adopt(iface)
     to_id = iface.other_side(from_id)[0]
     sf, st = comp.subdomain(from_id), comp.subdomain(to_id)
     perm = np.asarray(iface.index_map)
@@ -245,6 +246,7 @@ def build_schur_operator(comp: CompositeDomain, coupled_id: int | None = None,
     interface_only=True selects the opt-in Steklov form of the neighbour applies
     (same operator up to rounding) when every neighbour's
     interface line is a ghost-node DD pair of one length."""
+    comp = adopt(comp)
     if coupled_id is None:
         coupled_id = designate_center(comp)
     center = comp.subdomain(coupled_id)
@@ -273,6 +275,7 @@ def ddm_solve(comp: CompositeDomain, f, gmres_cfg=None, coupled_id: int | None =
     """Solve the composite system; returns ({id: GridField}, SolveReport)
     (ref ddm.py:210-270).  numpy right-hand sides give numpy solutions; torch
     CUDA right-hand sides stay on the device."""
+    comp = adopt(comp)
     validate(comp).require()
     cfg = gmres_cfg or krylov.GmresConfig()
     rhs, host = {}, True

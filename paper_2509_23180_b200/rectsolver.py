@@ -21,7 +21,7 @@ from . import _native, transforms
 from ._fields import empty, is_torch, like_input, to_device
 from ._native import UnsupportedError
 from .errors import SingularOperatorError, ValidationError
-from .geometry import BoundaryKind, GridField, RectSubdomain
+from .geometry import adopt, BoundaryKind, GridField, RectSubdomain
 
 
 _PAIR_CODE = {"DD": 0, "NN": 1, "PP": 2}
@@ -169,6 +169,7 @@ def plan_rect(subdomain: RectSubdomain, pin_mean: bool = False) -> RectPlan:
     minimum-norm sense: their sweep matrices' pseudo-inverses are formed here
     at plan time (host setup, like the reference's dense mode matrices) and
     applied on the device inside the solve."""
+    subdomain = adopt(subdomain)
     sub = subdomain
     _native.require_cuda()
     axis = _gpu_axis(sub)
@@ -228,6 +229,7 @@ def solve_rect_batched(plans, fields, out=None):
 
 def apply_rect_operator(sub: RectSubdomain, values):
     """5-point matvec with end modifiers or periodic wrap (ref rectsolver.py:264-289)."""
+    sub = adopt(sub)
     v, host = to_device(values, sub.size)
     out = empty(sub.size)
     ppx, ppy = int(sub.axis_pair("x") == "PP"), int(sub.axis_pair("y") == "PP")
@@ -242,6 +244,7 @@ def lift_dirichlet(sub: RectSubdomain, rhs, edge: str, boundary_values):
     """rhs - factor * delta * g on the line next to a Dirichlet edge; factor 2
     for half-cell edges (ref rectsolver.py:292-313).  Host numpy (problem
     assembly) or torch tensors."""
+    sub = adopt(sub)
     if sub.edge_bc[edge] is not BoundaryKind.DIRICHLET:
         raise ValueError(f"edge {edge} of subdomain {sub.id} is not Dirichlet")
     factor = 2.0 if edge in sub.half_cell_dirichlet else 1.0
