@@ -172,6 +172,12 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south,
                     const double *to_c_coupling,
                     const int64_t *const *from_c_from, const int64_t *const *from_c_to,
                     const double *from_c_coupling);
+/* The centre operator A_c of (A_c - S) (fd_unprecond_apply, the true
+ * residual) in the caller's layout: grid, 1/h^2, kappa, end modifiers and
+ * periodic axes of the coupled subdomain (rectsolver.py:264-289) -- needed
+ * for a transposed or periodic centre; default: from the centre plan. */
+int fd_schur_set_stencil(fd_schur op, int m, int n, double delta_x, double delta_y, double kappa, double mod_west,
+                         double mod_east, double mod_south, double mod_north, int periodic_x, int periodic_y);
 /* Interface-only (Steklov) neighbour applies -- SURVEY 8f row 2, an opt-in
  * variant of SchurOperator.schur (ddm.py:108-123) with the same result up to
  * rounding: neighbour i's interface line (length line_len, a DD pair with

@@ -30,7 +30,7 @@ EXPORTS = (
     "fd_center_solve", "fd_precond_apply", "fd_unprecond_apply", "fd_gmres_precond",
     "fd_ddm_solve", "fd_schur_set_steklov", "fd_schur_use_steklov", "fd_arnoldi_step", "fd_basis_update", "fd_axpby", "fd_norm", "fd_dot",
     "fd_comm_unique_id", "fd_comm_init", "fd_comm_init_loopback", "fd_comm_rank", "fd_comm_destroy",
-    "fd_schur_set_comm", "fd_ddm_solve_dist",
+    "fd_schur_set_comm", "fd_ddm_solve_dist", "fd_schur_set_stencil",
 )
 
 
@@ -99,6 +99,7 @@ def _declare(lib):
         "fd_comm_rank": (I, [P, ctypes.POINTER(I), ctypes.POINTER(I)]),
         "fd_comm_destroy": (I, [P]),
         "fd_schur_set_comm": (I, [P, P, ctypes.POINTER(I)]),
+        "fd_schur_set_stencil": (I, [P, I, I, D, D, D, D, D, D, D, I, I]),
         "fd_ddm_solve_dist": (I, [P, P, ctypes.POINTER(P), P, ctypes.POINTER(P), I, D, I, DP, I,
                                   ctypes.POINTER(FdReport), P]),
     }

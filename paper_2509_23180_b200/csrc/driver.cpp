@@ -234,6 +234,13 @@ struct fd_schur_s {
     // sharded solve: arm i is solved on rank owner[i]; rank 0 holds
     // the centre, the Krylov basis and drives the protocol; every rank holds
     // the same operator object (plans, couplings, work fields of its arms)
+    // the centre operator A_c in the caller's layout (unprecond_apply); set by
+    // fd_schur_set_stencil, else taken from the centre plan
+    struct Stencil {
+        int m = 0, n = 0, px = 0, py = 0;
+        double dx = 0, dy = 0, kappa = 0, mw = 0, me = 0, ms = 0, mn = 0;
+    } stencil;
+    bool stencil_set = false;
     fd_comm_s *comm = nullptr;
     std::vector<int> owner;
     int64_t *iota = nullptr;                  // 0 .. max line length - 1
@@ -567,7 +574,12 @@ static void precond_apply_loop(fd_schur_s *op, const double *p, cudaStream_t s) 
 
 // (A_c - S) p   (ddm.py:128-131)
 static void unprecond_apply(fd_schur_s *op, const double *p, double *out, cudaStream_t s) {
-    launch_stencil(*op->center, op->mod_s, op->mod_n, p, op->tmp2, s);
+    if (op->stencil_set) {
+        const auto &t = op->stencil;
+        launch_stencil(t.m, t.n, t.dx, t.dy, t.kappa, t.mw, t.me, t.ms, t.mn, p, op->tmp2, s, t.px, t.py);
+    } else {
+        launch_stencil(*op->center, op->mod_s, op->mod_n, p, op->tmp2, s);
+    }
     schur_apply(op, p, out, s);
     const long long N = (long long)op->center->m * op->center->n;
     launch_axpby(N, 1.0, op->tmp2, -1.0, out, out, s);
@@ -1052,6 +1064,28 @@ int fd_schur_create(fd_schur *out, fd_plan center, double center_mod_south, doub
         throw;
     }
     *out = op;
+    FD_API_END
+}
+
+int fd_schur_set_stencil(fd_schur op, int m, int n, double delta_x, double delta_y, double kappa, double mod_west,
+                         double mod_east, double mod_south, double mod_north, int periodic_x, int periodic_y) {
+    FD_API_BEGIN
+    if (!op) FD_FAIL(FD_ERR_VALIDATION, "null operator");
+    if ((long long)m * n != (long long)op->center->m * op->center->n)
+        FD_FAIL(FD_ERR_VALIDATION, "stencil grid does not match the centre plan");
+    auto &t = op->stencil;
+    t.m = m;
+    t.n = n;
+    t.dx = delta_x;
+    t.dy = delta_y;
+    t.kappa = kappa;
+    t.mw = mod_west;
+    t.me = mod_east;
+    t.ms = mod_south;
+    t.mn = mod_north;
+    t.px = periodic_x;
+    t.py = periodic_y;
+    op->stencil_set = true;
     FD_API_END
 }
 

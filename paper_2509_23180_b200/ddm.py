@@ -250,9 +250,6 @@ def build_schur_operator(comp: CompositeDomain, coupled_id: int | None = None,
     if coupled_id is None:
         coupled_id = designate_center(comp)
     center = comp.subdomain(coupled_id)
-    if "PP" in (center.axis_pair("x"), center.axis_pair("y")):
-        from ._native import UnsupportedError
-        raise UnsupportedError("a periodic coupled subdomain is not on the GPU path")
     neighbors = []
     for iface in comp.interfaces_of(coupled_id):
         other = iface.other_side(coupled_id)[0]
@@ -262,6 +259,12 @@ def build_schur_operator(comp: CompositeDomain, coupled_id: int | None = None,
                                    from_center=make_coupling(comp, iface, coupled_id), edge=edge))
     cplan = plan_rect(center)
     handle = _SchurHandle(cplan, neighbors)
+    # A_c in the caller's layout (periodic axes, transposed plans): rectsolver.py:264-289
+    _native.call("fd_schur_set_stencil", handle.ptr, center.m, center.n, float(center.delta_x),
+                 float(center.delta_y), float(center.kappa), float(center.end_modifier("west")),
+                 float(center.end_modifier("east")), float(center.end_modifier("south")),
+                 float(center.end_modifier("north")), int(center.axis_pair("x") == "PP"),
+                 int(center.axis_pair("y") == "PP"))
     if interface_only:
         kappas = {comp.subdomain(nb.plan.subdomain.id).kappa for nb in neighbors}
         if len(kappas) == 1:

@@ -889,3 +889,37 @@ class TestShardedSolve:
         assert rep.iterations == rrep.iterations
         for sid in ref:
             assert rel(got[sid].values.cpu().numpy(), ref[sid].values) < 1e-14
+
+
+class TestPeriodicCenter:
+    """A coupled subdomain with a periodic axis (the reference restricts no
+    centre, ddm.py:182-201): a centre periodic in y between two arms that are
+    periodic in y too, against the oracle's Algorithm 1."""
+
+    @staticmethod
+    def _comp(kappa):
+        from paper_2509_23180_b200.geometry import CompositeDomain, make_interface, validate
+        h = 1.0 / 16
+        c = make((12, 16, h, h, kappa, "IIPP", ()), 0)
+        w = make((8, 16, h, h, kappa, "DIPP", ()), 1)
+        e = make((10, 16, h, h, kappa, "IDPP", ("east",)), 2)
+        import dataclasses
+        w = dataclasses.replace(w, origin=(-8 * h, 0.0))
+        e = dataclasses.replace(e, origin=(12 * h, 0.0))
+        comp = CompositeDomain(subdomains=[c, w, e],
+                               interfaces=[make_interface(0, w, "east", c, "west"),
+                                           make_interface(1, c, "east", e, "west")])
+        validate(comp).require()
+        return comp
+
+    @pytest.mark.parametrize("kappa", [0.0, -5.0])
+    def test_against_oracle(self, kappa, rng):
+        comp = self._comp(kappa)
+        f = {s.id: rng.uniform(-1, 1, s.size) for s in comp.subdomains}
+        fields, rep = ddm.ddm_solve(comp, f, krylov.GmresConfig(m=50, tol=1e-10))
+        ofields, orep = O.ddm_solve(comp, f, m=50, tol=1e-10)
+        assert rep.iterations == orep.iterations
+        num = sum(float(np.sum((fields[s].values - ofields[s]) ** 2)) for s in ofields)
+        den = sum(float(np.sum(ofields[s] ** 2)) for s in ofields)
+        assert (num / den) ** 0.5 < 1e-10
+        assert rep.true_residual == pytest.approx(orep.true_residual, rel=0.5)
