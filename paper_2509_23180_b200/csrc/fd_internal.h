@@ -64,8 +64,6 @@ struct PlanDev {
     const double *mode;  // [n][8]: l_inf, 1/b_inf, b_inf, 1/(-l_inf), b_last, lambda, ex_off, fixed-point row (int64 bits)
     int ecap;            // rows [0, ecap) of every mode also stored row-major (coalesced):
     const double *dl, *dib, *db;   // [ecap][n] lower, 1/beta, beta
-    const double *fe;    // [2][ecap][fep]: dl, dib again with an even row pitch fep (FFT plans; split.cu)
-    int fep;
     int kt, ktp;         // slowly converging modes k < kt: row-major table (ktp = kt rounded to even)
     const double *lt;    // [m][3][ktp]: l_i, 1/beta_i, -beta_{i-1}/delta
     const double *blk;   // [nb][3][n]: Pe, xi_s, Q per block and mode
@@ -214,7 +212,6 @@ void dft_rows(long long rows, int M, const double2 *in, double2 *out, int invers
 void transform_rows_any(long long rows, int n, int pair, int inverse, const double *in, double *out, double alpha,
                         double beta, const double *other, cudaStream_t st);
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);
-bool launch_split(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws);   // split.cu
 void launch_transform_rows(int rows, int n, int pair, int inverse, const double *in, double *out,
                            const double *dense, cudaStream_t s);
 void launch_dst_rows(int rows, int n, const double *in, double *out, const double2 *tw,

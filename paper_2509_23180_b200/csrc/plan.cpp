@@ -517,17 +517,6 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.dl = upload(p, dl);
         d.dib = upload(p, dib);
         d.db = upload(p, db);
-        d.fe = nullptr;
-        d.fep = (n + 1) & ~1;
-        if (tk == kFFT) {   // split solve (split.cu): [2][ecap][fep] l, 1/beta with a 16-byte row pitch (TMA boxes)
-            std::vector<double> fe(size_t(2) * d.ecap * d.fep, 0.0);
-            for (int i = 0; i < d.ecap; ++i)
-                for (int k = 0; k < n; ++k) {
-                    fe[size_t(i) * d.fep + k] = dl[size_t(i) * n + k];
-                    fe[(size_t(d.ecap) + i) * d.fep + k] = dib[size_t(i) * n + k];
-                }
-            d.fe = upload(p, fe);
-        }
         if (tk == kFFT) {
             build_long_table(T, m, n, d.off, rs_kt_cap(n + 1));
         }

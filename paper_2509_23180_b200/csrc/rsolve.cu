@@ -684,7 +684,6 @@ struct RsK {
 bool launch_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws) {
     const int n = jobs[0].p.n;
     if (!rs_supported(n) || !jobs[0].p.ralpha) return false;
-    if (launch_split(jobs, s, ws)) return true;
     switch (n + 1) {
         case 256: run_persist<RsK<8>>(jobs, s, ws); return true;
         case 512: run_persist<RsK<9>>(jobs, s, ws); return true;

@@ -1,3 +1,38 @@
+// ARCHIVED EXPERIMENT (round 2, session 3) -- not compiled into libfftddm_b200.so.
+// To build it again: copy to paper_2509_23180_b200/csrc/split.cu, declare
+// `bool launch_split(const std::vector<SolveJob>&, cudaStream_t, Workspace&)` in
+// fd_internal.h, call it first in launch_persist (rsolve.cu), and add the padded
+// factor table `fe` / `fep` to PlanDev + plan.cpp (see git history, commit
+// "Split rectangle solve (opt-in, FD_SPLIT=1)").
+//
+// Measured on one B200 (c1: 5 x 1023^2, 8 rotating buffer sets; the shipped fused
+// kernel rsolve.cu: 89-90 us per apply):
+//   K_A row-pair DST (HBM -> Z)            33-35 us   (29 us under ncu, cold L2)
+//   K_C row-pair DST (Z -> out)            29-31 us
+//   K_B mode-sliced Thomas, TMA ring       48 us      (24 us for slices on the fixed
+//       point, 48 us for the four slices per job that stream the long-transient table)
+//   K_B blocks-in-one-CTA form             50-93 us
+//   whole apply                            105-115 us -- slower than the fused kernel.
+// Why (ncu + clock stamps + tools/micro):
+//  * K_A / K_C run the same RFft passes as rsolve.cu with the same 16 warps per SM
+//    (128 registers): 1562 warp instructions per row pair and warp at IPC 1.2 per SM,
+//    warp-cycles per issued instruction 11.4 -- latency-bound at 25 % occupancy.
+//    Independent small CTAs did not overlap better than the lockstep kernel; bulk-copy
+//    (TMA) input instead of global loads changed nothing (33.9 vs 33.9 us).
+//  * A lone in-order warp walking the Thomas chain can reach 9.2-11.3 cycles per row
+//    (tools/micro/chain.cu, chain2.cu: DFMA latency 8.2 cycles) only with straight-line
+//    code; every dependent test / branch between two links costs 4-10 cycles, a
+//    per-row cp.async.bulk costs ~64 cycles of the issuing warp (tools/micro/gather.cu,
+//    lat.cu), mbarrier.try_wait ~150 cycles.  The kernel below reaches 16-18
+//    cycles per row (1050 cycles per 64-row tile) after those were removed.
+//  * Splitting the rows of a mode slice over the warps of one CTA (second kernel)
+//    needs the slice on chip between the sweeps: 32 modes x 1023 rows x 8 B = 262 KB
+//    exceeds the register file (256 KB), so half of every block lives in shared
+//    memory, the CTA count (160) needs two rounds on 148 SMs, and the blocks holding
+//    table rows (the first 128 rows, strided 256-byte reads of dl/dib/db) run 3-6x
+//    longer than the others, which wait at the carry barrier.
+//  * Both extra trips of the field through the L2 are not free: the 2 x 42 MB
+//    scratch traffic of K_B alone is ~10 us at the L2 rates reached here.
 // Split rectangle solve for FFT lengths whose fields fit the L2 (n + 1 = N = 2^NL):
 // three launches instead of one cooperative kernel,
 //
@@ -39,6 +74,7 @@ struct XJob {
     double h2;        // 0.5 * scale
     int m, pairs;
     int spitch, dpitch;   // row pitch of src / dst in doubles (other: n)
+    int tma;              // src row pairs are 16-byte aligned multiples of 16 bytes: bulk copies
 };
 struct XList {
     int count, n;
@@ -47,7 +83,7 @@ struct XList {
     XJob job[kMaxPJobs];
 };
 
-template <int NL>
+template <int NL, bool STREAM>
 __global__ void __launch_bounds__(RS<NL>::T, (512 / RS<NL>::T) > 8 ? 8 : (512 / RS<NL>::T))
     dst_pair_kernel(const __grid_constant__ XList xl) {
     using C = RS<NL>;
@@ -68,7 +104,46 @@ __global__ void __launch_bounds__(RS<NL>::T, (512 / RS<NL>::T) > 8 ? 8 : (512 / 
     const bool hb = r0 + 1 < J.m;
     const double *A = J.src + size_t(r0) * J.spitch;
     double2 v[16];
-    F::load(v, A, hb ? A + J.spitch : nullptr, xl.ralpha, J.h2, t);
+    if (J.tma && hb) {
+        // the row pair arrives by one bulk copy (TMA) in the exchange region itself
+        // and is pre-weighted out of shared memory: one memory round trip per
+        // CTA instead of one per batch of loads the registers allow
+        __shared__ __align__(8) uint64_t bar;
+        if (t == 0) {
+            mbar_init(&bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(&bar, uint32_t(2 * J.spitch * 8));
+            tma_load_1d(buf, A, uint32_t(2 * J.spitch * 8), &bar);
+        }
+        __syncthreads();
+        mbar_wait(&bar, 0);
+        const double *SA = reinterpret_cast<const double *>(buf);
+        F::load(v, SA, SA + J.spitch, xl.ralpha, J.h2, t);
+        rsync<T>(0);   // the staged rows alias the exchange buffer
+    } else {
+        // pre-weighted input of the first pass (RFft::load) straight from global
+        // memory; STREAM: the user's right-hand side is read once -- evict-first,
+        // so that it does not push the scratch field Z out of the L2
+        const double *B = hb ? A + J.spitch : A;
+        constexpr int N = C::N;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int jj = t + r * T;
+            if (r == 0 && t == 0) {
+                v[0] = make_double2(0.0, 0.0);
+                continue;
+            }
+            const double a = __ldg(xl.ralpha + jj), bq = a - J.h2;
+            const int i1 = jj - 1, i2 = N - 1 - jj;
+            if (STREAM) {
+                v[r].x = fma(a, __ldcs(A + i1), bq * __ldcs(A + i2));
+                v[r].y = fma(a, __ldcs(B + i1), bq * __ldcs(B + i2));
+            } else {
+                v[r].x = fma(a, __ldcg(A + i1), bq * __ldcg(A + i2));
+                v[r].y = fma(a, __ldcg(B + i1), bq * __ldcg(B + i2));
+            }
+        }
+    }
     F::first(buf, v, t, 0);
     if constexpr (C::NMID > 0) F::mid(buf, xl.m16, t, 0);
     F::last(buf, xl.m16 + 16, t, 0);
@@ -83,13 +158,16 @@ __global__ void __launch_bounds__(RS<NL>::T, (512 / RS<NL>::T) > 8 ? 8 : (512 / 
         const double *qh = J.other ? J.other + size_t(r0 + h) * n : nullptr;
         if (qh) {
 #pragma unroll 8
-            for (int q = t; q < n; q += T) oh[q] = fma(be_, __ldg(qh + q), al_ * Xh[xi(q)]);
+            for (int q = t; q < n; q += T) __stcs(oh + q, fma(be_, __ldcs(qh + q), al_ * Xh[xi(q)]));
         } else if (al_ == 1.0) {
 #pragma unroll 8
-            for (int q = t; q < n; q += T) oh[q] = Xh[xi(q)];
+            for (int q = t; q < n; q += T) {
+                if (STREAM) oh[q] = Xh[xi(q)];      // stage A writes Z: keep it in the L2
+                else __stcs(oh + q, Xh[xi(q)]);
+            }
         } else {
 #pragma unroll 8
-            for (int q = t; q < n; q += T) oh[q] = al_ * Xh[xi(q)];
+            for (int q = t; q < n; q += T) __stcs(oh + q, al_ * Xh[xi(q)]);
         }
     }
 }
@@ -310,7 +388,7 @@ __global__ void __launch_bounds__(kThomasThreads, 1) thomas_kernel(const __grid_
 
     // ------------------------------ consumers ------------------------------
     const int q = 32 * warp + lane;        // mode within the slice
-    const bool inb = q < W && !(tl.dbgmask & 2);                // lane owns a column of the tile
+    const bool inb = q < W;                // lane owns a column of the tile
     const bool act = q < w;
     const int qq = inb ? q : 0;
     const int k = k0 + (act ? q : 0);
@@ -339,7 +417,7 @@ __global__ void __launch_bounds__(kThomasThreads, 1) thomas_kernel(const __grid_
         uint64_t *done = BWD ? done_b : done_f;
         auto need = [&](int t) { return !BWD || t < TS; };            // tile is copied in during this pass
         auto wrap = [&](int g) { return BWD ? (g == 0 ? NG - 1 : g - 1) : (g + 1 == NG ? 0 : g + 1); };
-        // make sure tile t's copies have landed (counters were read a tile ago)
+        // make sure tile t's copies have landed (the counters were read a tile ago)
         auto acquire = [&](int t) {
             if (need(t)) {
                 ++dneed;
@@ -358,132 +436,91 @@ __global__ void __launch_bounds__(kThomasThreads, 1) thomas_kernel(const __grid_
                 }
             }
         };
-        // chunk c (16 rows; ascending c forward, descending backward) of tile t in slot g -> registers
-        auto load = [&](int t, int g, int c, double (&dv)[kCH], double (&fv)[kCH]) {
-            const double *sl = slots + size_t(g) * TILE + c * kCH * W + qq;
-            if (!(tl.dbgmask & 4)) {
-#pragma unroll
-                for (int r = 0; r < kCH; ++r) dv[r] = sl[r * W];
-            }
-            const int i0 = t * kSR + c * kCH;
-            if (fact(t)) {
-                const double *fs = fslots + size_t(t % kFG) * TILE + c * kCH * W + qq;
-                const bool tab = i0 < ecap || tabm;
-#pragma unroll
-                for (int r = 0; r < kCH; ++r) {
-                    const double cst = BWD ? ((i0 + r == m - 1) ? ib_last : ib_inf) : l_inf;
-                    fv[r] = tab ? fs[r * W] : cst;
-                }
-            } else if (BWD && t == T - 1) {
-#pragma unroll
-                for (int r = 0; r < kCH; ++r) fv[r] = (i0 + r == m - 1) ? ib_last : ib_inf;
-            }
-            if (BWD && t == T - 1) {   // the forward pass ran on past row m-1 in this (resident) tile
-#pragma unroll
-                for (int r = 0; r < kCH; ++r)
-                    if (i0 + r >= m) dv[r] = 0.0;
-            }
-        };
-        // One chunk of the recurrence.  The results stay in registers (oc) and are
-        // stored one chunk LATER, interleaved with the next chunk's chain (op, sp):
-        // a store issued right behind the DFMA that produces its value waits ~20
-        // cycles for the fp64 result and, the warp issuing in order, holds up the
-        // next link of the chain (measured: 21.7 instead of 8.2 cycles per row).
-        auto compute = [&](int t, const double (&dv)[kCH], const double (&fv)[kCH], double (&oc)[kCH],
-                           const double (&op)[kCH], double *sp) {
-            const bool st = inb && sp != nullptr;
-            if (fact(t) || (BWD && t == T - 1)) {
-                if (!BWD) {
-#pragma unroll
-                    for (int r = 0; r < kCH; ++r) {
-                        carry = fma(-fv[r], carry, dv[r]);
-                        oc[r] = carry;
-                        if (st) sp[r * W] = op[r];
-                    }
-                } else {
-                    double a[kCH], gg[kCH];
-#pragma unroll
-                    for (int r = 0; r < kCH; ++r) {
-                        a[r] = dv[r] * fv[r];
-                        gg[r] = noff * fv[r];
-                    }
-#pragma unroll
-                    for (int r = kCH - 1; r >= 0; --r) {
-                        carry = fma(gg[r], carry, a[r]);
-                        oc[r] = carry;
-                        if (st) sp[r * W] = op[r];
-                    }
-                }
-            } else if (!BWD) {
-#pragma unroll
-                for (int r = 0; r < kCH; ++r) {
-                    carry = fma(nl_inf, carry, dv[r]);
-                    oc[r] = carry;
-                    if (st) sp[r * W] = op[r];
-                }
-            } else {
-                double a[kCH];
-#pragma unroll
-                for (int r = 0; r < kCH; ++r) a[r] = dv[r] * ib_inf;
-#pragma unroll
-                for (int r = kCH - 1; r >= 0; --r) {
-                    carry = fma(g_inf, carry, a[r]);
-                    oc[r] = carry;
-                    if (st) sp[r * W] = op[r];
-                }
-            }
-        };
-        auto signal = [&](int t, int g) {
-            // the producer's tensor store reads the slot (streamed y, every xhat tile)
-            if (BWD || t < TS) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&done[g]);
-        };
-        // Tile loop; the four chunks of a tile are unrolled with compile-time
-        // chunk indices, the registers ping-pong (A, B, A, B), and the last
-        // chunk prefetches the first chunk of the next tile.
-        double da[kCH], fa[kCH], db[kCH], fb[kCH], oa[kCH], ob[kCH];
-        double *sprev = nullptr;   // where the previous chunk's results (in oa / ob) go
-        int t = BWD ? T - 1 : 0, g = t % NG;
-        int tp = t, gp = g;
-        acquire(t);
-        load(t, g, BWD ? NC - 1 : 0, da, fa);
-        for (int it = 0; it < T; ++it) {
-            const int tn = t + dir, gn = wrap(g);
-            const bool more = it + 1 < T;
-            // counters for the next tile: read now, compared after this tile's first chunks
+        double da[kCH], db[kCH];   // data of the current / next chunk
+        // One tile.  KIND 0: fixed-point factors; 1: factors from the table tile
+        // (per lane: table or fixed point); 2: the pass's first backward tile
+        // (holds row m-1 and the rows past it).  Straight-line code: the chunk
+        // loop is unrolled with compile-time indices and has no tile-uniform
+        // tests inside (a lone in-order warp pays ~4-10 cycles for every
+        // dependent test and branch between two links of the chain).
+        auto tile = [&](auto kind_tag, int t, int g, int tn, int gn, bool more) {
+            constexpr int KIND = decltype(kind_tag)::value;
+            double *sl = slots + size_t(g) * TILE + qq;
+            const double *sn = slots + size_t(gn) * TILE + qq;
+            const double *fs = fslots + size_t(t % kFG) * TILE + qq;
+            const bool tab = t * kSR < ecap || tabm;
+            const bool isf = fact(t);
+            // counters for the next tile: read now, compared at this tile's last chunk
             dseen = ld_acquire(&landed[0]);
             fseen = ld_acquire(&landed[1]);
 #pragma unroll
             for (int ci = 0; ci < NC; ++ci) {
                 const int c = BWD ? NC - 1 - ci : ci;
-                double *sl = slots + size_t(g) * TILE + c * kCH * W + qq;
-                auto body = [&](double (&dc)[kCH], double (&fc)[kCH], double (&dn)[kCH], double (&fn)[kCH],
-                                double (&oc)[kCH], double (&op)[kCH]) {
-                    if (ci + 1 < NC) {
-                        load(t, g, c + dir, dn, fn);
-                    } else if (more) {
-                        acquire(tn);
-                        load(tn, gn, BWD ? NC - 1 : 0, dn, fn);
+                auto body = [&](double (&dc)[kCH], double (&dn)[kCH]) {
+                    double fv[kCH];
+                    if (KIND != 0) {
+                        const int i0 = t * kSR + c * kCH;
+#pragma unroll
+                        for (int r = 0; r < kCH; ++r) {
+                            const double cst = BWD ? ((KIND == 2 && i0 + r == m - 1) ? ib_last : ib_inf) : l_inf;
+                            fv[r] = (isf && tab) ? fs[(c * kCH + r) * W] : cst;
+                            if (KIND == 2 && i0 + r >= m) dc[r] = 0.0;   // the forward pass ran on past row m-1
+                        }
                     }
-                    compute(t, dc, fc, oc, op, sprev);
+                    if (ci + 1 < NC) {
+#pragma unroll
+                        for (int r = 0; r < kCH; ++r) dn[r] = sl[((c + dir) * kCH + r) * W];
+                    } else {
+                        if (more) acquire(tn);
+#pragma unroll
+                        for (int r = 0; r < kCH; ++r) dn[r] = sn[((BWD ? NC - 1 : 0) * kCH + r) * W];
+                    }
+                    double *so = sl + c * kCH * W;
+                    if (!BWD) {
+#pragma unroll
+                        for (int r = 0; r < kCH; ++r) {
+                            carry = fma(KIND != 0 ? -fv[r] : nl_inf, carry, dc[r]);
+                            if (inb) so[r * W] = carry;
+                        }
+                    } else {
+                        double a[kCH], gg[kCH];
+#pragma unroll
+                        for (int r = 0; r < kCH; ++r) {
+                            a[r] = dc[r] * (KIND != 0 ? fv[r] : ib_inf);
+                            gg[r] = KIND != 0 ? noff * fv[r] : g_inf;
+                        }
+#pragma unroll
+                        for (int r = kCH - 1; r >= 0; --r) {
+                            carry = fma(gg[r], carry, a[r]);
+                            if (inb) so[r * W] = carry;
+                        }
+                    }
                 };
-                if (ci & 1) body(db, fb, da, fa, ob, oa);
-                else body(da, fa, db, fb, oa, ob);
-                sprev = sl;
-                if (ci == 0 && it > 0) signal(tp, gp);   // the previous tile's last stores have been issued
+                if (ci & 1) body(db, da);
+                else body(da, db);
             }
+            // the producer's tensor store reads the slot (streamed y, every xhat tile)
+            if (BWD || t < TS) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&done[g]);
+        };
+        int t = BWD ? T - 1 : 0, g = t % NG;
+        acquire(t);
+        {
+            const double *sl = slots + size_t(g) * TILE + qq;
+#pragma unroll
+            for (int r = 0; r < kCH; ++r) da[r] = sl[((BWD ? NC - 1 : 0) * kCH + r) * W];
+        }
+        for (int it = 0; it < T; ++it) {
+            const int tn = t + dir, gn = wrap(g);
+            const bool more = it + 1 < T;
+            if (BWD && it == 0) tile(std::integral_constant<int, 2>{}, t, g, tn, gn, more);
+            else if (fact(t)) tile(std::integral_constant<int, 1>{}, t, g, tn, gn, more);
+            else tile(std::integral_constant<int, 0>{}, t, g, tn, gn, more);
             if (tl.dbg && tid == 0 && it < 20) tl.dbg[size_t(gridDim.x) * 16 + size_t(blockIdx.x) * 64 + (BWD ? 32 : 0) + it] = clock64();
-            tp = t;
-            gp = g;
             t = tn;
             g = gn;
         }
-        if (inb) {   // NC is even: the last chunk's results are in ob
-#pragma unroll
-            for (int r = 0; r < kCH; ++r) sprev[r * W] = ob[r];
-        }
-        signal(tp, gp);
     };
     {
         const long long c_start = clock64();
@@ -500,6 +537,278 @@ __global__ void __launch_bounds__(kThomasThreads, 1) thomas_kernel(const __grid_
             d[2] = w_f;
             d[3] = cwait - w_f;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K_B, second form: mode-sliced Thomas sweeps with the rows of a slice split
+// over the warps of ONE CTA (block carries exchanged through shared memory).
+//
+// CTA = 32 modes (lane = mode) x kNB = 16 row blocks (warp = block) of kRPB = 64
+// rows; a thread keeps its block of one mode on chip from the forward to the
+// backward sweep: the first kRR = 32 rows in registers, the other 32 in a
+// private shared-memory column.  The sweeps are those of rsolve.cu (the
+// reference recurrences rectsolver.py:86,90 inside a block, affine block carries
+// across blocks), but every block of a mode lives in the same CTA, so the carry
+// exchange is a __syncthreads and a 16-step scan instead of two grid barriers:
+//
+//   forward, block [s, e], local (y_{s-1} = 0):
+//     y_i = r_i - l_i y_{i-1},  w_i = prod_{j=s..i} (-l_j)      (Y_i = y_i + w_i Y_in)
+//     t_i = G_i / beta_i, G_s = 1, G_{i+1} = G_i g_i, g_i = -off / beta_i
+//     F0 = sum t_i y_i,  xi = sum t_i w_i,  Q = G_{e+1}         (x_s = F0 + xi Y_in + Q X_out)
+//   scan over blocks: Y_in(b+1) = y_e(b) + w_e(b) Y_in(b);  X_out(b-1) = x_s(b)
+//   backward: Y_i = y_i + w_i Y_in (w walked back with 1/(-l_i)),  x_i = (Y_i - off x_{i+1}) / beta_i
+//
+// fp64 work: 5 + 4 instructions per row and mode, 4 warps per scheduler: the
+// kernel is bound by fp64 issue, not by the latency of one chain.
+constexpr int kRPB = 64;    // rows per thread
+constexpr int kRR = 32;     // ... of which in registers
+constexpr int kNB = 16;     // row blocks (warps) per CTA
+constexpr int kBThreads = 32 * kNB;
+constexpr size_t kBSmem = size_t(kNB) * (kRPB - kRR) * 32 * 8 + size_t(kNB) * 5 * 32 * 8;
+
+struct BJob {
+    PlanDev p;
+    double *z;        // field (row pitch `pitch` doubles), swept in place
+    int pitch;
+    int cta0;         // CTAs [cta0, next job's cta0) take slices of 32 modes
+};
+struct BList {
+    int count;
+    long long *dbg;   // optional [grid][kNB][4] cycle stamps (FD_SPLIT_TIMING)
+    BJob job[kMaxPJobs];
+};
+
+__global__ void __launch_bounds__(kBThreads, 1) thomas_blocks_kernel(const __grid_constant__ BList bl) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *ycol = reinterpret_cast<double *>(smem_raw);                       // [kNB][kRPB - kRR][32]
+    double *scal = ycol + size_t(kNB) * (kRPB - kRR) * 32;                     // [kNB][5][32]
+    const int tid = threadIdx.x, lane = tid & 31, b = tid >> 5;
+    int j = 0;
+    while (j + 1 < bl.count && int(blockIdx.x) >= bl.job[j + 1].cta0) ++j;
+    const BJob &J = bl.job[j];
+    const PlanDev &p = J.p;
+    const int n = p.n, m = p.m, NP = J.pitch;
+    const int k0 = (int(blockIdx.x) - J.cta0) * 32;
+    const bool act = k0 + lane < n;
+    const int k = act ? k0 + lane : n - 1;
+    // The blocks cover rows [0, m-1); the last row (its 1/beta carries the end
+    // modifier) is one more link of the carry scan.
+    const int mb = m - 1;
+    const int s = b * kRPB;
+    const int nr = max(0, min(kRPB, mb - s));     // rows of this block (warp-uniform)
+    const int nb = (mb + kRPB - 1) / kRPB;        // blocks of the job (<= kNB)
+    double *Zj = J.z + k;
+    double *Z = Zj + size_t(s) * NP;
+    double *ys = ycol + (size_t(b) * (kRPB - kRR)) * 32 + lane;
+
+    const long long c_t0 = clock64();
+    ModeRec mr;
+    mr.load(p, k);
+    const double l_inf = mr.l_inf, ib_inf = mr.ib_inf, inv_nl = mr.inv_nl;
+    const double noff = -p.off, nio = p.nio;
+    const double g_inf = noff * ib_inf, nl_inf = -l_inf;
+    // Factors l_i, 1/beta_i, 1/(-l_i) = -beta_{i-1}/off of a row:
+    //   i < ecap: the row-major tables dl, dib, db (they hold every mode, the
+    //             fixed point filled in past a mode's transient);
+    //   i >= ecap: the mode's fixed point, except for the slowly converging
+    //             modes k < kt, which read the long-transient table lt.
+    const bool slowm = p.lt != nullptr && k < p.kt;
+    const double *ltk = p.lt + k;
+    const size_t lts = size_t(3) * p.ktp;
+    // block kind (warp-uniform): 0 fixed point, 1 tables (block below ecap), 2 mixed
+    const int ecap = p.ecap;
+    const bool any_slow = __any_sync(0xffffffffu, slowm);
+    const int kind = (s + nr <= ecap) ? 1 : ((s >= ecap && !any_slow) ? 0 : 2);
+
+    auto fac_fwd = [&](int i, double &l, double &ib) {   // kinds 1, 2
+        if (i < ecap) {
+            l = __ldg(p.dl + size_t(i) * n + k);
+            ib = __ldg(p.dib + size_t(i) * n + k);
+        } else if (slowm) {
+            l = __ldg(ltk + size_t(i) * lts);
+            ib = __ldg(ltk + size_t(i) * lts + p.ktp);
+        } else {
+            l = l_inf;
+            ib = ib_inf;
+        }
+    };
+    auto fac_bwd = [&](int i, double &ib, double &pm) {  // kinds 1, 2
+        if (i < ecap) {
+            ib = __ldg(p.dib + size_t(i) * n + k);
+            pm = (i >= 1) ? __ldg(p.db + size_t(i - 1) * n + k) * nio : 0.0;
+        } else if (slowm) {
+            ib = __ldg(ltk + size_t(i) * lts + p.ktp);
+            pm = __ldg(ltk + size_t(i) * lts + 2 * p.ktp);
+        } else {
+            ib = ib_inf;
+            pm = (i == ecap) ? __ldg(p.db + size_t(i - 1) * n + k) * nio : inv_nl;
+        }
+    };
+
+    // ---- the register rows; the other rows stream in during the forward sweep
+    double d[kRR];
+#pragma unroll
+    for (int r = 0; r < kRR; ++r) d[r] = (r < nr) ? __ldcg(Z + size_t(r) * NP) : 0.0;
+
+    // ---- forward sweep, 8 rows at a time (loads first, then the chains)
+    double y = 0.0, w = 1.0, t = nio, F0 = 0.0, xi = 0.0;
+    // full batch, fixed-point factors
+    auto fwd8c = [&](double (&v)[8]) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            y = fma(nl_inf, y, v[r]);
+            w *= nl_inf;
+            t *= g_inf;
+            F0 = fma(y, t, F0);
+            xi = fma(w, t, xi);
+            v[r] = y;
+        }
+    };
+    // batch of cnt <= 8 rows starting at block row r0, factors per row
+    auto fwd8g = [&](int r0, int cnt, double (&v)[8]) {
+        double lv[8], gv[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            lv[r] = 0.0;
+            gv[r] = 0.0;
+            if (r < cnt) fac_fwd(s + r0 + r, lv[r], gv[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            if (r < cnt) {
+                y = fma(-lv[r], y, v[r]);
+                w *= -lv[r];
+                t *= noff * gv[r];
+                F0 = fma(y, t, F0);
+                xi = fma(w, t, xi);
+                v[r] = y;
+            }
+        }
+    };
+#pragma unroll
+    for (int q = 0; q < kRR / 8; ++q) {
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = d[q * 8 + r];
+        if (kind == 0 && nr >= kRR) fwd8c(v);
+        else fwd8g(q * 8, min(8, nr - q * 8), v);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) d[q * 8 + r] = v[r];
+    }
+#pragma unroll 1
+    for (int r0 = kRR; r0 < nr; r0 += 8) {
+        const int cnt = min(8, nr - r0);
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = (r < cnt) ? __ldcg(Z + size_t(r0 + r) * NP) : 0.0;
+        if (kind == 0 && cnt == 8) fwd8c(v);
+        else fwd8g(r0, cnt, v);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) ys[(r0 - kRR + r) * 32] = v[r];
+    }
+    // block scalars: y_e, w_e, F0, xi, Q
+    {
+        double *sc = scal + size_t(b) * 5 * 32 + lane;
+        sc[0] = y;
+        sc[32] = w;
+        sc[64] = F0;
+        sc[96] = xi;
+        sc[128] = t * noff;
+    }
+    const long long c_t1 = clock64();
+    __syncthreads();
+
+    // ---- block carries: warp 0 scans the chains of the 32 modes (nb <= 16 steps
+    // each way, row m-1 in between) and leaves Y_in, X_out of every block in the
+    // scalar slots 0, 1
+    if (b == 0) {
+        double Y = 0.0;
+#pragma unroll 1
+        for (int q = 0; q < nb; ++q) {
+            double *sc = scal + size_t(q) * 5 * 32 + lane;
+            const double ye = sc[0], pe = sc[32];
+            sc[0] = Y;   // Y_in of block q
+            Y = fma(pe, Y, ye);
+        }
+        // last row: y = r - l y_{m-2}, x = y / beta_{m-1}
+        double ll = l_inf;
+        if (mb < ecap) ll = __ldg(p.dl + size_t(mb) * n + k);
+        else if (slowm) ll = __ldg(ltk + size_t(mb) * lts);
+        if (mb == 0) ll = 0.0;
+        const double yl = fma(-ll, Y, __ldcg(Zj + size_t(mb) * NP));
+        double X = yl * (1.0 / mr.b_last);
+        if (act) __stcg(Zj + size_t(mb) * NP, X);
+#pragma unroll 1
+        for (int q = nb - 1; q >= 0; --q) {
+            double *sc = scal + size_t(q) * 5 * 32 + lane;
+            const double xs = fma(sc[128], X, fma(sc[96], sc[0], sc[64]));
+            sc[32] = X;  // X_out of block q
+            X = xs;
+        }
+    }
+    __syncthreads();
+    const double Yin = scal[size_t(b) * 5 * 32 + lane], Xout = scal[size_t(b) * 5 * 32 + 32 + lane];
+    const long long c_t2 = clock64();
+
+    // ---- backward sweep: true y, then x, rows descending; results straight to Z
+    double x = Xout, Pc = w;
+    auto bwd8c = [&](double (&v)[8]) {
+#pragma unroll
+        for (int r = 7; r >= 0; --r) {
+            const double Y = fma(Pc, Yin, v[r]);
+            Pc *= inv_nl;
+            x = fma(g_inf, x, Y * ib_inf);
+            v[r] = x;
+        }
+    };
+    auto bwd8g = [&](int r0, int cnt, double (&v)[8]) {
+        double gv[8], pv[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            gv[r] = 0.0;
+            pv[r] = 0.0;
+            if (r < cnt) fac_bwd(s + r0 + r, gv[r], pv[r]);
+        }
+#pragma unroll
+        for (int r = 7; r >= 0; --r) {
+            if (r < cnt) {
+                const double Y = fma(Pc, Yin, v[r]);
+                Pc *= pv[r];
+                x = fma(noff * gv[r], x, Y * gv[r]);
+                v[r] = x;
+            }
+        }
+    };
+#pragma unroll 1
+    for (int r0 = ((nr - 1) & ~7); r0 >= kRR; r0 -= 8) {
+        const int cnt = min(8, nr - r0);
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = ys[(r0 - kRR + r) * 32];
+        if (kind == 0 && cnt == 8) bwd8c(v);
+        else bwd8g(r0, cnt, v);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            if (act && r < cnt) __stcg(Z + size_t(r0 + r) * NP, v[r]);
+    }
+#pragma unroll
+    for (int q = kRR / 8 - 1; q >= 0; --q) {
+        double v[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[r] = d[q * 8 + r];
+        if (kind == 0 && nr >= kRR) bwd8c(v);
+        else bwd8g(q * 8, min(8, nr - q * 8), v);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            if (act && q * 8 + r < nr) __stcg(Z + size_t(q * 8 + r) * NP, v[r]);
+    }
+    if (bl.dbg && lane == 0) {
+        long long *dd = bl.dbg + (size_t(blockIdx.x) * kNB + b) * 4;
+        dd[0] = c_t1 - c_t0;
+        dd[1] = c_t2 - c_t1;
+        dd[2] = clock64() - c_t2;
+        dd[3] = kind;
     }
 }
 
@@ -630,7 +939,9 @@ void run_split(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws)
     const double2 *tw = pair_twiddles<NL>(device);
     const size_t xsmem = C::REG + 16 * 8;
     static const bool timing = getenv("FD_SPLIT_TIMING") != nullptr;
-    const int n = jobs[0].p.n, NP = C::N;
+    const int n = jobs[0].p.n;
+    static const int padq = getenv("FD_SPLIT_PAD") ? atoi(getenv("FD_SPLIT_PAD")) : 16;
+    const int NP = C::N + padq;   // row pitch of Z: not a power of two (mode slices walk it row by row)
     size_t zrows = 0;
     for (size_t j0 = 0; j0 < jobs.size(); j0 += kMaxPJobs) {
         size_t r = 0;
@@ -669,7 +980,10 @@ void run_split(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws)
             a.h2 = 0.5 * p.scale;
             a.m = p.m;
             a.pairs = (p.m + 1) / 2;
+            static const bool use_tma = !getenv("FD_SPLIT_NOTMA");
+            a.tma = use_tma && (reinterpret_cast<uintptr_t>(sj.in) % 16 == 0) && (2 * size_t(n) * 8) % 16 == 0;
             c = a;
+            c.tma = use_tma;   // Z rows: even pitch, aligned base
             c.src = Zj;
             c.spitch = NP;
             c.dst = sj.out;
@@ -711,13 +1025,58 @@ void run_split(const std::vector<SolveJob> &jobs, cudaStream_t s, Workspace &ws)
         if (timing)
             for (auto &e : ev) FD_CUDA(cudaEventCreate(&e));
         if (timing) FD_CUDA(cudaEventRecord(ev[0], s));
-        dst_pair_kernel<NL><<<pairs, C::T, xsmem, s>>>(xa);
+        dst_pair_kernel<NL, true><<<pairs, C::T, xsmem, s>>>(xa);
         FD_CUDA(cudaGetLastError());
         if (timing) FD_CUDA(cudaEventRecord(ev[1], s));
-        launch_thomas(W, ctas, tsmem, s, tl, di.smem);
+        static const int bmode = getenv("FD_SPLIT") ? atoi(getenv("FD_SPLIT")) : 1;
+        bool blocks_ok = bmode != 2;
+        for (int j = 0; j < cnt; ++j) blocks_ok = blocks_ok && jobs[j0 + j].p.m <= kRPB * kNB;
+        if (blocks_ok) {
+            BList bq{};
+            bq.count = cnt;
+            int c0 = 0;
+            size_t zo = 0;
+            for (int j = 0; j < cnt; ++j) {
+                const PlanDev &p = jobs[j0 + j].p;
+                bq.job[j].p = p;
+                bq.job[j].z = Z + zo;
+                bq.job[j].pitch = NP;
+                bq.job[j].cta0 = c0;
+                c0 += (n + 31) / 32;
+                zo += size_t(p.m) * NP;
+            }
+            static std::once_flag once;
+            std::call_once(once, [] {
+                cudaFuncSetAttribute((const void *)thomas_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kBSmem);
+            });
+            long long *bdbg = nullptr;
+            if (timing) {
+                FD_CUDA(cudaMallocAsync(&bdbg, size_t(c0) * kNB * 4 * 8, s));
+                FD_CUDA(cudaMemsetAsync(bdbg, 0, size_t(c0) * kNB * 4 * 8, s));
+            }
+            bq.dbg = bdbg;
+            thomas_blocks_kernel<<<c0, kBThreads, kBSmem, s>>>(bq);
+            if (timing) {
+                std::vector<long long> hb(size_t(c0) * kNB * 4);
+                FD_CUDA(cudaMemcpyAsync(hb.data(), bdbg, hb.size() * 8, cudaMemcpyDeviceToHost, s));
+                FD_CUDA(cudaStreamSynchronize(s));
+                FD_CUDA(cudaFreeAsync(bdbg, s));
+                for (int c : {0, 10, c0 - 1}) {
+                    fprintf(stderr, "  blocks cta %d [fwd/scan/bwd cycles, kind] per warp:", c);
+                    for (int q = 0; q < kNB; ++q) {
+                        const long long *e = &hb[(size_t(c) * kNB + q) * 4];
+                        fprintf(stderr, " %lld/%lld/%lld,%lld", e[0], e[1], e[2], e[3]);
+                    }
+                    fprintf(stderr, "\n");
+                }
+            }
+        } else {
+            launch_thomas(W, ctas, tsmem, s, tl, di.smem);
+        }
         FD_CUDA(cudaGetLastError());
         if (timing) FD_CUDA(cudaEventRecord(ev[2], s));
-        dst_pair_kernel<NL><<<pairs, C::T, xsmem, s>>>(xc);
+        dst_pair_kernel<NL, false><<<pairs, C::T, xsmem, s>>>(xc);
         FD_CUDA(cudaGetLastError());
         if (timing) {
             FD_CUDA(cudaEventRecord(ev[3], s));
