@@ -40,8 +40,9 @@ struct PList {
     int count;
     int V;               // virtual row ranges (carry blocks)
     long long total_rows;
-    double *carry;       // [total_blocks][kCarryVals][n]
+    double *carry;       // [total_blocks][kCarryVals][cn]
     int n;
+    int cn;              // even row pitch of the carry rows (n rounded up): 16-byte aligned rows for bulk copies
     unsigned long long *tstamp;   // optional [gridDim][8] phase timestamps (FD_PHASE_TIMING)
     unsigned long long *trace;    // optional per-item timeline of one CTA (FD_TRACE=cta)
     int trace_cta;
@@ -289,7 +290,8 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
             blocks += pj.nblk;
             row0 += sj.p.m;
         }
-        const size_t carry_sz = size_t(blocks) * kCarryVals * pl.n;
+        pl.cn = (pl.n + 1) & ~1;
+        const size_t carry_sz = size_t(blocks) * kCarryVals * pl.cn;
         pl.carry = ws.get(carry_sz);
         pl.bsave = nullptr;
         pl.bstride = 0;

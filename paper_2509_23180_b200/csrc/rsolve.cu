@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 fss[u] = f;
                 s2s[u] = s2;
                 if (last && rb == rows) {
-                    double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
+                    const int cn = pl.cn;
+                    double *cb = pl.carry + size_t(sg.blk) * kCarryVals * cn + k;
                     const int e = sg.e;
                     // Q = pi_e * (-l_{e+1}),  l_{e+1} = delta / beta_e
                     double lnext = l_inf;
@@ -329,11 +330,11 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                         factors_slow(p, k, e + 1, len, l_inf, ib_inf, ibm, 0.0, &lnext, &ib_, &bm1_);
                     }
                     const double Q = (e < p.m - 1) ? w * (-lnext) : 0.0;
-                    __stcg(cb + 0 * n, y);
-                    __stcg(cb + 1 * n, f);
-                    __stcg(cb + 2 * n, cc * w);
-                    __stcg(cb + 3 * n, cc * s2);
-                    __stcg(cb + 4 * n, Q);
+                    __stcg(cb + 0 * cn, y);
+                    __stcg(cb + 1 * cn, f);
+                    __stcg(cb + 2 * cn, cc * w);
+                    __stcg(cb + 3 * cn, cc * s2);
+                    __stcg(cb + 4 * cn, Q);
                 }
             }
             __syncthreads();   // this part's rows consumed (after part 1: the table slice too)
@@ -357,85 +358,64 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
     // Per (job, mode) chain over the job's blocks b:
     //   Y_b = yhat_b + P_b Y_{b-1}                  (forward)
     //   X_b = F_b + Y_{b-1} xi_b + Q_b X_{b+1}      (backward)
-    // Items of (job, W modes), W ~ chains / grid so every CTA takes about one: the
-    // item's block scalars are staged in shared memory (coalesced over modes), then
-    // every warp evaluates chains as inclusive scans of the composed affine maps
-    // y -> A y + B over 32 blocks at a time (lane = block), and Y, X go back.
+    // Items of (job, W modes), W ~ chains / grid so every CTA takes about one.  The
+    // item's block scalars arrive by 16-byte async copies (the carry rows have an
+    // even pitch, so every row of W values starts 16-byte aligned), then one
+    // thread per mode walks its chain forward and back -- the jobs have a few
+    // dozen blocks, so two serial passes of FMAs over shared memory are shorter
+    // than scans of composed maps -- and Y, X go back coalesced.
     {
         const int warp = tid >> 5;
         constexpr int NW = NT / 32;
-        const size_t bs = size_t(kCarryVals) * n;
+        const int cn = pl.cn;
+        const size_t bs = size_t(kCarryVals) * cn;
         int nbmax = 1;
         for (int j = 0; j < pl.count; ++j) nbmax = max(nbmax, pl.job[j].nblk);
         const int cap = int(C::OFF_TW / (7 * 8)) / nbmax;   // modes per item that fit the regions
         const int cpj = max(1, int(gridDim.x) / pl.count);   // CTAs per job
         int W = (n + cpj - 1) / cpj;
-        W = max(1, min(min(W, 64), cap - 1));
-        const int WP = W | 1;                               // odd stride: lane-per-block reads conflict-free
+        W = max(2, min(min((W + 1) & ~1, 64), cap & ~1));    // even: rows start 16-byte aligned
         const int per_job = (n + W - 1) / W;
-        double *sv = reinterpret_cast<double *>(smem_raw);   // [nb][7][WP]
-        auto scan = [&](double &A, double &B) {   // lane l ends with f_l o ... o f_0
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double Ao = __shfl_up_sync(0xffffffffu, A, o), Bo = __shfl_up_sync(0xffffffffu, B, o);
-                if (lane >= o) {
-                    B = fma(A, Bo, B);
-                    A *= Ao;
-                }
-            }
-        };
-            for (int item = blockIdx.x; item < pl.count * per_job; item += gridDim.x) {
+        double *sv = reinterpret_cast<double *>(smem_raw);   // [nb][7][W]
+        for (int item = blockIdx.x; item < pl.count * per_job; item += gridDim.x) {
             const PJob &J = pl.job[item / per_job];
             const int k0 = (item % per_job) * W, w = min(W, n - k0);
             double *cb = pl.carry + size_t(J.blk_base) * bs + k0;
             const int nb = J.nblk;
-            // async copies global -> shared (no register round trip): every load of
-            // the item in flight at once from a small loop
+            const uint32_t rb = uint32_t((w + 1) & ~1) * 8u;   // bytes per row (the pitch pads odd n)
+            // 16-byte async copies global -> shared, every copy of the item in flight at once
+            {
+                const int cpr = int(rb / 16);   // chunks per row
+                const int total = nb * 5 * cpr;
 #pragma unroll 1
-            for (int bv = warp; bv < nb * 5; bv += NW) {
-                const int b = bv / 5, v = bv - 5 * b;
-                const double *src = cb + b * bs + v * n;
-                double *dst = sv + (b * 7 + v) * WP;
-#pragma unroll 1
-                for (int m = lane; m < w; m += 32)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst + m)), "l"(src + m)
+                for (int c = tid; c < total; c += NT) {
+                    const int bv = c / cpr, q = c - bv * cpr;
+                    const int b = bv / 5, v = bv - 5 * b;
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sv + (b * 7 + v) * W + 2 * q)),
+                                 "l"(cb + b * bs + v * cn + 2 * q)
                                  : "memory");
+                }
+                asm volatile("cp.async.wait_all;" ::: "memory");
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            trace(12, item / gridDim.x, 0);
             __syncthreads();
             trace(12, item / gridDim.x, 1);
-#pragma unroll 1
-            for (int m = warp; m < w; m += NW) {
-                double carry = 0.0;
-#pragma unroll 1
-                for (int b0 = 0; b0 < nb; b0 += 32) {
-                    const int b = b0 + lane;
-                    double A = 1.0, B = 0.0;
-                    if (b < nb) {
-                        B = sv[(b * 7 + 0) * WP + m];
-                        A = (b == 0) ? 0.0 : sv[(b * 7 + 2) * WP + m];
-                    }
-                    scan(A, B);
-                    const double Y = fma(A, carry, B);
-                    if (b < nb) sv[(b * 7 + 5) * WP + m] = Y;
-                    carry = __shfl_sync(0xffffffffu, Y, 31);
+            if (tid < w) {
+                double *c = sv + tid;
+                double Y = 0.0;
+#pragma unroll 4
+                for (int b = 0; b < nb; ++b) {
+                    const double A = (b == 0) ? 0.0 : c[(b * 7 + 2) * W];
+                    Y = fma(A, Y, c[(b * 7 + 0) * W]);
+                    c[(b * 7 + 5) * W] = Y;
                 }
-                __syncwarp();
-                carry = 0.0;
-#pragma unroll 1
-                for (int b1 = nb; b1 > 0; b1 -= 32) {
-                    const int b = b1 - 1 - lane;   // lane 0 = highest block of the chunk
-                    double A = 1.0, B = 0.0;
-                    if (b >= 0) {
-                        B = sv[(b * 7 + 1) * WP + m];
-                        if (b > 0) B = fma(sv[((b - 1) * 7 + 5) * WP + m], sv[(b * 7 + 3) * WP + m], B);
-                        A = (b < nb - 1) ? sv[(b * 7 + 4) * WP + m] : 0.0;
-                    }
-                    scan(A, B);
-                    const double X = fma(A, carry, B);
-                    if (b >= 0) sv[(b * 7 + 6) * WP + m] = X;
-                    carry = __shfl_sync(0xffffffffu, X, 31);
+                double X = 0.0;
+#pragma unroll 4
+                for (int b = nb - 1; b >= 0; --b) {
+                    double B = c[(b * 7 + 1) * W];
+                    if (b > 0) B = fma(c[((b - 1) * 7 + 5) * W], c[(b * 7 + 3) * W], B);
+                    const double A = (b < nb - 1) ? c[(b * 7 + 4) * W] : 0.0;
+                    X = fma(A, X, B);
+                    c[(b * 7 + 6) * W] = X;
                 }
             }
             trace(13, item / gridDim.x, 0);
@@ -445,7 +425,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
             for (int bv = warp; bv < nb * 2; bv += NW) {
                 const int b = bv >> 1, v = 5 + (bv & 1);
 #pragma unroll 1
-                for (int m = lane; m < w; m += 32) __stcg(cb + b * bs + v * n + m, sv[(b * 7 + v) * WP + m]);
+                for (int m = lane; m < w; m += 32) __stcg(cb + b * bs + v * cn + m, sv[(b * 7 + v) * W + m]);
             }
             __syncthreads();
             trace(14, item / gridDim.x, 0);
@@ -513,11 +493,12 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                         cibl[u] = 1.0 / c.b_last;
                         clen[u] = c.len;
                     }
-                    const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * n + k;
-                    const size_t bs = size_t(kCarryVals) * n;
-                    xs[u] = has_next ? __ldcg(cb + bs + 6 * n) : 0.0;
-                    yins[u] = has_in ? __ldcg(cb - bs + 5 * n) : 0.0;
-                    pcs[u] = __ldcg(cb + 2 * n);
+                    const int cn = pl.cn;
+                    const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * cn + k;
+                    const size_t bs = size_t(kCarryVals) * cn;
+                    xs[u] = has_next ? __ldcg(cb + bs + 6 * cn) : 0.0;
+                    yins[u] = has_in ? __ldcg(cb - bs + 5 * cn) : 0.0;
+                    pcs[u] = __ldcg(cb + 2 * cn);
                 }
                 double x = xs[u], Pc = pcs[u];
                 const double yin = yins[u];
