@@ -320,11 +320,20 @@ constexpr int kCarryModes = 32;
 constexpr int kCarryChunk = 40;
 constexpr int kCarryThreads = 256;
 
+// Jobs of at most kCarryFast blocks (the small dense problems, where this kernel
+// is a visible part of a GMRES iteration): all five block scalars of the chain
+// are fetched at once into dynamic shared memory, one thread per mode walks
+// the chain forward and back, and Y, X are stored -- one memory round trip
+// instead of one per pass and chunk.
+constexpr int kCarryFast = 96;
+constexpr size_t kCarrySmem = size_t(5) * kCarryFast * kCarryModes * sizeof(double);
+
 __global__ void __launch_bounds__(kCarryThreads) carry_kernel(const __grid_constant__ JobList jl) {
     __shared__ double sa[kCarryChunk][kCarryModes];
     __shared__ double sb[kCarryChunk][kCarryModes];
     __shared__ double sc[kCarryChunk][kCarryModes];
     __shared__ double sd[kCarryChunk][kCarryModes];
+    extern __shared__ __align__(16) double dyn[];   // [5][nb][kCarryModes] (fast path)
     const int job = find_job(jl, blockIdx.x);
     const PlanDev &p = jl.job[job].p;
     const int k0 = (blockIdx.x - jl.block_start[job]) * kCarryModes;
@@ -334,6 +343,48 @@ __global__ void __launch_bounds__(kCarryThreads) carry_kernel(const __grid_const
     const int k = k0 + lane;
     const bool ok = k < n;
     const double *Pe = p.blk;  // [nb][3][n]
+    if (nb <= kCarryFast) {
+        double *ye = dyn, *pe = ye + nb * kCarryModes, *fs = pe + nb * kCarryModes, *xi = fs + nb * kCarryModes,
+               *qq = xi + nb * kCarryModes;
+        for (int b = slot; b < nb; b += SLOTS) {
+            const int o = b * kCarryModes + lane;
+            ye[o] = ok ? p.ye[size_t(b) * n + k] : 0.0;
+            fs[o] = ok ? p.fs[size_t(b) * n + k] : 0.0;
+            pe[o] = ok ? __ldg(Pe + (size_t(b) * 3 + 0) * n + k) : 0.0;
+            xi[o] = ok ? __ldg(Pe + (size_t(b) * 3 + 1) * n + k) : 0.0;
+            qq[o] = ok ? __ldg(Pe + (size_t(b) * 3 + 2) * n + k) : 0.0;
+        }
+        __syncthreads();
+        if (slot == 0) {
+            double y = 0.0;
+#pragma unroll 4
+            for (int b = 0; b < nb; ++b) {   // Y_b = ye_b + Pe_b Y_{b-1}
+                const int o = b * kCarryModes + lane;
+                double v = ye[o];
+                if (b > 0) v = fma(pe[o], y, v);
+                ye[o] = v;
+                y = v;
+            }
+            double x = 0.0;
+#pragma unroll 4
+            for (int b = nb - 1; b >= 0; --b) {   // X_b = fs_b + Y_{b-1} xi_b + Q_b X_{b+1}
+                const int o = b * kCarryModes + lane;
+                double v = fs[o];
+                if (b > 0) v = fma(ye[o - kCarryModes], xi[o], v);
+                if (b < nb - 1) v = fma(qq[o], x, v);
+                fs[o] = v;
+                x = v;
+            }
+        }
+        __syncthreads();
+        if (ok)
+            for (int b = slot; b < nb; b += SLOTS) {
+                const int o = b * kCarryModes + lane;
+                p.ye[size_t(b) * n + k] = ye[o];
+                p.fs[size_t(b) * n + k] = fs[o];
+            }
+        return;
+    }
     // forward: Y_b = ye_b + Pe_b Y_{b-1}
     double yprev = 0.0;
 #pragma unroll 1
@@ -388,6 +439,18 @@ __global__ void __launch_bounds__(kCarryThreads) carry_kernel(const __grid_const
             if (ok) p.fs[size_t(c0 + bb) * n + k] = sa[bb][lane];
         __syncthreads();
     }
+}
+
+// dynamic shared memory of the carry kernel's fast path (0: chunked path only)
+static size_t carry_smem(const JobList &jc) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute((const void *)carry_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCarrySmem);
+    });
+    int nbmax = 0;
+    for (int j = 0; j < jc.count; ++j)
+        if (jc.job[j].p.nb <= kCarryFast) nbmax = std::max(nbmax, jc.job[j].p.nb);
+    return size_t(5) * nbmax * kCarryModes * sizeof(double);
 }
 
 // ---------------------------------------------------------------------------
@@ -643,7 +706,7 @@ static void run_sep(const std::vector<SolveJob> &jobs, cudaStream_t s) {
         jc.block_start[jc.count] = totc;
         sep_pass1_kernel<<<tot, kSepThreads, 0, s>>>(jl);
         FD_CUDA(cudaGetLastError());
-        carry_kernel<<<totc, kCarryThreads, 0, s>>>(jc);
+        carry_kernel<<<totc, kCarryThreads, carry_smem(jc), s>>>(jc);
         FD_CUDA(cudaGetLastError());
         for (int j = 0; j < jl.count; ++j) {
             const PlanDev &p = jl.job[j].p;
@@ -744,7 +807,7 @@ static void run_solve(const std::vector<SolveJob> &jobs, cudaStream_t s) {
         setup_smem<P>((const void *)pass2_kernel<P>);
         pass1_kernel<P><<<tot, P::NT, P::SMEM, s>>>(jl);
         FD_CUDA(cudaGetLastError());
-        carry_kernel<<<totc, kCarryThreads, 0, s>>>(jc);
+        carry_kernel<<<totc, kCarryThreads, carry_smem(jc), s>>>(jc);
         FD_CUDA(cudaGetLastError());
         for (int j = 0; j < jl.count; ++j) {
             const PlanDev &p = jl.job[j].p;
