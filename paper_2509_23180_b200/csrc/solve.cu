@@ -443,10 +443,16 @@ __global__ void __launch_bounds__(kCarryThreads) carry_kernel(const __grid_const
 
 // dynamic shared memory of the carry kernel's fast path (0: chunked path only)
 static size_t carry_smem(const JobList &jc) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute((const void *)carry_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCarrySmem);
-    });
+    {   // once per device
+        static std::mutex mu;
+        static std::set<int> done;
+        int dev = 0;
+        FD_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> g(mu);
+        if (done.insert(dev).second)
+            FD_CUDA(cudaFuncSetAttribute((const void *)carry_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kCarrySmem));
+    }
     int nbmax = 0;
     for (int j = 0; j < jc.count; ++j)
         if (jc.job[j].p.nb <= kCarryFast) nbmax = std::max(nbmax, jc.job[j].p.nb);
