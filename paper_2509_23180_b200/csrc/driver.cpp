@@ -18,6 +18,8 @@
 #include <sstream>
 #include <tuple>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "fd_internal.h"
 
 namespace fd {
@@ -52,6 +54,17 @@ void dfree(void *p) {
 }
 
 // FD_HOST_TIMING=1: host-side phase times of the drivers on stderr (diagnostics)
+// NVTX range of a host-side phase (header-only NVTX 3: a no-op unless a
+// profiler is attached); the ranges name the phases of Algorithm 1 in nsys /
+// ncu timelines: ddm_solve > presolves | gmres (> cycle) | backsub, schur_apply,
+// rect_solve_batched.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 struct HostTimer {
     const char *name;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
@@ -693,6 +706,7 @@ static int gmres_precond(fd_schur_s *op, const double *rhs, double *x, int x_is_
         const double beta = norm2(N, r, sc, s);
         if (beta / r0 <= tol) break;
         ++cycles;
+        NvtxRange nvtx_cycle("fd:gmres_cycle");
         std::fill(H.begin(), H.end(), 0.0);
         std::fill(g.begin(), g.end(), 0.0);
         std::fill(cs.begin(), cs.end(), 0.0);
@@ -940,6 +954,7 @@ int fd_rect_solve(fd_plan plan, const double *f, double *out, void *stream) {
 int fd_rect_solve_batched(int count, const fd_plan *plans, const double *const *f, double *const *out,
                           void *stream) {
     FD_API_BEGIN
+    NvtxRange nvtx("fd:rect_solve_batched");
     std::vector<UJob> jobs;
     for (int i = 0; i < count; ++i) {
         if (!plans[i] || !f[i] || !out[i]) FD_FAIL(FD_ERR_VALIDATION, "null argument");
@@ -1168,6 +1183,7 @@ int fd_center_solve(fd_schur op, const double *r, double *out, void *stream) {
 
 int fd_precond_apply(fd_schur op, const double *p, double *out, void *stream) {
     FD_API_BEGIN
+    NvtxRange nvtx("fd:precond_apply");
     precond_apply(op, p, out, S(stream));
     FD_API_END
 }
@@ -1204,6 +1220,8 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     cudaStream_t s = S(stream);
     HostTimer ht("ddm_solve");
     ht.mark("entry", s, false);
+    NvtxRange nvtx_solve("fd:ddm_solve");
+    nvtxRangePushA("fd:presolves");
     const size_t nnb = op->nb.size();
     const long long Nc = (long long)op->center->m * op->center->n;
     // pre-solves q_i = A_i^{-1} f_i into the caller's output fields (ddm.py:249-250)
@@ -1226,9 +1244,15 @@ int fd_ddm_solve(fd_schur op, const double *f_center, const double *const *f_nb,
     FD_CUDA(cudaMallocAsync(&rhs, sizeof(double) * Nc, s));
     center_solve(op, fp, rhs, 1.0, 0.0, nullptr, s);
     ht.mark("presolves+rhs", s);
+    nvtxRangePop();
     std::vector<double> hist;
-    int st = gmres_precond(op, rhs, p_center, 1, m, tol, max_restarts, hist, rep, s);
+    int st;
+    {
+        NvtxRange nvtx_gmres("fd:gmres");
+        st = gmres_precond(op, rhs, p_center, 1, m, tol, max_restarts, hist, rep, s);
+    }
     ht.mark("gmres", s);
+    NvtxRange nvtx_back("fd:residual+backsub");
     copy_hist(hist, history, hist_cap, rep);
     // true residual ||(A_c - S) x - f'|| (krylov.py:189); rhs buffer reused
     unprecond_apply(op, p_center, rhs, s);
