@@ -329,11 +329,14 @@ constexpr int kCarryFast = 96;
 constexpr size_t kCarrySmem = size_t(5) * kCarryFast * kCarryModes * sizeof(double);
 
 __global__ void __launch_bounds__(kCarryThreads) carry_kernel(const __grid_constant__ JobList jl) {
-    __shared__ double sa[kCarryChunk][kCarryModes];
-    __shared__ double sb[kCarryChunk][kCarryModes];
-    __shared__ double sc[kCarryChunk][kCarryModes];
-    __shared__ double sd[kCarryChunk][kCarryModes];
-    extern __shared__ __align__(16) double dyn[];   // [5][nb][kCarryModes] (fast path)
+    // one dynamic buffer: [5][nb][kCarryModes] on the fast path, four chunk
+    // arrays on the chunked path (no static arrays on top: a kernel whose
+    // shared-memory footprint differs a lot from its neighbours' makes the SM
+    // re-partition L1 / shared memory at every switch)
+    extern __shared__ __align__(16) double dyn[];
+    typedef double (*ChunkArr)[kCarryModes];
+    ChunkArr sa = reinterpret_cast<ChunkArr>(dyn);
+    ChunkArr sb = sa + kCarryChunk, sc = sb + kCarryChunk, sd = sc + kCarryChunk;
     const int job = find_job(jl, blockIdx.x);
     const PlanDev &p = jl.job[job].p;
     const int k0 = (blockIdx.x - jl.block_start[job]) * kCarryModes;
@@ -454,9 +457,14 @@ static size_t carry_smem(const JobList &jc) {
                                          (int)kCarrySmem));
     }
     int nbmax = 0;
-    for (int j = 0; j < jc.count; ++j)
+    bool chunked = false;
+    for (int j = 0; j < jc.count; ++j) {
         if (jc.job[j].p.nb <= kCarryFast) nbmax = std::max(nbmax, jc.job[j].p.nb);
-    return size_t(5) * nbmax * kCarryModes * sizeof(double);
+        else chunked = true;
+    }
+    const size_t fast = size_t(5) * nbmax * kCarryModes * sizeof(double);
+    const size_t chunk = chunked ? size_t(4) * kCarryChunk * kCarryModes * sizeof(double) : 0;
+    return std::max(fast, chunk);
 }
 
 // ---------------------------------------------------------------------------
