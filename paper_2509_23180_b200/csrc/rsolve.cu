@@ -50,6 +50,10 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
     __shared__ __align__(8) uint64_t ltbar;
     __shared__ Seg segs[kMaxSegs];
     __shared__ int nseg_s, nitems_s;
+    // >= 4 modes per thread (N >= 2048): the sweeps' per-mode state and factors live
+    // in tensor memory between the row groups (one CTA per SM owns all 512 columns)
+    constexpr bool kTm = MPT >= 4;
+    __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int n = pl.n;
@@ -105,7 +109,16 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
         for (int q = tid; q < C::NB; q += NT) la[q] = __ldg(tw + 2 * q);
         for (int q = tid; q < N; q += NT) al[q] = __ldg(ra + q);
     }
+    if constexpr (kTm) {
+        if (tid < 32) tmem_alloc512(&tmem_base_s);
+        tmem_fence_before();
+    }
     __syncthreads();
+    uint32_t tm = 0;   // this thread's slots: lane quarter of its warp, 128 columns per warp
+    if constexpr (kTm) {
+        tmem_fence_after();
+        tm = tmem_base_s + ((uint32_t(tid >> 5) & 3u) << 21) + (uint32_t(tid >> 7) << 7);
+    }
     const int nseg = nseg_s, nitems = nitems_s;
     uint32_t ppar = 0, ltpar = 0;
 
@@ -155,10 +168,10 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 
     // ===================== phase 1: DST + local forward elimination ===================
     {
-        constexpr bool kReload = MPT >= 4;
-        double ys[MPT], pis[MPT], fss[MPT], s2s[MPT], ccs[MPT];
-        double cl[kReload ? 1 : MPT], cib[kReload ? 1 : MPT], cibl[kReload ? 1 : MPT];
-        int clen[kReload ? 1 : MPT];
+        constexpr int SR = kTm ? 1 : MPT;   // per-mode state in registers (short transforms)
+        double ys[SR], pis[SR], fss[SR], s2s[SR], ccs[SR];
+        double cl[SR], cib[SR], cibl[SR];
+        int clen[SR];
         Tail tail{0.0, -1};
         if (nitems > 0) {
             int si, g0, rows;
@@ -207,37 +220,10 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 #pragma unroll 1
             for (int part = 0; part < 2; ++part) {
             const int ra = part ? half : 0, rb = part ? rows : half;
-#pragma unroll
-            for (int u = 0; u < MPT; ++u) {
-                const int k = tid + u * NT;
-                if (k >= n || ra >= rb || (FD_DIAG && (pl.dbg & 16))) continue;
-                double y = ys[u], w = pis[u], f = fss[u], s2 = s2s[u];
-                int len;
-                double l_inf, ib_inf, ibm;
-                if constexpr (kReload) {
-                    // many modes per thread: the per-mode constants are re-read from
-                    // the (L2-resident) mode records each part instead of living in
-                    // registers across the transforms
-                    const double2 *rec = reinterpret_cast<const double2 *>(p.mode) + 4 * k;
-                    const double2 a = __ldg(rec), d = __ldg(rec + 3);
-                    l_inf = a.x;
-                    ib_inf = a.y;
-                    len = int(__double_as_longlong(d.y));
-                    ibm = (g0 + rb - 1 >= p.m - 1) ? 1.0 / mode_blast(p, k) : ib_inf;
-                } else {
-                    if (first && part == 0) {
-                        ModeRec c;
-                        c.load(p, k);
-                        cl[u] = c.l_inf;
-                        cib[u] = c.ib_inf;
-                        cibl[u] = 1.0 / c.b_last;
-                        clen[u] = c.len;
-                    }
-                    len = clen[u];
-                    l_inf = cl[u];
-                    ib_inf = cib[u];
-                    ibm = cibl[u];
-                }
+            // one mode's rows [ra, rb) of the group: local forward elimination and
+            // block scalars; the state (y, w, f, s2, cc) lives with the caller
+            auto sweep1 = [&](int k, double &y, double &w, double &f, double &s2, double &ccr, double l_inf,
+                              double ib_inf, double ibm, int len) {
                 const int xk = xi(k);
                 double *og = outg + k;
                 // one row of the local forward elimination (rectsolver.py:86) with
@@ -269,7 +255,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                     w = 1.0;
                     f = y * ib0;
                     s2 = ib0;
-                    ccs[u] = (g0 == 0) ? 0.0 : -l0;
+                    ccr = (g0 == 0) ? 0.0 : -l0;
                     og[0] = y;
                     rr = 1;
                 }
@@ -311,11 +297,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                         for (; rr < rb; ++rr) step(rr, l_inf, (g0 + rr == mlast) ? ibm : ib_inf);
                     }
                 }
-                const double cc = ccs[u];
-                ys[u] = y;
-                pis[u] = w;
-                fss[u] = f;
-                s2s[u] = s2;
+                const double cc = ccr;
                 if (last && rb == rows) {
                     const int cn = pl.cn;
                     double *cb = pl.carry + size_t(sg.blk) * kCarryVals * cn + k;
@@ -335,6 +317,60 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                     __stcg(cb + 2 * cn, cc * w);
                     __stcg(cb + 3 * cn, cc * s2);
                     __stcg(cb + 4 * cn, Q);
+                }
+            };
+            if constexpr (kTm) {
+                // long transforms: a mode's state and fixed-point factors live in one
+                // 8-double tensor-memory slot of the thread (y, w, f, s2, cc, l_inf,
+                // 1/beta_inf, fixed-point row); the factors are fetched once per
+                // segment, every fetch of the thread in flight at once
+                if (first && ra == 0) {
+                    double2 ca[MPT];
+                    double cd[MPT];
+#pragma unroll
+                    for (int u = 0; u < MPT; ++u) {
+                        const double2 *rec = reinterpret_cast<const double2 *>(p.mode) + 4 * min(tid + u * NT, n - 1);
+                        ca[u] = __ldg(rec);
+                        cd[u] = __ldg(reinterpret_cast<const double *>(rec + 3) + 1);
+                    }
+#pragma unroll
+                    for (int u = 0; u < MPT; ++u) {
+                        const double st[8] = {0.0, 0.0, 0.0, 0.0, 0.0, ca[u].x, ca[u].y, cd[u]};
+                        tmem_st8d(tm + u * 16, st);
+                    }
+                    tmem_wait_st();
+                }
+                if (ra < rb) {
+#pragma unroll
+                    for (int u = 0; u < MPT; ++u) {
+                        const int k = tid + u * NT;
+                        double st[8];
+                        __syncwarp();
+                        tmem_ld8d(tm + u * 16, st);
+                        if (k < n && !(FD_DIAG && (pl.dbg & 16))) {
+                            const double ibm = (g0 + rb - 1 >= p.m - 1) ? 1.0 / mode_blast(p, k) : st[6];
+                            sweep1(k, st[0], st[1], st[2], st[3], st[4], st[5], st[6], ibm,
+                                   int(__double_as_longlong(st[7])));
+                        }
+                        __syncwarp();
+                        tmem_st8d(tm + u * 16, st);
+                    }
+                    tmem_wait_st();
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < MPT; ++u) {
+                    const int k = tid + u * NT;
+                    if (k >= n || ra >= rb || (FD_DIAG && (pl.dbg & 16))) continue;
+                    if (first && part == 0) {
+                        ModeRec c;
+                        c.load(p, k);
+                        cl[u] = c.l_inf;
+                        cib[u] = c.ib_inf;
+                        cibl[u] = 1.0 / c.b_last;
+                        clen[u] = c.len;
+                    }
+                    sweep1(k, ys[u], pis[u], fss[u], s2s[u], ccs[u], cl[u], cib[u], cibl[u], clen[u]);
                 }
             }
             __syncthreads();   // this part's rows consumed (after part 1: the table slice too)
@@ -437,10 +473,10 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
 
     // ===================== phase 3: back-substitution + inverse DST ===================
     {
-        constexpr bool kReload = MPT >= 4;
-        double xs[MPT], yins[MPT], pcs[MPT];
-        double cib_inf[kReload ? 1 : MPT], cinv[kReload ? 1 : MPT], cibl[kReload ? 1 : MPT];
-        int clen[kReload ? 1 : MPT];
+        constexpr int SR = kTm ? 1 : MPT;
+        double xs[SR], yins[SR], pcs[SR];
+        double cib_inf[SR], cinv[SR], cibl[SR];
+        int clen[SR];
         Tail tail{0.0, -1};
         if (nitems > 0) {
             int si, g0, rows;
@@ -480,43 +516,10 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
             }
             trace(2, it, 1);
             auto yrow = [&](int rr) { return regd(rr >> 1) + so + (rr & 1) * n; };
-#pragma unroll
-            for (int u = 0; u < MPT; ++u) {
-                const int k = tid + u * NT;
-                if (k >= n || (FD_DIAG && (pl.dbg & 64))) continue;
-                if (top) {
-                    if constexpr (!kReload) {
-                        ModeRec c;
-                        c.load(p, k);
-                        cib_inf[u] = c.ib_inf;
-                        cinv[u] = c.inv_nl;
-                        cibl[u] = 1.0 / c.b_last;
-                        clen[u] = c.len;
-                    }
-                    const int cn = pl.cn;
-                    const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * cn + k;
-                    const size_t bs = size_t(kCarryVals) * cn;
-                    xs[u] = has_next ? __ldcg(cb + bs + 6 * cn) : 0.0;
-                    yins[u] = has_in ? __ldcg(cb - bs + 5 * cn) : 0.0;
-                    pcs[u] = __ldcg(cb + 2 * cn);
-                }
-                double x = xs[u], Pc = pcs[u];
-                const double yin = yins[u];
-                int len;
-                double ib_inf, inl_, iblast;
-                if constexpr (kReload) {   // see phase 1
-                    const double2 *rec = reinterpret_cast<const double2 *>(p.mode) + 4 * k;
-                    const double2 a = __ldg(rec), b = __ldg(rec + 1), d = __ldg(rec + 3);
-                    ib_inf = a.y;
-                    inl_ = b.y;
-                    len = int(__double_as_longlong(d.y));
-                    iblast = (g0 + rows - 1 >= p.m - 1) ? 1.0 / mode_blast(p, k) : ib_inf;
-                } else {
-                    len = clen[u];
-                    ib_inf = cib_inf[u];
-                    inl_ = cinv[u];
-                    iblast = cibl[u];
-                }
+            // one mode's rows of the group, descending: carry fix-up and
+            // back-substitution in place on the staged rows
+            auto sweep3 = [&](int k, double &x, double &Pc, double yin, double ib_inf, double inl_, double iblast,
+                              int len) {
                 if (k < p.kt) {
                     const double *tb = lts + k;
 #pragma unroll 4
@@ -601,8 +604,67 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                         }
                     }
                 }
-                xs[u] = x;
-                pcs[u] = Pc;
+            };
+            if constexpr (kTm) {
+                // slot: x, P, Y_in, 1/beta_inf, 1/(-l_inf), fixed-point row (see phase 1)
+                if (top) {
+                    double cx[MPT], cy[MPT], cp[MPT], cib[MPT], cnl[MPT], cd[MPT];
+                    const int cn = pl.cn;
+                    const size_t bs = size_t(kCarryVals) * cn;
+#pragma unroll
+                    for (int u = 0; u < MPT; ++u) {
+                        const int k = min(tid + u * NT, n - 1);
+                        const double *rec = p.mode + 8 * size_t(k);
+                        const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * cn + k;
+                        cib[u] = __ldg(rec + 1);
+                        cnl[u] = __ldg(rec + 3);
+                        cd[u] = __ldg(rec + 7);
+                        cx[u] = has_next ? __ldcg(cb + bs + 6 * cn) : 0.0;
+                        cy[u] = has_in ? __ldcg(cb - bs + 5 * cn) : 0.0;
+                        cp[u] = __ldcg(cb + 2 * cn);
+                    }
+#pragma unroll
+                    for (int u = 0; u < MPT; ++u) {
+                        const double st[8] = {cx[u], cp[u], cy[u], cib[u], cnl[u], cd[u], 0.0, 0.0};
+                        tmem_st8d(tm + u * 16, st);
+                    }
+                    tmem_wait_st();
+                }
+#pragma unroll
+                for (int u = 0; u < MPT; ++u) {
+                    const int k = tid + u * NT;
+                    double st[8];
+                    __syncwarp();
+                    tmem_ld8d(tm + u * 16, st);
+                    if (k < n && !(FD_DIAG && (pl.dbg & 64))) {
+                        const double iblast = (g0 + rows - 1 >= p.m - 1) ? 1.0 / mode_blast(p, k) : st[3];
+                        sweep3(k, st[0], st[1], st[2], st[3], st[4], iblast, int(__double_as_longlong(st[5])));
+                    }
+                    __syncwarp();
+                    tmem_st8d(tm + u * 16, st);
+                }
+                tmem_wait_st();
+            } else {
+#pragma unroll
+                for (int u = 0; u < MPT; ++u) {
+                    const int k = tid + u * NT;
+                    if (k >= n || (FD_DIAG && (pl.dbg & 64))) continue;
+                    if (top) {
+                        ModeRec c;
+                        c.load(p, k);
+                        cib_inf[u] = c.ib_inf;
+                        cinv[u] = c.inv_nl;
+                        cibl[u] = 1.0 / c.b_last;
+                        clen[u] = c.len;
+                        const int cn = pl.cn;
+                        const double *cb = pl.carry + size_t(sg.blk) * kCarryVals * cn + k;
+                        const size_t bs = size_t(kCarryVals) * cn;
+                        xs[u] = has_next ? __ldcg(cb + bs + 6 * cn) : 0.0;
+                        yins[u] = has_in ? __ldcg(cb - bs + 5 * cn) : 0.0;
+                        pcs[u] = __ldcg(cb + 2 * cn);
+                    }
+                    sweep3(k, xs[u], pcs[u], yins[u], cib_inf[u], cinv[u], cibl[u], clen[u]);
+                }
             }
             trace(5, it, 0);
             __syncthreads();   // swept rows complete, table slice consumed
@@ -651,6 +713,14 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
         }
     }
     stamp(5);
+    if constexpr (kTm) {
+        tmem_fence_before();
+        __syncthreads();
+        if (tid < 32) {
+            tmem_fence_after();
+            tmem_dealloc512(tmem_base_s);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------

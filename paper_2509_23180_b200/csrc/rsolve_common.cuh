@@ -282,6 +282,42 @@ __device__ __forceinline__ void tmem_ld2(uint32_t taddr, double &a, double &b) {
     b = __longlong_as_double((long long)(((unsigned long long)r3 << 32) | r2));
 }
 
+// eight doubles <-> 16 consecutive columns of this thread's lane (warp-collective).
+// The sweeps of the long transforms (>= 4 modes per thread) keep each mode's
+// recurrence state and fixed-point factors in one such slot, so nothing of it
+// occupies registers (or spills) across the transforms.
+__device__ __forceinline__ void tmem_ld8d(uint32_t taddr, double (&d)[8]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+    // the registers are valid only after the wait: tie them to it
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+                 :
+                 : "memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = __hiloint2double(int(r[2 * i + 1]), int(r[2 * i]));
+}
+__device__ __forceinline__ void tmem_st8d(uint32_t taddr, const double (&d)[8]) {
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        r[2 * i] = uint32_t(__double2loint(d[i]));
+        r[2 * i + 1] = uint32_t(__double2hiint(d[i]));
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
 // Phase 2 of the persistent solves: block carries (see rsolve.cu).  All NT
 // threads of the CTA; the first cap_bytes of shared memory are scratch.
 template <int NT>
