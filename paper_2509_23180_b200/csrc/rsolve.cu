@@ -27,6 +27,14 @@
 // FD_DIAG=1 (build flag) compiles in the per-item trace and the FD_DBG
 // component-skip bits used by the timing studies in DESIGN.md; off by default
 // so the production kernel carries no diagnostic code.
+// unroll factor of the per-mode loops of the tensor-memory sweeps (>= 4 modes per
+// thread): 1 keeps one copy of the sweep body in the instruction stream
+#ifndef FD_TM_MIN_MPT
+#define FD_TM_MIN_MPT 4
+#endif
+#ifndef FD_TM_UNROLL
+#define FD_TM_UNROLL 1
+#endif
 #ifndef FD_DIAG
 #define FD_DIAG 0
 #endif
@@ -52,7 +60,8 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
     __shared__ int nseg_s, nitems_s;
     // >= 4 modes per thread (N >= 2048): the sweeps' per-mode state and factors live
     // in tensor memory between the row groups (one CTA per SM owns all 512 columns)
-    constexpr bool kTm = MPT >= 4;
+    constexpr bool kTm = MPT >= FD_TM_MIN_MPT;
+    constexpr int kTmUnroll = FD_TM_UNROLL;
     __shared__ uint32_t tmem_base_s;
 
     const int tid = threadIdx.x, lane = tid & 31;
@@ -341,7 +350,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                     tmem_wait_st();
                 }
                 if (ra < rb) {
-#pragma unroll
+#pragma unroll kTmUnroll
                     for (int u = 0; u < MPT; ++u) {
                         const int k = tid + u * NT;
                         double st[8];
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                     }
                     tmem_wait_st();
                 }
-#pragma unroll
+#pragma unroll kTmUnroll
                 for (int u = 0; u < MPT; ++u) {
                     const int k = tid + u * NT;
                     double st[8];
