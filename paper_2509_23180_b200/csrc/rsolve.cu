@@ -30,7 +30,7 @@
 // unroll factor of the per-mode loops of the tensor-memory sweeps (>= 4 modes per
 // thread): 1 keeps one copy of the sweep body in the instruction stream
 #ifndef FD_TM_MIN_MPT
-#define FD_TM_MIN_MPT 4
+#define FD_TM_MIN_MPT 2
 #endif
 #ifndef FD_TM_UNROLL
 #define FD_TM_UNROLL 1

@@ -182,7 +182,10 @@ struct RFft {
         }
     }
     // full transform of the staged rows A (, B) -> padded X rows in the same region
-    __device__ __forceinline__ static void run(double2 *buf, const double *A, const double *B, const double *al,
+#ifndef FD_FFT_INLINE
+#define FD_FFT_INLINE __forceinline__
+#endif
+    __device__ FD_FFT_INLINE static void run(double2 *buf, const double *A, const double *B, const double *al,
                                             double h2, const double2 *m16, const double2 *la, double *scr, int t,
                                             int pr, int lane, double *XA, double *XB,
                                             long long *dbgp = nullptr) {
