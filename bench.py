@@ -273,18 +273,21 @@ def full_solve(dev, name="c2", reps=3):
     c4 = {}
     for variant, kw in (("default", {}), ("interface_only", {"interface_only": True})):
         ts = []
-        for _ in range(2):
+        for _ in range(3):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             comp4, f4, ex4, meta4 = configs.build_cross_case("c4", device=True)
             fields4, rep4 = ddm.ddm_solve(comp4, f4, cfg, **kw)
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
-        c4[variant] = {"iterations": rep4.iterations, "wall_s": min(ts), "value": meta4["points"] / min(ts),
-                       "rel_l2_vs_exact": configs.rel_l2_device(fields4, ex4)}
+            if len(ts) < 3:
+                del fields4, f4, ex4
+        wall4 = float(np.median(ts[1:]))
+        c4[variant] = {"iterations": rep4.iterations, "wall_s": wall4, "value": meta4["points"] / wall4,
+                       "first_call_wall_s": ts[0], "rel_l2_vs_exact": configs.rel_l2_device(fields4, ex4)}
         del fields4, f4, ex4
     out["c4_device_assembled"] = dict(c4, points=meta4["points"],
-                                      timing="assembly + ddm_solve, best of 2 (the first call of each builds plan tables)",
+                                      timing="assembly + ddm_solve, median of 2 calls after a first call that builds the plan tables",
                                       reference=golden_ref("c4"))
     # c3 (84M points, kappa = -100, random RHS) and c0 (latency-bound), RHS on the device
     for extra in ("c3", "c0"):
