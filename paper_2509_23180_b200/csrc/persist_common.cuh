@@ -212,6 +212,9 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
         for (int j = 0; j < pl.count; ++j) total += jobs[j0 + j].p.m;
         pl.total_rows = total;
         long long V = std::max<long long>(grid, (total + kMaxRowsPerBlock - 1) / kMaxRowsPerBlock);
+        // more ranges than CTAs (long batches, rows-per-block cap): a whole number of
+        // ranges per CTA, or some CTAs would sweep one range more than the others
+        if (V > grid && (V + grid - 1) / grid * grid <= kMaxV) V = (V + grid - 1) / grid * grid;
         V = std::min<long long>(std::min<long long>(V, total), kMaxV);
         pl.V = (int)V;
         // Cost-balanced ranges: a row weighs 1 + tau1 * (fraction of modes in
