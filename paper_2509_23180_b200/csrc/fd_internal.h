@@ -50,6 +50,8 @@ struct Error {
 // i < ex_len[k] are stored explicitly at ex_off[k] + i; rows >= ex_len[k]
 // (a multiple of R) carry the bitwise fixed point (l_inf, beta_inf).  Row m-1
 // always uses last_b (it carries the east end modifier).
+constexpr int kLtNarrow = 32;   // modes of the narrow slow-mode table: the sweeps' first warp
+
 struct PlanDev {
     int m, n, R, nb;
     double off;          // delta_x: constant off-diagonal of the sweep system
@@ -64,8 +66,14 @@ struct PlanDev {
     const double *mode;  // [n][8]: l_inf, 1/b_inf, b_inf, 1/(-l_inf), b_last, lambda, ex_off, fixed-point row (int64 bits)
     int ecap;            // rows [0, ecap) of every mode also stored row-major (coalesced):
     const double *dl, *dib, *db;   // [ecap][n] lower, 1/beta, beta
-    int kt, ktp;         // slowly converging modes k < kt: row-major table (ktp = kt rounded to even)
-    const double *lt;    // [m][3][ktp]: l_i, 1/beta_i, -beta_{i-1}/delta
+    // slowly converging modes k < kt (ktp = kt rounded to even): row-major factor tables
+    // (l_i, 1/beta_i, -beta_{i-1}/delta).  Row groups starting before lt_need read all kt
+    // modes from the wide table; from lt_need on every mode >= kLtNarrow is on its fixed
+    // point and only the first kta modes are read, from the narrow table
+    int kt, ktp, kta, ktpa;
+    int lt_rows, lt_need;
+    const double *lt;    // [lt_rows][3][ktp], lt_rows >= lt_need + one group of rows
+    const double *lta;   // [m][3][ktpa]
     const double *blk;   // [nb][3][n]: Pe, xi_s, Q per block and mode
     double *ye;          // [nb][n] pass-1 local forward value at block end -> Y carries
     double *fs;          // [nb][n] pass-1 local backward value at block start -> X carries

@@ -150,7 +150,9 @@ struct HostTables {
     std::vector<int> bad_modes;
     std::vector<double> lam;   // eigenvalues lambda_k (+ kappa)
     std::vector<int> fix;      // first row of the bitwise fixed point (m if none)
-    std::vector<double> lt;    // [m][3][ktp] l_i, 1/beta_i, -beta_{i-1}/delta for modes < kt
+    std::vector<double> lt;    // [lt_rows][3][ktp] l_i, 1/beta_i, -beta_{i-1}/delta for modes < kt
+    std::vector<double> lta;   // [m][3][ktpa] the same for the first kta = min(kt, kLtNarrow) modes
+    int kta = 0, ktpa = 0, lt_rows = 0, lt_need = 0;
     std::vector<std::vector<double>> fl, fb;   // per mode: explicit l_i, beta_i (i < len)
     int kt = 0, ktp = 0;
     long long explicit_rows = 0;
@@ -338,8 +340,12 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
     return T;
 }
 
-// Row-major factor table of the slowly converging lowest modes (persistent
-// kernel): modes k < kt whose fixed point is >= kLongTransient rows away.
+// Row-major factor tables of the slowly converging lowest modes (persistent
+// kernel): modes k < kt whose fixed point is >= kLongTransient rows away.  Two
+// tables: the wide one [lt_rows][3][ktp] holds all kt modes down to the row
+// where every mode >= kLtNarrow has reached its fixed point (+ one group of
+// rows); below it only the first kLtNarrow modes (one warp of the sweeps) are
+// still in their transient, and the narrow table [m][3][ktpa] holds just those.
 constexpr int kLongTransient = 48;
 static void build_long_table(HostTables &T, int m, int n, double off, int kt_cap) {
     int kt = 0;
@@ -348,22 +354,32 @@ static void build_long_table(HostTables &T, int m, int n, double off, int kt_cap
     kt = std::min(kt, kt_cap);
     T.kt = kt;
     T.ktp = (kt + 1) & ~1;
+    T.kta = std::min(kt, kLtNarrow);
+    T.ktpa = (T.kta + 1) & ~1;
+    T.lt_need = 0;
+    for (int k = kLtNarrow; k < kt; ++k) T.lt_need = std::max(T.lt_need, std::min(T.fix[k], m));
+    T.lt_rows = kt > kLtNarrow ? std::min(m, T.lt_need + 16) : 0;
     if (kt == 0) return;
-    T.lt.assign(size_t(m) * 3 * T.ktp, 0.0);
-    const int ktp = T.ktp;
-    parallel_for(m, [&](int i0, int i1) {
-        for (int i = i0; i < i1; ++i) {
-            double *r = &T.lt[size_t(i) * 3 * ktp];
-            for (int k = 0; k < kt; ++k) {
-                const int len = T.len[k];
-                auto gl = [&](int q) { return q < len ? T.fl[k][q] : T.cv[4 * k + 0]; };
-                auto gb = [&](int q) { return q == m - 1 ? T.last[2 * k] : (q < len ? T.fb[k][q] : T.cv[4 * k + 2]); };
-                r[k] = (i == 0) ? 0.0 : gl(i);
-                r[ktp + k] = 1.0 / gb(i);
-                r[2 * ktp + k] = (i == 0) ? 0.0 : -gb(i - 1) / off;
+    auto fill = [&](std::vector<double> &tab, int rows, int cnt, int pitch) {
+        tab.assign(size_t(rows) * 3 * pitch, 0.0);
+        parallel_for(rows, [&](int i0, int i1) {
+            for (int i = i0; i < i1; ++i) {
+                double *r = &tab[size_t(i) * 3 * pitch];
+                for (int k = 0; k < cnt; ++k) {
+                    const int len = T.len[k];
+                    auto gl = [&](int q) { return q < len ? T.fl[k][q] : T.cv[4 * k + 0]; };
+                    auto gb = [&](int q) {
+                        return q == m - 1 ? T.last[2 * k] : (q < len ? T.fb[k][q] : T.cv[4 * k + 2]);
+                    };
+                    r[k] = (i == 0) ? 0.0 : gl(i);
+                    r[pitch + k] = 1.0 / gb(i);
+                    r[2 * pitch + k] = (i == 0) ? 0.0 : -gb(i - 1) / off;
+                }
             }
-        }
-    });
+        });
+    };
+    fill(T.lta, m, T.kta, T.ktpa);
+    if (T.lt_rows > 0) fill(T.lt, T.lt_rows, kt, T.ktp);
 }
 
 // ---------------------------------------------------------------------------
@@ -522,6 +538,10 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         }
         d.kt = T.kt;
         d.ktp = T.ktp;
+        d.kta = T.kta;
+        d.ktpa = T.ktpa;
+        d.lt_rows = T.lt_rows;
+        d.lt_need = T.lt_need;
         {   // transient profile of the table-free modes (row partition cost model)
             int tl = 0;
             for (int k = T.kt; k < n; ++k) tl = std::max(tl, T.len[k]);
@@ -535,7 +555,8 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
                 p->tprof[i] = float(alive) / float(n);
             }
         }
-        d.lt = T.kt ? upload(p, T.lt) : nullptr;
+        d.lta = T.kt ? upload(p, T.lta) : nullptr;
+        d.lt = T.lt_rows ? upload(p, T.lt) : d.lta;
         d.blk = T.blk.empty() ? nullptr : upload(p, T.blk);
         d.ye = d.fs = nullptr;   // per-plan scratch (plan_create)
         d.tw = tk == kFFT ? twiddles_for(device, n) : nullptr;

@@ -162,11 +162,15 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
         }
         return tl;
     };
+    // slow-mode factor slice of a group: all kt modes before row lt_need, the
+    // first kta (one warp's) after it, where every other mode is on its fixed point
     auto issue_lts = [&](const PlanDev &p, int g0, int rows) {
-        const uint32_t bytes = uint32_t(rows) * 3u * uint32_t(p.ktp) * 8u;
+        const bool wide = g0 < p.lt_need;
+        const int pitch = wide ? p.ktp : p.ktpa;
+        const uint32_t bytes = uint32_t(rows) * 3u * uint32_t(pitch) * 8u;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(&ltbar, bytes);
-        tma_load_1d(lts, p.lt + size_t(g0) * 3 * p.ktp, bytes, &ltbar);
+        tma_load_1d(lts, (wide ? p.lt : p.lta) + size_t(g0) * 3 * pitch, bytes, &ltbar);
     };
     auto pair_tail = [&](const double *base, int g0, int rows, int m) {
         const int r0 = 2 * pr, rp = min(2, rows - r0);
@@ -198,6 +202,8 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
             const PlanDev &p = J.p;
             const int so = stg_off(J.in, g0, n);
             const int rp = min(2, rows - 2 * pr);
+            // modes read from the staged table slice in this group, and its pitch
+            const int ktg = g0 < p.lt_need ? p.kt : p.kta, ktpg = g0 < p.lt_need ? p.ktp : p.ktpa;
             trace(0, it, 0);
             if (rp > 0) {
                 mbar_wait(&pbar[pr], (ppar >> pr) & 1u);
@@ -248,9 +254,9 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                 int rr = ra;
                 if (first && ra == 0) {   // block start: y = r, pi = 1, P_i = -l_s pi_i
                     double l0 = l_inf, ib0 = (g0 == mlast) ? ibm : ib_inf;
-                    if (k < p.kt) {
+                    if (k < ktg) {
                         l0 = lts[k];
-                        ib0 = lts[p.ktp + k];
+                        ib0 = lts[ktpg + k];
                     } else if (g0 < len) {
                         if (g0 < p.ecap) {
                             l0 = __ldg(p.dl + size_t(g0) * n + k);
@@ -268,11 +274,11 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                     og[0] = y;
                     rr = 1;
                 }
-                if (k < p.kt) {
+                if (k < ktg) {
                     // slowly converging low mode: reference factors from the table
                     const double *tb = lts + k;
 #pragma unroll 4
-                    for (; rr < rb; ++rr) step(rr, tb[rr * 3 * p.ktp], tb[rr * 3 * p.ktp + p.ktp]);
+                    for (; rr < rb; ++rr) step(rr, tb[rr * 3 * ktpg], tb[rr * 3 * ktpg + ktpg]);
                 } else if (g0 + rr < len && g0 + rb <= p.ecap) {
                     // transient rows: the reference factors (rectsolver.py:72-73) from
                     // the row-major tables, 8 rows of loads ahead of their sweep
@@ -313,7 +319,12 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                     const int e = sg.e;
                     // Q = pi_e * (-l_{e+1}),  l_{e+1} = delta / beta_e
                     double lnext = l_inf;
-                    if (k < p.kt) lnext = (e + 1 < p.m) ? __ldg(p.lt + size_t(e + 1) * 3 * p.ktp + k) : 0.0;
+                    if (k < p.kt && e + 1 < p.lt_need)
+                        lnext = __ldg(p.lt + size_t(e + 1) * 3 * p.ktp + k);
+                    else if (k < p.kta)
+                        lnext = (e + 1 < p.m) ? __ldg(p.lta + size_t(e + 1) * 3 * p.ktpa + k) : 0.0;
+                    else if (k < p.kt)
+                        lnext = l_inf;
                     else if (e + 1 < len && e + 1 < p.ecap)
                         lnext = __ldg(p.dl + size_t(e + 1) * n + k);
                     else if (e + 1 < len) {
@@ -509,6 +520,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
             const bool has_in = sg.blk > J.blk_base;                 // block does not start at row 0
             const bool has_next = sg.blk < J.blk_base + J.nblk - 1;  // a block below carries X
             const int so = stg_off(J.out, g0, n);
+            const int ktg = g0 < p.lt_need ? p.kt : p.kta, ktpg = g0 < p.lt_need ? p.ktp : p.ktpa;   // see phase 1
             trace(2, it, 0);
             const uint32_t gm = group_mask(rows);
 #pragma unroll 1
@@ -529,7 +541,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
             // back-substitution in place on the staged rows
             auto sweep3 = [&](int k, double &x, double &Pc, double yin, double ib_inf, double inl_, double iblast,
                               int len) {
-                if (k < p.kt) {
+                if (k < ktg) {
                     const double *tb = lts + k;
 #pragma unroll 4
                     for (int rr = rows - 1; rr >= 0; --rr) {
@@ -537,9 +549,9 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
                         double y = *yp;
                         if (has_in) {
                             y = fma(Pc, yin, y);
-                            Pc *= tb[rr * 3 * p.ktp + 2 * p.ktp];   // P_{i-1} = -P_i beta_{i-1} / delta
+                            Pc *= tb[rr * 3 * ktpg + 2 * ktpg];   // P_{i-1} = -P_i beta_{i-1} / delta
                         }
-                        x = __dsub_rn(y, __dmul_rn(off, x)) * tb[rr * 3 * p.ktp + p.ktp];   // rectsolver.py:90
+                        x = __dsub_rn(y, __dmul_rn(off, x)) * tb[rr * 3 * ktpg + ktpg];   // rectsolver.py:90
                         *yp = x;
                     }
                 } else if (g0 < len && g0 + rows <= p.ecap) {
