@@ -456,22 +456,45 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
             __syncthreads();
             trace(12, item / gridDim.x, 1);
             if (tid < w) {
+                // eight blocks of coefficients are read ahead of each stretch of the
+                // dependent chain (the stores in between would otherwise order every
+                // load behind the previous link)
                 double *c = sv + tid;
                 double Y = 0.0;
-#pragma unroll 4
-                for (int b = 0; b < nb; ++b) {
-                    const double A = (b == 0) ? 0.0 : c[(b * 7 + 2) * W];
-                    Y = fma(A, Y, c[(b * 7 + 0) * W]);
-                    c[(b * 7 + 5) * W] = Y;
+#pragma unroll 1
+                for (int b0 = 0; b0 < nb; b0 += 8) {
+                    double A[8], B[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int b = min(b0 + q, nb - 1);
+                        A[q] = c[(b * 7 + 2) * W];
+                        B[q] = c[(b * 7 + 0) * W];
+                    }
+                    if (b0 == 0) A[0] = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (b0 + q < nb) {
+                            Y = fma(A[q], Y, B[q]);
+                            c[((b0 + q) * 7 + 5) * W] = Y;
+                        }
                 }
                 double X = 0.0;
-#pragma unroll 4
-                for (int b = nb - 1; b >= 0; --b) {
-                    double B = c[(b * 7 + 1) * W];
-                    if (b > 0) B = fma(c[((b - 1) * 7 + 5) * W], c[(b * 7 + 3) * W], B);
-                    const double A = (b < nb - 1) ? c[(b * 7 + 4) * W] : 0.0;
-                    X = fma(A, X, B);
-                    c[(b * 7 + 6) * W] = X;
+#pragma unroll 1
+                for (int b1 = nb - 1; b1 >= 0; b1 -= 8) {
+                    double A[8], B[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int b = max(b1 - q, 0);
+                        B[q] = c[(b * 7 + 1) * W];
+                        if (b > 0) B[q] = fma(c[((b - 1) * 7 + 5) * W], c[(b * 7 + 3) * W], B[q]);
+                        A[q] = (b < nb - 1) ? c[(b * 7 + 4) * W] : 0.0;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (b1 - q >= 0) {
+                            X = fma(A[q], X, B[q]);
+                            c[((b1 - q) * 7 + 6) * W] = X;
+                        }
                 }
             }
             trace(13, item / gridDim.x, 0);
