@@ -134,6 +134,18 @@ class TestPersistentGeometry:
         p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f)
         assert rel(p.values, O.solve(O.plan(sub), f)) < 1e-12
 
+    @pytest.mark.parametrize("n", [1023, 2047])
+    @pytest.mark.parametrize("kappa", [-3.0e5, -1.0e7, -1.0e9])
+    def test_slow_mode_table_widths(self, n, kappa, rng):
+        """Strong shifts shrink the set of slowly converging modes: fewer than one
+        warp's 32 (narrow table only), or none (no table); the row where the wide
+        table hands over to the narrow one moves with it."""
+        m = 700
+        sub = make((m, n, 1.0 / n, 1.0 / n, kappa, "DDDD", ()))
+        f = rng.uniform(-1, 1, m * n)
+        p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f)
+        assert rel(p.values, O.solve(O.plan(sub), f)) < 1e-12
+
     @pytest.mark.parametrize("n", [511, 1023, 2047])
     def test_mixed_batch(self, n, rng):
         ms = [7, 300, 1, 64, 513]
