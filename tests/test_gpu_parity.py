@@ -146,7 +146,7 @@ class TestPersistentGeometry:
         p = rectsolver.solve_rect(rectsolver.plan_rect(sub), f)
         assert rel(p.values, O.solve(O.plan(sub), f)) < 1e-12
 
-    @pytest.mark.parametrize("n", [511, 1023, 2047])
+    @pytest.mark.parametrize("n", [511, 1023, 2047, 4095])
     def test_mixed_batch(self, n, rng):
         ms = [7, 300, 1, 64, 513]
         subs = [make((m, n, 1.0 / n, 1.0 / n, k, "DDDD", ("west",) if i % 2 else ()), sid=i)
