@@ -42,7 +42,7 @@
 namespace fd {
 
 template <int NL>
-__global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(const __grid_constant__ PList pl) {
+__global__ void __launch_bounds__(RS<NL>::NT, RS<NL>::NT <= 256 ? 2 : 1) rsolve_kernel(const __grid_constant__ PList pl) {
     using C = RS<NL>;
     using F = RFft<NL>;
     constexpr int NT = C::NT, G = C::G, P = C::P, T = C::T, MPT = C::MPT, XR = C::XR;
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(RS<NL>::NT, 512 / RS<NL>::NT) rsolve_kernel(co
     uint32_t tm = 0;   // this thread's slots: lane quarter of its warp, 128 columns per warp
     if constexpr (kTm) {
         tmem_fence_after();
-        tm = tmem_base_s + ((uint32_t(tid >> 5) & 3u) << 21) + (uint32_t(tid >> 7) << 7);
+        tm = tmem_base_s + ((uint32_t(tid >> 5) & 3u) << 21) + uint32_t(tid >> 7) * uint32_t(16 * MPT);
     }
     const int nseg = nseg_s, nitems = nitems_s;
     uint32_t ppar = 0, ltpar = 0;
