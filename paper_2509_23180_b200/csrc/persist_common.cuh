@@ -372,6 +372,11 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
                     fprintf(stderr, "  median %.1f\n", d[d.size() / 2].first);
                 }
             }
+            if (getenv("FD_PHASE_TIMING_ALL")) {   // every CTA: SM id, row range, phase-1 and phase-3 durations
+                for (int c = 0; c < grid; ++c)
+                    fprintf(stderr, "  cta %3d sm %3llu [%d,%d) p1 %.1f p3 %.1f\n", c, h[8 * c + 6], pl.vstart[c],
+                            pl.vstart[c + 1], (h[8 * c + 1] - h[8 * c]) * 1e-3, (h[8 * c + 5] - h[8 * c + 4]) * 1e-3);
+            }
             fprintf(stderr, "[fd phase us] start %.1f-%.1f p1end %.1f-%.1f sync1 %.1f-%.1f p2end %.1f-%.1f sync2 %.1f-%.1f end %.1f-%.1f (grid %d, V %d, rows %lld)\n",
                     mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[3], mx[3], mn[4], mx[4], mn[5], mx[5], grid, pl.V, total);
         }

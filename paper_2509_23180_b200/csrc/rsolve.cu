@@ -84,6 +84,11 @@ __global__ void __launch_bounds__(RS<NL>::NT, RS<NL>::NT <= 256 ? 2 : 1) rsolve_
         }
     };
     stamp(0);
+    if (pl.tstamp && tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        pl.tstamp[blockIdx.x * 8 + 6] = smid;
+    }
 
     if (tid == 0) {
         int ns = 0, items = 0;
