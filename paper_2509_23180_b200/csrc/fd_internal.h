@@ -127,8 +127,12 @@ constexpr size_t rs_fixed_smem(int N) {
     return size_t(rs_pairs(N)) * size_t(N + N / 16) * 16 + 272 * 16 + size_t(N) * 8 +
            size_t(rs_pairs(N)) * 16 * 8;
 }
+#ifndef FD_KT_CAP_MAX
+#define FD_KT_CAP_MAX (1 << 20)   // test builds lower it to drive modes onto the capped-table paths
+#endif
 constexpr int rs_kt_cap(int N) {
-    return int((rs_smem(N) - rs_fixed_smem(N)) / (24 * size_t(rs_rows_per_group(N)))) & ~1;
+    const int cap = int((rs_smem(N) - rs_fixed_smem(N)) / (24 * size_t(rs_rows_per_group(N)))) & ~1;
+    return cap < FD_KT_CAP_MAX ? cap : FD_KT_CAP_MAX;
 }
 inline bool rs_supported(int n) {
     const int N = n + 1;
