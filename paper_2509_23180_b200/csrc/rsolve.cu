@@ -1,8 +1,8 @@
 // Persistent fused rectangle solve with a real-symmetric DST-I
-// (n + 1 = N = 2^NL, 256 <= N <= 2048).
+// (n + 1 = N = 2^NL, 256 <= N <= 4096).
 //
-// Same three phases as persist.cu (DST + local forward elimination | block
-// carries | back-substitution + inverse DST), but the transform of a row pair
+// Three phases in one cooperative launch (DST + local forward elimination |
+// block carries | back-substitution + inverse DST); the transform of a row pair
 // is ONE N-point complex FFT instead of a 2N-point FFT of the odd extension:
 //
 //   y_j = alpha_j x_j + (alpha_j - s/2) x_{N-j},  alpha_j = s/2 sin(pi j/N) + s/4
@@ -14,14 +14,21 @@
 // k, done per pair with a serial/warp-shuffle/cross-warp scan).  This halves the
 // fp64 work of the transform, which bounds the complex-FFT kernel.
 //
-// Shared memory per CTA (one CTA of 512 threads per SM):
+// One CTA per SM (512 threads; 576 = nine row pairs at N = 1024, see fd_internal.h).
+// Shared memory:
 //   P pair regions of (N + N/16) complex: a row pair is TMA-copied into its
 //   region (unpadded, at offset so in {0,1}), transformed in place (padded
 //   Stockham radix-16 passes, pad16(q) = q + q/16), and the transformed rows
 //   are written back padded (xi(q) = q + q/16) for the mode-parallel Thomas
 //   sweep; phase 3 runs the sweep in place on the staged yhat rows first.
 //   Every pair has its own mbarrier, so a pair starts transforming as soon as
-//   its rows have landed.
+//   its rows have landed.  The rest holds the transform tables and one group's
+//   slice of the slow-mode factor tables (wide before PlanDev::lt_need, one
+//   warp's 32 modes after it).
+// Tensor memory (N >= 1024): the CTA owns the SM's 512 columns; every thread
+//   keeps the recurrence state and fixed-point factors of each of its modes in a
+//   16-column slot of its lane (tcgen05.ld/st), so the sweeps hold nothing in
+//   registers across the transforms and their body exists once per kernel.
 #include "rsolve_common.cuh"
 
 // FD_DIAG=1 (build flag) compiles in the per-item trace and the FD_DBG
