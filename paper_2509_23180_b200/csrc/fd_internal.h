@@ -119,7 +119,12 @@ constexpr size_t kRsSmem = 227 * 1024 - 2048;
 #endif
 // N = 1024: optionally 9 row pairs per CTA (576 threads, 112 registers), so that a CTA's
 // ~35 rows of the c1 batch are two groups of 18 instead of 16 + 16 + 3
-constexpr int rs_threads(int N) { return N <= FD_RS_SMALL_N ? 256 : (N == 1024 ? FD_RS1024_NT : kRsThreads); }
+#ifndef FD_RS2048_NT
+#define FD_RS2048_NT 512
+#endif
+constexpr int rs_threads(int N) {
+    return N <= FD_RS_SMALL_N ? 256 : (N == 1024 ? FD_RS1024_NT : N == 2048 ? FD_RS2048_NT : kRsThreads);
+}
 constexpr size_t rs_smem(int N) { return rs_threads(N) == 256 ? size_t(110) * 1024 : kRsSmem; }
 constexpr int rs_pairs(int N) { return rs_threads(N) / (N / 16); }
 constexpr int rs_rows_per_group(int N) { return 2 * rs_pairs(N); }

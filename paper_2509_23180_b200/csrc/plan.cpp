@@ -347,6 +347,9 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
 // rows); below it only the first kLtNarrow modes (one warp of the sweeps) are
 // still in their transient, and the narrow table [m][3][ktpa] holds just those.
 constexpr int kLongTransient = 48;
+#ifndef FD_ECAP
+#define FD_ECAP 128   // rows of every mode kept in the row-major transient tables
+#endif
 static void build_long_table(HostTables &T, int m, int n, double off, int kt_cap) {
     int kt = 0;
     for (int k = 0; k < n; ++k)
@@ -518,7 +521,7 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         }
         d.mode = upload(p, rec);
         // row-major copies of the first ecap rows (the transient region of most modes)
-        d.ecap = std::min(m, 128);
+        d.ecap = std::min(m, FD_ECAP);
         std::vector<double> dl(size_t(d.ecap) * n), dib(size_t(d.ecap) * n), db(size_t(d.ecap) * n);
         parallel_for(d.ecap, [&](int i0, int i1) {
             for (int i = i0; i < i1; ++i)
