@@ -223,6 +223,9 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
         {
             static const double tau1 = getenv("FD_TAU1") ? atof(getenv("FD_TAU1")) : 1.2;
             static const double tau0 = getenv("FD_TAU0") ? atof(getenv("FD_TAU0")) : 4.0;
+            // a row with any sizeable set of modes in their transient pays the divergent
+            // transient path in every warp that holds one of them (step term)
+            static const double tau2 = getenv("FD_TAU2") ? atof(getenv("FD_TAU2")) : 0.0;
             struct JW {
                 long long r0;
                 int m, t;
@@ -241,7 +244,8 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
                 q.start = W;
                 q.pre.assign(q.t + 1, 0.0);
                 for (int i = 0; i < q.t; ++i)
-                    q.pre[i + 1] = q.pre[i] + 1.0 + tau1 * sj.tprof[i] + (i == 0 ? tau0 : 0.0);
+                    q.pre[i + 1] = q.pre[i] + 1.0 + tau1 * sj.tprof[i] + (sj.tprof[i] > 0.02f ? tau2 : 0.0) +
+                                   (i == 0 ? tau0 : 0.0);
                 const double wj = (q.t > 0 ? q.pre[q.t] : tau0) + double(q.m - q.t);
                 W += wj;
                 r0 += q.m;
@@ -259,11 +263,12 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
                 return q.r0 + std::min<long long>(q.m, q.t + (long long)std::ceil(x));
             };
             pl.vstart[0] = 0;
+            static const long long snap = getenv("FD_SNAP") ? atoll(getenv("FD_SNAP")) : 3;
             for (long long v = 1; v < V; ++v) {
                 long long r = row_at(W * double(v) / double(V));
                 // snap to a subdomain start within 3 rows: no tiny extra segment
                 for (int j = 1; j < pl.count; ++j)
-                    if (std::llabs(r - jw[j].r0) <= 3) r = jw[j].r0;
+                    if (std::llabs(r - jw[j].r0) <= snap) r = jw[j].r0;
                 r = std::max<long long>(r, pl.vstart[v - 1] + 1);             // non-empty ranges
                 r = std::min<long long>(r, total - (V - v));
                 pl.vstart[v] = (int)r;
