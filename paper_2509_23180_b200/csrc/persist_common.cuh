@@ -225,7 +225,7 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
             static const double tau0 = getenv("FD_TAU0") ? atof(getenv("FD_TAU0")) : 4.0;
             // a row with any sizeable set of modes in their transient pays the divergent
             // transient path in every warp that holds one of them (step term)
-            static const double tau2 = getenv("FD_TAU2") ? atof(getenv("FD_TAU2")) : 0.0;
+            static const double tau2 = getenv("FD_TAU2") ? atof(getenv("FD_TAU2")) : 0.3;
             struct JW {
                 long long r0;
                 int m, t;
