@@ -115,11 +115,10 @@ constexpr size_t kRsSmem = 227 * 1024 - 2048;
 // N <= FD_RS_SMALL_N: two CTAs of 256 threads per SM (one CTA's barriers and
 // copy waits overlap the other's transforms); larger N: one CTA of 512.
 #ifndef FD_RS1024_NT
-#define FD_RS1024_NT 512
+#define FD_RS1024_NT 576
 #endif
-// N = 1024: 576 = nine row pairs per CTA (96 registers; a CTA's ~35 rows of the c1 batch are
-// two groups of 18 instead of 16 + 16 + 3) is 3 % faster but WRONG under some row partitions
-// (tools/dbg_loop.sh, DESIGN 3.1): experimental builds only
+// N = 1024: nine row pairs per CTA (576 threads, 96 registers), so that a CTA's ~35 rows of
+// the c1 batch are two groups of 18 instead of 16 + 16 + 3
 #ifndef FD_RS2048_NT
 #define FD_RS2048_NT 512
 #endif

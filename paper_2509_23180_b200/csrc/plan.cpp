@@ -343,14 +343,14 @@ static HostTables build_tables(int m, int n, double dx, double dy, double kappa,
 // Row-major factor tables of the slowly converging lowest modes (persistent
 // kernel): modes k < kt whose fixed point is >= kLongTransient rows away.  Two
 // tables: the wide one [lt_rows][3][ktp] holds all kt modes down to the row
-// where every mode >= kLtNarrow has reached its fixed point (+ one group of
-// rows); below it only the first kLtNarrow modes (one warp of the sweeps) are
+// where every mode >= kLtNarrow has reached its fixed point (+ one row group
+// of the kernel); below it only the first kLtNarrow modes (one warp of the sweeps) are
 // still in their transient, and the narrow table [m][3][ktpa] holds just those.
 constexpr int kLongTransient = 48;
 #ifndef FD_ECAP
 #define FD_ECAP 128   // rows of every mode kept in the row-major transient tables
 #endif
-static void build_long_table(HostTables &T, int m, int n, double off, int kt_cap) {
+static void build_long_table(HostTables &T, int m, int n, double off, int kt_cap, int group_rows) {
     int kt = 0;
     for (int k = 0; k < n; ++k)
         if (T.fix[k] >= kLongTransient) kt = k + 1;
@@ -361,7 +361,8 @@ static void build_long_table(HostTables &T, int m, int n, double off, int kt_cap
     T.ktpa = (T.kta + 1) & ~1;
     T.lt_need = 0;
     for (int k = kLtNarrow; k < kt; ++k) T.lt_need = std::max(T.lt_need, std::min(T.fix[k], m));
-    T.lt_rows = kt > kLtNarrow ? std::min(m, T.lt_need + 16) : 0;
+    // a group that starts before lt_need reads all its rows from the wide table
+    T.lt_rows = kt > kLtNarrow ? std::min(m, T.lt_need + group_rows) : 0;
     if (kt == 0) return;
     auto fill = [&](std::vector<double> &tab, int rows, int cnt, int pitch) {
         tab.assign(size_t(rows) * 3 * pitch, 0.0);
@@ -537,7 +538,7 @@ static Plan *build_proto(int m, int n, double dx, double dy, double kappa, doubl
         d.dib = upload(p, dib);
         d.db = upload(p, db);
         if (tk == kFFT) {
-            build_long_table(T, m, n, d.off, rs_kt_cap(n + 1));
+            build_long_table(T, m, n, d.off, rs_kt_cap(n + 1), rs_rows_per_group(n + 1));
         }
         d.kt = T.kt;
         d.ktp = T.ktp;

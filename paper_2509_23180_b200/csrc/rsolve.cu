@@ -14,7 +14,7 @@
 // k, done per pair with a serial/warp-shuffle/cross-warp scan).  This halves the
 // fp64 work of the transform, which bounds the complex-FFT kernel.
 //
-// One CTA per SM (512 threads).
+// One CTA per SM (512 threads; 576 = nine row pairs at N = 1024, see fd_internal.h).
 // Shared memory:
 //   P pair regions of (N + N/16) complex: a row pair is TMA-copied into its
 //   region (unpadded, at offset so in {0,1}), transformed in place (padded
