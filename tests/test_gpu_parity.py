@@ -160,15 +160,18 @@ class TestPersistentGeometry:
 class TestPartitionScan:
     """The fused solve under different row partitions of the same batch: the
     partition knobs (FD_TAU0 / FD_TAU2, read once per process) move every range
-    boundary; each setting runs 5 x 1023^2 against the oracle in its own process."""
+    boundary; each setting runs 5 x n^2 against the oracle in its own process.
+    (1023, 0.3, 3 / 4 / 8) are the partitions that exposed a slow-mode table read one
+    row past its end with 18-row groups.)"""
 
-    @pytest.mark.parametrize("tau2,tau0", [(0.0, 4.0), (0.3, 3.0), (0.3, 8.0), (0.6, 5.0)])
-    def test_c1_batch(self, tau2, tau0):
+    @pytest.mark.parametrize("n,tau2,tau0", [(1023, 0.0, 4.0), (1023, 0.3, 3.0), (1023, 0.3, 4.0), (1023, 0.3, 8.0),
+                                             (1023, 0.6, 5.0), (511, 0.3, 3.0), (2047, 0.3, 6.0)])
+    def test_c1_batch(self, n, tau2, tau0):
         import subprocess
         import sys
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         env = dict(os.environ, FD_TAU2=str(tau2), FD_TAU0=str(tau0))
-        r = subprocess.run([sys.executable, os.path.join(root, "tools", "dbg_tau.py"), "1023"], env=env,
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "dbg_tau.py"), str(n)], env=env,
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         assert "BAD []" in r.stdout, r.stdout[-500:]
