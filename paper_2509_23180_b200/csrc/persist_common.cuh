@@ -220,12 +220,19 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
         // Cost-balanced ranges: a row weighs 1 + tau1 * (fraction of modes in
         // their transient at that row); a subdomain's first row carries the
         // extra group/segment set-up (tau0 rows).
-        {
-            static const double tau1 = getenv("FD_TAU1") ? atof(getenv("FD_TAU1")) : 1.2;
-            static const double tau0 = getenv("FD_TAU0") ? atof(getenv("FD_TAU0")) : 4.0;
+        // Group quantisation: a range one row longer than a whole number of row groups
+        // pays a whole extra group in both phases.  When the average range fits k
+        // groups, the transient weights are backed off (x 2/3, 1/3, 0) until no range
+        // of one subdomain is longer than k groups.
+        const long long cap = ((total + V - 1) / V + K::G - 1) / K::G * K::G;
+        for (int attempt = 0; attempt < 4; ++attempt) {
+            static const double tau1_ = getenv("FD_TAU1") ? atof(getenv("FD_TAU1")) : 1.2;
+            static const double tau0_ = getenv("FD_TAU0") ? atof(getenv("FD_TAU0")) : 4.0;
             // a row with any sizeable set of modes in their transient pays the divergent
             // transient path in every warp that holds one of them (step term)
-            static const double tau2 = getenv("FD_TAU2") ? atof(getenv("FD_TAU2")) : 0.3;
+            static const double tau2_ = getenv("FD_TAU2") ? atof(getenv("FD_TAU2")) : 0.3;
+            const double back = double(3 - attempt) / 3.0;
+            const double tau1 = tau1_ * back, tau0 = tau0_ * back, tau2 = tau2_ * back;
             struct JW {
                 long long r0;
                 int m, t;
@@ -274,6 +281,15 @@ static void run_persist(const std::vector<SolveJob> &jobs, cudaStream_t s, Works
                 pl.vstart[v] = (int)r;
             }
             pl.vstart[V] = (int)total;
+            bool over = false;
+            for (long long v = 0; v < V && !over; ++v) {
+                if (pl.vstart[v + 1] - pl.vstart[v] <= cap) continue;
+                bool one_job = false;   // ranges across a subdomain start have their own group structure
+                for (int j = 0; j < pl.count; ++j)
+                    one_job = one_job || (pl.vstart[v] >= jw[j].r0 && pl.vstart[v + 1] <= jw[j].r0 + jw[j].m);
+                over = one_job;
+            }
+            if (!over) break;
         }
         auto lo = [&](long long v) { return (long long)pl.vstart[v]; };
         auto range_of = [&](long long r) {   // largest v with lo(v) <= r
